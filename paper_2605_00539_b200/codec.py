@@ -1,0 +1,258 @@
+"""L1 block codec on device tensors — Python mirror of the reference API in
+/root/reference/proj/include/agq/quantize.hpp and tensor_io.hpp, running the
+sm_100a kernels of libagq_cuda.so through the C ABI.
+
+`quantize_blockwise` / `dequantize_blockwise` keep the reference's names,
+argument meaning and exceptions (InvalidArgument == std::invalid_argument);
+tensors live in HBM. Codes are stored packed (LSB-first bitstream at
+`bit_width` bits, tensor_io.hpp:63-80) unless `packed=False` asks for the
+reference's one-byte-per-element layout.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import torch
+
+from . import _lib as L
+
+
+class CodecKind(enum.IntEnum):  # quantize.hpp:15-19
+    SymmetricLinear = 0
+    Fp4E2M1 = 1
+    Fp8E4M3 = 2
+
+
+kDefaultBlockSize = 128
+
+
+@dataclass
+class QuantizedTensor:  # quantize.hpp:40-50, device resident
+    codes: torch.Tensor
+    scales: torch.Tensor
+    bit_width: int
+    block_size: int = kDefaultBlockSize
+    shape: tuple = ()
+    codec_kind: CodecKind = CodecKind.SymmetricLinear
+    packed: bool = True
+
+    def num_elements(self) -> int:
+        n = 1
+        for d in self.shape:
+            n *= int(d)
+        return n
+
+    def num_blocks(self) -> int:
+        return int(self.scales.numel())
+
+    def nbytes(self) -> int:
+        return self.codes.numel() + 4 * self.scales.numel()
+
+
+def _stream(stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+class ErrorRecord:
+    """Device-resident agq_errors record; `raise_if_any` syncs the stream."""
+
+    def __init__(self, device):
+        self.t = torch.empty(C.sizeof(L.AgqErrors), dtype=torch.uint8, device=device)
+
+    @property
+    def ptr(self) -> int:
+        return self.t.data_ptr()
+
+    def reset(self, stream=None):
+        L.check(L.lib.agq_errors_reset(self.ptr, _stream(stream)))
+        return self
+
+    def read(self) -> L.AgqErrors:
+        raw = bytes(self.t.cpu().numpy().tobytes())
+        return L.AgqErrors.from_buffer_copy(raw)
+
+    def raise_if_any(self, op: int) -> L.AgqErrors:
+        h = self.read()
+        L.errors_message(h, op)
+        return h
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return L.AGQ_BF16
+    if t.dtype == torch.float32:
+        return L.AGQ_F32
+    raise L.InvalidArgument(f"unsupported input dtype {t.dtype} (float32 or bfloat16)")
+
+
+def _require_cuda(t: torch.Tensor, what: str):
+    if not t.is_cuda:
+        raise L.InvalidArgument(f"{what} must be a CUDA tensor (no CPU path)")
+    if not t.is_contiguous():
+        raise L.InvalidArgument(f"{what} must be contiguous")
+
+
+def check_codec_args(bit_width: int, block_size: int, kind: CodecKind) -> None:
+    L.check(L.lib.agq_check_codec_args(int(bit_width), int(block_size), int(kind)))
+
+
+def quantize_blockwise(x: torch.Tensor, bit_width: int, block_size: int = kDefaultBlockSize,
+                       kind: CodecKind = CodecKind.SymmetricLinear, shape: Sequence[int] = (),
+                       packed: bool = True, stream=None, check: bool = True,
+                       errors: ErrorRecord | None = None) -> QuantizedTensor:
+    """quantize.hpp:78-138 (+ pack_codes when packed). x: float32/bfloat16 CUDA."""
+    check_codec_args(bit_width, block_size, kind)
+    _require_cuda(x, "x")
+    shape = tuple(int(d) for d in shape) if shape else (int(x.numel()),)
+    n = 1
+    for d in shape:
+        n *= d
+    if n != x.numel():
+        raise L.InvalidArgument("shape does not match element count")
+    nb = int(L.lib.agq_num_blocks(n, block_size))
+    ncode = int(L.lib.agq_packed_bytes(n, bit_width)) if packed else n
+    codes = torch.empty(ncode, dtype=torch.uint8, device=x.device)
+    scales = torch.empty(nb, dtype=torch.float32, device=x.device)
+    err = errors if errors is not None else (ErrorRecord(x.device) if check else None)
+    s = _stream(stream)
+    if err is not None:
+        err.reset(stream)
+    L.check(L.lib.agq_quantize(x.data_ptr(), _dtype_code(x), n, bit_width, block_size, int(kind),
+                               codes.data_ptr(), L.AGQ_CODES_PACKED if packed else L.AGQ_CODES_BYTES,
+                               scales.data_ptr(), err.ptr if err is not None else None, s))
+    if check and err is not None:
+        err.raise_if_any(L.AGQ_OP_QUANTIZE)
+    return QuantizedTensor(codes, scales, bit_width, block_size, shape, CodecKind(kind), packed)
+
+
+def validate(q: QuantizedTensor) -> None:
+    """quantize.hpp:157-176 (argument/shape part; data checks run on device)."""
+    check_codec_args(q.bit_width, q.block_size, q.codec_kind)
+    n = q.num_elements()
+    if q.scales.numel() != int(L.lib.agq_num_blocks(n, q.block_size)):
+        raise L.InvalidArgument("quantized tensor: wrong number of scales")
+    expect = int(L.lib.agq_packed_bytes(n, q.bit_width)) if q.packed else n
+    if q.codes.numel() != expect:
+        raise L.InvalidArgument("quantized tensor: shape/code count mismatch")
+
+
+def dequantize_blockwise(q: QuantizedTensor, out_dtype: torch.dtype = torch.float32,
+                         stream=None, check: bool = True, out: torch.Tensor | None = None,
+                         errors: ErrorRecord | None = None) -> torch.Tensor:
+    """quantize.hpp:178-189. float32 output is bit-identical to the reference;
+    bfloat16 output is its round-to-nearest-even."""
+    validate(q)
+    n = q.num_elements()
+    if out is None:
+        out = torch.empty(n, dtype=out_dtype, device=q.codes.device)
+    err = errors if errors is not None else (ErrorRecord(q.codes.device) if check else None)
+    s = _stream(stream)
+    if err is not None:
+        err.reset(stream)
+    L.check(L.lib.agq_dequantize(q.codes.data_ptr(),
+                                 L.AGQ_CODES_PACKED if q.packed else L.AGQ_CODES_BYTES,
+                                 q.scales.data_ptr(), n, q.bit_width, q.block_size,
+                                 int(q.codec_kind), out.data_ptr(), _dtype_code(out),
+                                 1 if err is not None else 0,
+                                 err.ptr if err is not None else None, s))
+    if check and err is not None:
+        err.raise_if_any(L.AGQ_OP_DEQUANTIZE)
+    return out.view(q.shape) if len(q.shape) > 1 else out
+
+
+def code_unit_value(kind: CodecKind, bit_width: int, code: int) -> float:
+    """quantize.hpp:142-155 (host scalar)."""
+    if kind == CodecKind.SymmetricLinear:
+        lv = (1 << (bit_width - 1)) - 1
+        return (int(code) - lv) / lv
+    if kind == CodecKind.Fp4E2M1:
+        mag = (0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0)[code & 7]
+        return (-mag if code & 8 else mag) / 6.0
+    from .scalar import fp8_decode
+    return fp8_decode(code) / 448.0
+
+
+def pack_codes(codes: torch.Tensor, bit_width: int, stream=None) -> torch.Tensor:
+    """tensor_io.hpp:63-80 on device."""
+    _require_cuda(codes, "codes")
+    n = codes.numel()
+    out = torch.empty(int(L.lib.agq_packed_bytes(n, bit_width)), dtype=torch.uint8,
+                      device=codes.device)
+    L.check(L.lib.agq_pack_codes(codes.data_ptr(), n, bit_width, out.data_ptr(), _stream(stream)))
+    return out
+
+
+def unpack_codes(packed: torch.Tensor, bit_width: int, count: int, stream=None) -> torch.Tensor:
+    """tensor_io.hpp:82-100 on device."""
+    _require_cuda(packed, "packed")
+    if packed.numel() < int(L.lib.agq_packed_bytes(count, bit_width)):
+        raise L.ProtocolError("tensor dump: packed codes truncated")
+    out = torch.empty(count, dtype=torch.uint8, device=packed.device)
+    L.check(L.lib.agq_unpack_codes(packed.data_ptr(), count, bit_width, out.data_ptr(),
+                                   _stream(stream)))
+    return out
+
+
+def quantize_grouped(xs: Sequence[torch.Tensor], bit_width: int,
+                     kind: CodecKind = CodecKind.SymmetricLinear, stream=None,
+                     check: bool = True, errors: ErrorRecord | None = None,
+                     outs: Sequence[QuantizedTensor] | None = None) -> list[QuantizedTensor]:
+    """One launch over all tensors a pipeline stage stores (block 128, packed)."""
+    if not xs:
+        return []
+    dt = _dtype_code(xs[0])
+    qs = list(outs) if outs is not None else []
+    segs = (L.AgqSegment * len(xs))()
+    for i, x in enumerate(xs):
+        _require_cuda(x, "x")
+        if _dtype_code(x) != dt:
+            raise L.InvalidArgument("grouped tensors must share a dtype")
+        n = x.numel()
+        if outs is None:
+            q = QuantizedTensor(
+                torch.empty(int(L.lib.agq_packed_bytes(n, bit_width)), dtype=torch.uint8,
+                            device=x.device),
+                torch.empty(int(L.lib.agq_num_blocks(n, 128)), dtype=torch.float32, device=x.device),
+                bit_width, 128, tuple(x.shape), CodecKind(kind), True)
+            qs.append(q)
+        q = qs[i]
+        segs[i] = L.AgqSegment(x.data_ptr(), q.codes.data_ptr(), q.scales.data_ptr(), n)
+    err = errors if errors is not None else (ErrorRecord(xs[0].device) if check else None)
+    if err is not None:
+        err.reset(stream)
+    L.check(L.lib.agq_quantize_grouped(segs, len(xs), dt, bit_width, int(kind),
+                                       err.ptr if err is not None else None, _stream(stream)))
+    if check and err is not None:
+        err.raise_if_any(L.AGQ_OP_QUANTIZE)
+    return qs
+
+
+def dequantize_grouped(qs: Sequence[QuantizedTensor], out_dtype: torch.dtype = torch.bfloat16,
+                       stream=None, outs: Sequence[torch.Tensor] | None = None) -> list[torch.Tensor]:
+    if not qs:
+        return []
+    res = list(outs) if outs is not None else [
+        torch.empty(q.shape, dtype=out_dtype, device=q.codes.device) for q in qs]
+    segs = (L.AgqSegment * len(qs))()
+    for i, q in enumerate(qs):
+        if q.bit_width != qs[0].bit_width or q.codec_kind != qs[0].codec_kind or not q.packed:
+            raise L.InvalidArgument("grouped tensors must share bits/codec and be packed")
+        segs[i] = L.AgqSegment(res[i].data_ptr(), q.codes.data_ptr(), q.scales.data_ptr(),
+                               q.num_elements())
+    L.check(L.lib.agq_dequantize_grouped(segs, len(qs), _dtype_code(res[0]), qs[0].bit_width,
+                                         int(qs[0].codec_kind), _stream(stream)))
+    return res
+
+
+def roundtrip_relative_delta(x: torch.Tensor, bit_width: int, block_size: int = kDefaultBlockSize,
+                             kind: CodecKind = CodecKind.SymmetricLinear) -> torch.Tensor:
+    """quantize.hpp:193-206: x_hat = x (1 + delta); zero elements get 0."""
+    q = quantize_blockwise(x, bit_width, block_size, kind)
+    back = dequantize_blockwise(q).reshape(-1).double()
+    xd = x.reshape(-1).double()
+    delta = torch.where(xd == 0, torch.zeros_like(xd), (back - xd) / xd)
+    return delta

@@ -1,0 +1,116 @@
+"""Decomposed 8-bit all-reduce across real ranks (one process per GPU).
+
+Replaces allreduce_decomposed (collective.hpp:226-333) when the workers are
+GPUs of one NVLink/NVSwitch box. torch.distributed is only the plumbing that
+carries the NCCL unique id and the CUDA IPC handles between processes; the
+data path is libagq_cuda.so (NCCL grouped send/recv + the reduce-requant
+kernel, or the fused NVLink peer-memory kernel).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib as L
+from .codec import CodecKind, ErrorRecord, QuantizedTensor, _stream
+
+
+class _CudaArray:
+    """Zero-copy view of raw device memory for torch.as_tensor."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+class Communicator:
+    ALGOS = {"nccl": L.AGQ_AR_NCCL, "p2p": L.AGQ_AR_FUSED_P2P}
+
+    def __init__(self, group=None, device: int | None = None, p2p_capacity: int = 0):
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device = torch.cuda.current_device() if device is None else device
+        uid = C.create_string_buffer(128)
+        if self.rank == 0:
+            L.check(L.lib.agq_comm_unique_id(uid))
+        t = torch.frombuffer(bytearray(uid.raw), dtype=torch.uint8).clone()
+        t = self._bcast_bytes(t, group)
+        uid = C.create_string_buffer(bytes(t.tolist()), 128)
+        self._h = C.c_void_p()
+        L.check(L.lib.agq_comm_init(C.byref(self._h), uid, self.world, self.rank, self.device))
+        self._group = group
+        self.p2p_capacity = 0
+        if p2p_capacity:
+            self.enable_p2p(p2p_capacity)
+
+    @staticmethod
+    def _bcast_bytes(t: torch.Tensor, group):
+        import torch.distributed as dist
+        if dist.get_backend(group) == "nccl":
+            d = t.cuda()
+            dist.broadcast(d, 0, group=group)
+            return d.cpu()
+        dist.broadcast(t, 0, group=group)
+        return t
+
+    def enable_p2p(self, capacity: int):
+        """Allocate + IPC-export this rank's symmetric FP8 buffer, open all
+        peers' (collective over the group)."""
+        import torch.distributed as dist
+        h = C.create_string_buffer(256)
+        L.check(L.lib.agq_comm_p2p_export(self._h, int(capacity), h))
+        mine = torch.frombuffer(bytearray(h.raw), dtype=torch.uint8).clone()
+        if dist.get_backend(self._group) == "nccl":
+            outs = [torch.empty(256, dtype=torch.uint8, device="cuda") for _ in range(self.world)]
+            dist.all_gather(outs, mine.cuda(), group=self._group)
+            outs = [o.cpu() for o in outs]
+        else:
+            outs = [torch.empty(256, dtype=torch.uint8) for _ in range(self.world)]
+            dist.all_gather(outs, mine, group=self._group)
+        blob = b"".join(bytes(o.tolist()) for o in outs)
+        L.check(L.lib.agq_comm_p2p_open(self._h, C.create_string_buffer(blob, len(blob))))
+        self.p2p_capacity = int(capacity)
+
+    def p2p_buffers(self, n: int):
+        """(codes, scales) torch views of this rank's symmetric buffer for an
+        n-element gradient; all-reducing these runs fully in place."""
+        c, s = C.c_void_p(), C.c_void_p()
+        L.check(L.lib.agq_comm_p2p_buffers(self._h, C.byref(c), C.byref(s)))
+        nb = (n + 127) // 128
+        codes = torch.as_tensor(_CudaArray(c.value, n, "|u1"), device=f"cuda:{self.device}")
+        scales = torch.as_tensor(_CudaArray(s.value, nb, "<f4"), device=f"cuda:{self.device}")
+        return codes, scales
+
+    def allreduce_fp8(self, q: QuantizedTensor, algo: str = "nccl", stream=None,
+                      check: bool = True, errors: ErrorRecord | None = None) -> QuantizedTensor:
+        """In place on this rank's FP8 gradient (one byte per code)."""
+        if q.codec_kind != CodecKind.Fp8E4M3:
+            raise L.InvalidArgument("worker gradients are FP8 E4M3 tensors")
+        err = errors if errors is not None else ErrorRecord(q.codes.device)
+        err.reset(stream)
+        L.check(L.lib.agq_allreduce_fp8(self._h, q.codes.data_ptr(), q.scales.data_ptr(),
+                                        q.num_elements(), q.block_size, self.ALGOS[algo], err.ptr,
+                                        _stream(stream)))
+        if check:
+            err.raise_if_any(L.AGQ_OP_ALLREDUCE)
+        return q
+
+    def allreduce_bf16(self, t: torch.Tensor, stream=None) -> torch.Tensor:
+        """Baseline: ncclAllReduce(bf16, sum) in place."""
+        if t.dtype != torch.bfloat16:
+            raise L.InvalidArgument("baseline expects bfloat16")
+        L.check(L.lib.agq_allreduce_bf16_nccl(self._h, t.data_ptr(), t.numel(), _stream(stream)))
+        return t
+
+    def close(self):
+        if self._h:
+            L.lib.agq_comm_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

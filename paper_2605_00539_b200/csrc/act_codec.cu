@@ -1,0 +1,848 @@
+// L1 block codec on sm_100a: block-absmax quantize + LSB-first packing (K1)
+// and unpack + dequantize (K2).
+//
+// Reference: /root/reference/proj/include/agq/quantize.hpp:78-189 and
+// tensor_io.hpp:63-100. Results are bit-identical to quantize_blockwise /
+// dequantize_blockwise + pack_codes (tests/test_gpu_codec.py).
+//
+// Fast path (block 128, 16-byte aligned buffers, full 8192-element tiles):
+// persistent CTAs stream tiles through a STAGES-deep ring of shared-memory
+// buffers filled by 1-D TMA bulk copies (cp.async.bulk + mbarrier) and drain
+// packed codes / scales / outputs back with bulk stores. Each thread owns 32
+// consecutive elements (4 threads per 128-element block): two shuffles give
+// the block absmax and a thread's 32 codes are exactly `bits` 32-bit words of
+// the packed stream. The shared-memory rows are read in a per-thread rotated
+// chunk order (bank-conflict free) and put back in order with selects.
+//
+// Generic path (any block size / alignment / the tail after the last full
+// tile): warp-per-block absmax, thread-per-output-byte encode+pack and
+// thread-per-element decode, same element functions (agq_numerics.cuh).
+#include <utility>
+
+#include "agq_common.cuh"
+
+namespace agqk {
+
+template <int CB, int NW, int NC, int... J>
+__device__ __forceinline__ void pack_chunks(uint32_t (&w)[NW], const uint64_t (&pk)[NC],
+                                            std::integer_sequence<int, J...>) {
+  (or_bits<J * CB, NW>(w, pk[J]), ...);
+}
+template <int CB, int NW, int NC, int... J>
+__device__ __forceinline__ void unpack_chunks(const uint32_t (&w)[NW], uint64_t (&pk)[NC],
+                                              std::integer_sequence<int, J...>) {
+  ((pk[J] = get_bits<J * CB, CB, NW>(w)), ...);
+}
+
+// ---------------------------------------------------------------------------
+// K1: quantize
+// ---------------------------------------------------------------------------
+template <typename Tin>
+struct InTraits;
+template <>
+struct InTraits<__nv_bfloat16> {
+  static constexpr int kChunks = 4;  // 16-byte chunks per thread row
+  static constexpr int kStages = 4;
+  static constexpr bool kBf16 = true;
+};
+template <>
+struct InTraits<float> {
+  static constexpr int kChunks = 8;
+  static constexpr int kStages = 3;
+  static constexpr bool kBf16 = false;
+};
+
+template <int BITS, int CODEC, bool BF16IN>
+__device__ __forceinline__ uint32_t encode_one(float x, float a, float inv,
+                                               float rcp, bool fast) {
+  if (CODEC == 0) {
+    constexpr int L = (1 << (BITS - 1)) - 1;
+    if (fast) {
+      if (BF16IN) return (uint32_t)(linear_k_bf16(x, a, inv, rcp, (float)L) + L);
+      return (uint32_t)(linear_k_f32(x, a, inv, (float)L) + L);
+    }
+    return encode_double(0, BITS, x, a);
+  } else if (CODEC == 1) {
+    return fast ? fp4_code(x, a) : encode_double(1, 4, x, a);
+  } else {
+    return fast ? fp8_code(x, a, inv) : encode_double(2, 8, x, a);
+  }
+}
+
+// PACK: bits per stored code (BITS for the packed stream, 8 for one byte per
+// element).
+template <int BITS, int PACK, int CODEC, typename Tin>
+__global__ void __launch_bounds__(kThreads)
+    k_quant_tiled(SegTable st, agq_errors* err) {
+  using TR = InTraits<Tin>;
+  constexpr int kStages = TR::kStages;
+  constexpr int kChunks = TR::kChunks;
+  constexpr int kPerChunk = 32 / kChunks;               // elements per chunk
+  constexpr uint32_t kInBytes = kTileElems * sizeof(Tin);
+  constexpr uint32_t kCodeBytes = kTileElems * PACK / 8;
+  constexpr int kChunkBits = kPerChunk * PACK;         // <= 64
+  constexpr int L = (1 << (BITS - 1)) - 1;
+  constexpr uint32_t kZeroCode = CODEC == 0 ? (uint32_t)L : 0u;
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* in_buf = smem;
+  unsigned char* out_buf = smem + kStages * kInBytes;
+  float* sc_buf = reinterpret_cast<float*>(out_buf + 2 * kCodeBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sc_buf + 2 * kTileBlocks);
+
+  const int tid = threadIdx.x;
+  const uint64_t ntiles = st.tile_begin[st.nseg];
+  const uint64_t policy = policy_evict_first();
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue_load = [&](uint64_t t, int s) {
+    const int g = seg_of(st, t);
+    const unsigned char* src = static_cast<const unsigned char*>(st.src[g]) +
+                               (t - st.tile_begin[g]) * kInBytes;
+    mbar_arrive_expect_tx(&full[s], kInBytes);
+    bulk_g2s(in_buf + s * kInBytes, src, kInBytes, &full[s], policy);
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      const uint64_t t = blockIdx.x + (uint64_t)s * gridDim.x;
+      if (t < ntiles) issue_load(t, s);
+    }
+  }
+
+  const int rot = kChunks == 4 ? ((tid >> 1) & 3) : (tid & 7);
+  const int lblk = tid >> 2;  // block within the tile
+
+  for (uint64_t it = 0;; ++it) {
+    const uint64_t t = blockIdx.x + it * gridDim.x;
+    if (t >= ntiles) break;
+    const int s = (int)(it % kStages);
+    const uint32_t parity = (uint32_t)((it / kStages) & 1);
+    mbar_wait(&full[s], parity);
+
+    // ---- load my 32 elements, chunk j of the rotated order = chunk (j+rot)
+    const unsigned char* row = in_buf + s * kInBytes + tid * (32 * sizeof(Tin));
+    uint4 ch[kChunks];
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j)
+      ch[j] = lds128(row + ((j + rot) & (kChunks - 1)) * 16);
+
+    // ---- block absmax on |x| bit patterns (integer max; NaN/Inf sort high)
+    uint32_t m;
+    if constexpr (TR::kBf16) {
+      uint32_t mm = 0;
+#pragma unroll
+      for (int j = 0; j < kChunks; ++j) {
+        mm = __vmaxu2(mm, ch[j].x & 0x7fff7fffu);
+        mm = __vmaxu2(mm, ch[j].y & 0x7fff7fffu);
+        mm = __vmaxu2(mm, ch[j].z & 0x7fff7fffu);
+        mm = __vmaxu2(mm, ch[j].w & 0x7fff7fffu);
+      }
+      m = max(mm & 0xffffu, mm >> 16) << 16;
+    } else {
+      m = 0;
+#pragma unroll
+      for (int j = 0; j < kChunks; ++j) {
+        m = max(m, ch[j].x & 0x7fffffffu);
+        m = max(m, ch[j].y & 0x7fffffffu);
+        m = max(m, ch[j].z & 0x7fffffffu);
+        m = max(m, ch[j].w & 0x7fffffffu);
+      }
+    }
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
+    const float a = u2f(m);
+    const int g = seg_of(st, t);
+    const uint64_t tile_in_seg = t - st.tile_begin[g];
+    if (m >= 0x7f800000u && (tid & 3) == 0)
+      err_min(&err->nonfinite_block,
+              (long long)(st.block_base[g] + tile_in_seg * kTileBlocks + lblk));
+
+    const bool zero = (m == 0);
+    const bool fast = fast_scale(a);
+    float inv = 0.f, rcp = 0.f;
+    if (!zero) {
+      inv = codec_inv(CODEC, BITS, a);
+      if (CODEC == 0 && TR::kBf16) rcp = fdiv(1.0f, a);
+    }
+
+    // ---- encode + pack each chunk (kPerChunk codes -> kChunkBits bits)
+    uint64_t pk[kChunks];
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) {
+      const uint32_t wv[4] = {ch[j].x, ch[j].y, ch[j].z, ch[j].w};
+      uint64_t acc = 0;
+#pragma unroll
+      for (int e = 0; e < kPerChunk; ++e) {
+        float x;
+        if constexpr (TR::kBf16)
+          x = u2f((e & 1) ? (wv[e >> 1] & 0xffff0000u) : (wv[e >> 1] << 16));
+        else
+          x = u2f(wv[e]);
+        const uint32_t c =
+            zero ? kZeroCode : encode_one<BITS, CODEC, TR::kBf16>(x, a, inv, rcp, fast);
+        acc |= (uint64_t)c << (e * PACK);
+      }
+      pk[j] = acc;
+    }
+    // undo the rotation: pk[(j + rot)] must hold chunk j
+    if constexpr (kChunks == 4) rotr4(pk, rot); else rotr8(pk, rot);
+
+    uint32_t words[PACK] = {};
+    pack_chunks<kChunkBits>(words, pk, std::make_integer_sequence<int, kChunks>{});
+
+    // ---- stage out: wait until the bulk store of two tiles ago released it
+    const int ob = (int)(it & 1);
+    if (tid == 0) bulk_wait_read<1>();
+    __syncthreads();
+    uint32_t* ow = reinterpret_cast<uint32_t*>(out_buf + ob * kCodeBytes) + tid * PACK;
+    if constexpr (PACK % 4 == 0) {
+#pragma unroll
+      for (int k = 0; k < PACK / 4; ++k)
+        sts128(ow + 4 * k, make_uint4(words[4 * k], words[4 * k + 1],
+                                      words[4 * k + 2], words[4 * k + 3]));
+    } else {
+#pragma unroll
+      for (int k = 0; k < PACK; ++k) ow[k] = words[k];
+    }
+    if ((tid & 3) == 0) sc_buf[ob * kTileBlocks + lblk] = a;
+    fence_proxy_async_smem();
+    __syncthreads();
+
+    if (tid == 0) {
+      unsigned char* cdst = static_cast<unsigned char*>(st.codes[g]) + tile_in_seg * kCodeBytes;
+      float* sdst = st.scales[g] + tile_in_seg * kTileBlocks;
+      bulk_s2g(cdst, out_buf + ob * kCodeBytes, kCodeBytes);
+      bulk_s2g(sdst, sc_buf + ob * kTileBlocks, kTileBlocks * 4);
+      bulk_commit();
+      const uint64_t nt = t + (uint64_t)kStages * gridDim.x;
+      if (nt < ntiles) issue_load(nt, s);
+    }
+  }
+  if (tid == 0) bulk_wait_all<0>();
+}
+
+// ---------------------------------------------------------------------------
+// K2: dequantize
+// ---------------------------------------------------------------------------
+template <typename Tout>
+struct OutTraits;
+template <>
+struct OutTraits<__nv_bfloat16> {
+  static constexpr int kChunks = 4;
+};
+template <>
+struct OutTraits<float> {
+  static constexpr int kChunks = 8;
+};
+
+// Decode of one code with the block constants (exact, see agq_numerics.cuh).
+template <int BITS, int CODEC>
+__device__ __forceinline__ float decode_one(uint32_t c, float s, bool fast,
+                                            const double* fp8lut) {
+  if (CODEC == 0) {
+    constexpr int L = (1 << (BITS - 1)) - 1;
+    if (fast) return dq_linear_bf16scale((int)c - L, s, (float)L, 1.0f / (float)L);
+    return dequant_double(0, BITS, c, s);
+  } else if (CODEC == 1) {
+    if (fast) return div_const_rn(fmul(e2m1_value(c), s), 6.0f, 1.0f / 6.0f);
+    return dequant_double(1, 4, c, s);
+  } else {
+    if ((c & 0x7fu) == 0x7fu) return u2f(0x7fc00000u | ((c & 0x80u) << 24));
+    if (fast) return div_const_rn(fmul(e4m3_value(c), s), 448.0f, 1.0f / 448.0f);
+    const float mag = d2f_rn(dmul(fp8lut[c & 0x7fu], (double)s));
+    return u2f(f2u(mag) | ((c & 0x80u) << 24));
+  }
+}
+
+// round-to-nearest-even to bf16 with the reference's integer rule
+// (collective.hpp:101-110; identical to cvt.rn for non-NaN values, and keeps
+// the quiet-NaN payload the reference produces).
+__device__ __forceinline__ uint32_t bf16_bits_rne(float f) {
+  uint32_t u = f2u(f);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return u >> 16;
+}
+
+template <int BITS, int PACK, int CODEC, typename Tout>
+__global__ void __launch_bounds__(kThreads)
+    k_dequant_tiled(SegTable st, int validate, agq_errors* err) {
+  constexpr int kStages = 4;
+  constexpr int kChunks = OutTraits<Tout>::kChunks;
+  constexpr int kPerChunk = 32 / kChunks;
+  constexpr uint32_t kCodeBytes = kTileElems * PACK / 8;
+  constexpr uint32_t kStageBytes = kCodeBytes + kTileBlocks * 4;
+  constexpr uint32_t kOutBytes = kTileElems * sizeof(Tout);
+  constexpr int kChunkBits = kPerChunk * PACK;
+  constexpr bool kBf16Out = sizeof(Tout) == 2;
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* in_buf = smem;                                // stages
+  unsigned char* out_buf = smem + kStages * kStageBytes;       // 2 x out
+  uint64_t* full = reinterpret_cast<uint64_t*>(out_buf + 2 * kOutBytes);
+  double* fp8lut = reinterpret_cast<double*>(full + kStages);
+
+  const int tid = threadIdx.x;
+  const uint64_t ntiles = st.tile_begin[st.nseg];
+  const uint64_t policy = policy_evict_first();
+  if (CODEC == 2) fill_fp8_unit_lut(fp8lut);
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue_load = [&](uint64_t t, int s) {
+    const int g = seg_of(st, t);
+    const uint64_t lt = t - st.tile_begin[g];
+    unsigned char* dst = in_buf + s * kStageBytes;
+    mbar_arrive_expect_tx(&full[s], kStageBytes);
+    bulk_g2s(dst, static_cast<const unsigned char*>(st.codes[g]) + lt * kCodeBytes,
+             kCodeBytes, &full[s], policy);
+    bulk_g2s(dst + kCodeBytes, st.scales[g] + lt * kTileBlocks, kTileBlocks * 4,
+             &full[s], policy);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      const uint64_t t = blockIdx.x + (uint64_t)s * gridDim.x;
+      if (t < ntiles) issue_load(t, s);
+    }
+  }
+
+  const int rot = kChunks == 4 ? ((tid >> 1) & 3) : (tid & 7);
+  const int lblk = tid >> 2;
+
+  for (uint64_t it = 0;; ++it) {
+    const uint64_t t = blockIdx.x + it * gridDim.x;
+    if (t >= ntiles) break;
+    const int s = (int)(it % kStages);
+    mbar_wait(&full[s], (uint32_t)((it / kStages) & 1));
+    const unsigned char* sb = in_buf + s * kStageBytes;
+    const uint32_t* wsrc = reinterpret_cast<const uint32_t*>(sb) + tid * PACK;
+    uint32_t words[PACK];
+    if constexpr (PACK % 4 == 0) {
+#pragma unroll
+      for (int k = 0; k < PACK / 4; ++k) {
+        const uint4 v = lds128(wsrc + 4 * k);
+        words[4 * k] = v.x; words[4 * k + 1] = v.y;
+        words[4 * k + 2] = v.z; words[4 * k + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < PACK; ++k) words[k] = wsrc[k];
+    }
+    const float sc = reinterpret_cast<const float*>(sb + kCodeBytes)[lblk];
+    const int g = seg_of(st, t);
+    const uint64_t lt = t - st.tile_begin[g];
+
+    if (validate) {
+      if (!(sc >= 0.0f) || !(sc <= 3.402823466e38f)) {
+        if ((tid & 3) == 0)
+          err_min(&err->bad_scale_block,
+                  (long long)(st.block_base[g] + lt * kTileBlocks + lblk));
+      }
+      if constexpr (PACK == 8 && BITS < 8) {
+        uint32_t bad = 0;
+#pragma unroll
+        for (int k = 0; k < PACK; ++k) bad |= words[k] & (0x01010101u * (0xffu << BITS & 0xffu));
+        if (bad) {
+          // lowest offending element of this thread
+#pragma unroll 1
+          for (int e = 0; e < 32; ++e) {
+            const uint32_t c = (words[e >> 2] >> ((e & 3) * 8)) & 0xffu;
+            if (c >> BITS) {
+              err_min(&err->bad_code_index,
+                      (long long)((st.block_base[g] + lt * kTileBlocks) * kBlock + tid * 32 + e));
+              break;
+            }
+          }
+        }
+      }
+    }
+
+    const bool fast = is_bf16_value(sc) && fast_scale(sc);
+    uint64_t pk[kChunks];
+    unpack_chunks<kChunkBits>(words, pk, std::make_integer_sequence<int, kChunks>{});
+    // rotated order: slot j holds chunk (j + rot)
+    if constexpr (kChunks == 4) rotl4(pk, rot); else rotl8(pk, rot);
+
+    const int ob = (int)(it & 1);
+    if (tid == 0) bulk_wait_read<1>();
+    __syncthreads();
+    unsigned char* orow = out_buf + ob * kOutBytes + tid * (32 * sizeof(Tout));
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) {
+      float v[kPerChunk];
+#pragma unroll
+      for (int e = 0; e < kPerChunk; ++e) {
+        const uint32_t c = (uint32_t)(pk[j] >> (e * PACK)) & ((1u << PACK) - 1u);
+        v[e] = decode_one<BITS, CODEC>(c & ((1u << BITS) - 1u), sc, fast, fp8lut);
+      }
+      uint4 o;
+      if constexpr (kBf16Out) {
+        uint32_t h[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (CODEC == 2)
+            h[k] = bf16_bits_rne(v[2 * k]) | (bf16_bits_rne(v[2 * k + 1]) << 16);
+          else {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+            h[k] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+        }
+        o = make_uint4(h[0], h[1], h[2], h[3]);
+      } else {
+        o = make_uint4(f2u(v[0]), f2u(v[1]), f2u(v[2]), f2u(v[3]));
+      }
+      sts128(orow + ((j + rot) & (kChunks - 1)) * 16, o);
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      unsigned char* dst = static_cast<unsigned char*>(st.dst[g]) + lt * kOutBytes;
+      bulk_s2g(dst, out_buf + ob * kOutBytes, kOutBytes);
+      bulk_commit();
+      const uint64_t nt = t + (uint64_t)kStages * gridDim.x;
+      if (nt < ntiles) issue_load(nt, s);
+    }
+  }
+  if (tid == 0) bulk_wait_all<0>();
+}
+
+// ---------------------------------------------------------------------------
+// Generic kernels (any block size, alignment, tails)
+// ---------------------------------------------------------------------------
+template <typename Tin>
+__device__ __forceinline__ float load_in(const Tin* x, uint64_t i) {
+  if constexpr (sizeof(Tin) == 2)
+    return u2f((uint32_t)reinterpret_cast<const uint16_t*>(x)[i] << 16);
+  else
+    return x[i];
+}
+
+// One warp per block: absmax (as |x| bits), non-finite detection.
+template <typename Tin>
+__global__ void k_absmax_generic(const Tin* x, uint64_t n, uint32_t block,
+                                 uint64_t nblocks, float* scales,
+                                 long long blk_base, agq_errors* err) {
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+  for (uint64_t b = warp; b < nblocks; b += nwarps) {
+    const uint64_t beg = b * block;
+    const uint64_t end = min(n, beg + block);
+    uint32_t m = 0;
+    for (uint64_t i = beg + lane; i < end; i += 32) m = max(m, f2u(load_in(x, i)) & 0x7fffffffu);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) {
+      scales[b] = u2f(m);
+      if (m >= 0x7f800000u) err_min(&err->nonfinite_block, blk_base + (long long)b);
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t encode_generic(int codec, int bits, float x,
+                                                   float a) {
+  if (a == 0.0f) return codec == 0 ? (uint32_t)levels_of(bits) : 0u;
+  if (!(a <= 3.402823466e38f)) return 0u;  // non-finite block: error recorded
+  return encode_f32(codec, bits, x, a, codec_inv(codec, bits, a));
+}
+
+// One thread per output byte of the LSB-first stream (tensor_io.hpp:69-77).
+template <typename Tin>
+__global__ void k_encode_packed_generic(const Tin* x, uint64_t n, int bits,
+                                        uint32_t block, int codec,
+                                        const float* scales, uint8_t* packed) {
+  const uint64_t nbytes = (n * bits + 7) / 8;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nbytes;
+       j += gridDim.x * (uint64_t)blockDim.x) {
+    const uint64_t bit0 = j * 8;
+    const uint64_t e0 = bit0 / bits;
+    const uint64_t e1 = min(n - 1, (bit0 + 7) / bits);
+    uint32_t byte = 0;
+    for (uint64_t e = e0; e <= e1; ++e) {
+      const uint32_t c = encode_generic(codec, bits, load_in(x, e), scales[e / block]);
+      const long long off = (long long)(e * bits) - (long long)bit0;
+      byte |= off >= 0 ? (c << off) : (c >> (-off));
+    }
+    packed[j] = (uint8_t)(byte & 0xffu);
+  }
+}
+
+template <typename Tin>
+__global__ void k_encode_bytes_generic(const Tin* x, uint64_t n, int bits,
+                                       uint32_t block, int codec,
+                                       const float* scales, uint8_t* codes) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += gridDim.x * (uint64_t)blockDim.x)
+    codes[i] = (uint8_t)encode_generic(codec, bits, load_in(x, i), scales[i / block]);
+}
+
+__device__ __forceinline__ uint32_t read_code(const uint8_t* codes, int layout,
+                                              int bits, uint64_t i) {
+  if (layout == AGQ_CODES_BYTES) return codes[i];
+  const uint64_t bit = i * bits;
+  const uint64_t byte = bit >> 3;
+  uint32_t v = codes[byte];
+  if ((bit & 7) + bits > 8) v |= (uint32_t)codes[byte + 1] << 8;
+  return (v >> (bit & 7)) & ((1u << bits) - 1u);
+}
+
+template <typename Tout>
+__global__ void k_dequant_generic(const uint8_t* codes, int layout,
+                                  const float* scales, uint64_t n, int bits,
+                                  uint32_t block, int codec, Tout* out,
+                                  int validate, long long elem_base,
+                                  agq_errors* err) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += gridDim.x * (uint64_t)blockDim.x) {
+    const uint32_t c = read_code(codes, layout, bits, i);
+    const float s = scales[i / block];
+    if (validate) {
+      if (c >> bits) err_min(&err->bad_code_index, elem_base + (long long)i);
+      if ((i % block) == 0 && (!(s >= 0.0f) || !(s <= 3.402823466e38f)))
+        err_min(&err->bad_scale_block, (elem_base + (long long)i) / block);
+    }
+    const uint32_t cc = c & ((1u << bits) - 1u);
+    float v;
+    if (codec == 2 && (cc & 0x7fu) == 0x7fu)
+      v = u2f(0x7fc00000u | ((cc & 0x80u) << 24));
+    else
+      v = dequant_double(codec, bits, cc, s);
+    if constexpr (sizeof(Tout) == 2)
+      reinterpret_cast<uint16_t*>(out)[i] = (uint16_t)bf16_bits_rne(v);
+    else
+      out[i] = v;
+  }
+}
+
+__global__ void k_pack_generic(const uint8_t* codes, uint64_t n, int bits,
+                               uint8_t* packed) {
+  const uint64_t nbytes = (n * bits + 7) / 8;
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < nbytes;
+       j += gridDim.x * (uint64_t)blockDim.x) {
+    const uint64_t bit0 = j * 8;
+    const uint64_t e0 = bit0 / bits;
+    const uint64_t e1 = min(n - 1, (bit0 + 7) / bits);
+    uint32_t byte = 0;
+    for (uint64_t e = e0; e <= e1; ++e) {
+      const uint32_t c = codes[e] & ((1u << bits) - 1u);
+      const long long off = (long long)(e * bits) - (long long)bit0;
+      byte |= off >= 0 ? (c << off) : (c >> (-off));
+    }
+    packed[j] = (uint8_t)(byte & 0xffu);
+  }
+}
+
+__global__ void k_unpack_generic(const uint8_t* packed, uint64_t n, int bits,
+                                 uint8_t* codes) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += gridDim.x * (uint64_t)blockDim.x)
+    codes[i] = (uint8_t)read_code(packed, AGQ_CODES_PACKED, bits, i);
+}
+
+}  // namespace agqk
+
+// ===========================================================================
+// Host launchers
+// ===========================================================================
+namespace agqh {
+using namespace agqk;
+
+namespace {
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+template <typename K>
+int grid_for(K kernel, size_t smem, uint64_t ntiles) {
+  static_assert(sizeof(K) > 0, "");
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
+  if (occ < 1) occ = 1;
+  const uint64_t g = (uint64_t)num_sms() * (uint64_t)occ;
+  return (int)(ntiles < g ? ntiles : g);
+}
+
+template <typename K>
+cudaError_t prep(K kernel, size_t smem) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+int gen_grid(uint64_t work, int threads) {
+  const uint64_t g = (work + threads - 1) / threads;
+  const uint64_t cap = (uint64_t)num_sms() * 16;
+  return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+template <int BITS, int PACK, int CODEC, typename Tin>
+agq_status launch_quant_tiled(const SegTable& st, agq_errors* err, cudaStream_t s) {
+  using TR = InTraits<Tin>;
+  const size_t smem = TR::kStages * (size_t)kTileElems * sizeof(Tin) +
+                      2 * (size_t)kTileElems * PACK / 8 + 2 * kTileBlocks * 4 +
+                      TR::kStages * 8;
+  auto k = k_quant_tiled<BITS, PACK, CODEC, Tin>;
+  cudaError_t e = prep(k, smem);
+  if (e != cudaSuccess) return cuda_fail(e, "quantize: smem attribute");
+  const int grid = grid_for(k, smem, st.tile_begin[st.nseg]);
+  k<<<grid, kThreads, smem, s>>>(st, err);
+  count_launch();
+  return cuda_fail(cudaGetLastError(), "quantize: launch");
+}
+
+template <int PACK, typename Tin>
+agq_status quant_dispatch_bits(int bits, int codec, const SegTable& st,
+                               agq_errors* err, cudaStream_t s) {
+  if (codec == AGQ_CODEC_FP8_E4M3) return launch_quant_tiled<8, 8, 2, Tin>(st, err, s);
+  if (codec == AGQ_CODEC_FP4_E2M1) return launch_quant_tiled<4, PACK == 8 ? 8 : 4, 1, Tin>(st, err, s);
+  switch (bits) {
+    case 4: return launch_quant_tiled<4, PACK == 8 ? 8 : 4, 0, Tin>(st, err, s);
+    case 5: return launch_quant_tiled<5, PACK == 8 ? 8 : 5, 0, Tin>(st, err, s);
+    case 6: return launch_quant_tiled<6, PACK == 8 ? 8 : 6, 0, Tin>(st, err, s);
+    case 7: return launch_quant_tiled<7, PACK == 8 ? 8 : 7, 0, Tin>(st, err, s);
+    default: return launch_quant_tiled<8, 8, 0, Tin>(st, err, s);
+  }
+}
+
+template <int BITS, int PACK, int CODEC, typename Tout>
+agq_status launch_dequant_tiled(const SegTable& st, int validate, agq_errors* err,
+                                cudaStream_t s) {
+  const size_t smem = 4 * ((size_t)kTileElems * PACK / 8 + kTileBlocks * 4) +
+                      2 * (size_t)kTileElems * sizeof(Tout) + 4 * 8 + 128 * 8;
+  auto k = k_dequant_tiled<BITS, PACK, CODEC, Tout>;
+  cudaError_t e = prep(k, smem);
+  if (e != cudaSuccess) return cuda_fail(e, "dequantize: smem attribute");
+  const int grid = grid_for(k, smem, st.tile_begin[st.nseg]);
+  k<<<grid, kThreads, smem, s>>>(st, validate, err);
+  count_launch();
+  return cuda_fail(cudaGetLastError(), "dequantize: launch");
+}
+
+template <int PACK, typename Tout>
+agq_status dequant_dispatch_bits(int bits, int codec, const SegTable& st,
+                                 int validate, agq_errors* err, cudaStream_t s) {
+  if (codec == AGQ_CODEC_FP8_E4M3) return launch_dequant_tiled<8, 8, 2, Tout>(st, validate, err, s);
+  if (codec == AGQ_CODEC_FP4_E2M1) return launch_dequant_tiled<4, PACK == 8 ? 8 : 4, 1, Tout>(st, validate, err, s);
+  switch (bits) {
+    case 4: return launch_dequant_tiled<4, PACK == 8 ? 8 : 4, 0, Tout>(st, validate, err, s);
+    case 5: return launch_dequant_tiled<5, PACK == 8 ? 8 : 5, 0, Tout>(st, validate, err, s);
+    case 6: return launch_dequant_tiled<6, PACK == 8 ? 8 : 6, 0, Tout>(st, validate, err, s);
+    case 7: return launch_dequant_tiled<7, PACK == 8 ? 8 : 7, 0, Tout>(st, validate, err, s);
+    default: return launch_dequant_tiled<8, 8, 0, Tout>(st, validate, err, s);
+  }
+}
+
+template <typename Tin>
+agq_status quant_generic(const Tin* x, uint64_t n, int bits, uint32_t block,
+                         int codec, void* codes, int layout, float* scales,
+                         long long blk_base, agq_errors* err, cudaStream_t s) {
+  const uint64_t nb = (n + block - 1) / block;
+  k_absmax_generic<Tin><<<gen_grid(nb * 32, 256), 256, 0, s>>>(x, n, block, nb, scales,
+                                                              blk_base, err);
+  count_launch();
+  if (layout == AGQ_CODES_PACKED) {
+    const uint64_t nbytes = (n * bits + 7) / 8;
+    k_encode_packed_generic<Tin><<<gen_grid(nbytes, 256), 256, 0, s>>>(
+        x, n, bits, block, codec, scales, static_cast<uint8_t*>(codes));
+  } else {
+    k_encode_bytes_generic<Tin><<<gen_grid(n, 256), 256, 0, s>>>(
+        x, n, bits, block, codec, scales, static_cast<uint8_t*>(codes));
+  }
+  count_launch();
+  return cuda_fail(cudaGetLastError(), "quantize (generic): launch");
+}
+
+}  // namespace
+
+agq_status quantize_device(const void* x, int x_dtype, uint64_t n, int bits,
+                           uint32_t block, int codec, void* codes, int layout,
+                           float* scales, agq_errors* err, cudaStream_t s) {
+  if (n == 0) return AGQ_OK;
+  const int pack = layout == AGQ_CODES_PACKED ? bits : 8;
+  const size_t esz = x_dtype == AGQ_BF16 ? 2 : 4;
+  uint64_t ntiles = 0;
+  if (block == (uint32_t)kBlock && aligned16(x) && aligned16(codes) && aligned16(scales))
+    ntiles = n / kTileElems;
+  if (ntiles > 0) {
+    SegTable st{};
+    st.src[0] = x;
+    st.codes[0] = codes;
+    st.scales[0] = scales;
+    st.tile_begin[0] = 0;
+    st.tile_begin[1] = ntiles;
+    st.block_base[0] = 0;
+    st.nseg = 1;
+    agq_status r;
+    if (x_dtype == AGQ_BF16)
+      r = layout == AGQ_CODES_PACKED ? quant_dispatch_bits<0, __nv_bfloat16>(bits, codec, st, err, s)
+                                     : quant_dispatch_bits<8, __nv_bfloat16>(bits, codec, st, err, s);
+    else
+      r = layout == AGQ_CODES_PACKED ? quant_dispatch_bits<0, float>(bits, codec, st, err, s)
+                                     : quant_dispatch_bits<8, float>(bits, codec, st, err, s);
+    if (r != AGQ_OK) return r;
+  }
+  const uint64_t done = ntiles * kTileElems;
+  if (done == n) return AGQ_OK;
+  // tail (block-aligned start, byte-aligned in the packed stream)
+  const uint64_t rest = n - done;
+  const long long bb = (long long)(done / block);
+  void* ctail = static_cast<uint8_t*>(codes) + (done * pack) / 8;
+  if (x_dtype == AGQ_BF16)
+    return quant_generic(reinterpret_cast<const __nv_bfloat16*>(x) + done, rest, bits, block,
+                         codec, ctail, layout, scales + done / block, bb, err, s);
+  return quant_generic(reinterpret_cast<const float*>(x) + done, rest, bits, block, codec, ctail,
+                       layout, scales + done / block, bb, err, s);
+  (void)esz;
+}
+
+agq_status dequantize_device(const void* codes, int layout, const float* scales,
+                             uint64_t n, int bits, uint32_t block, int codec,
+                             void* out, int out_dtype, int validate,
+                             agq_errors* err, cudaStream_t s) {
+  if (n == 0) return AGQ_OK;
+  const int pack = layout == AGQ_CODES_PACKED ? bits : 8;
+  uint64_t ntiles = 0;
+  if (block == (uint32_t)kBlock && aligned16(out) && aligned16(codes) && aligned16(scales))
+    ntiles = n / kTileElems;
+  if (ntiles > 0) {
+    SegTable st{};
+    st.codes[0] = const_cast<void*>(codes);
+    st.scales[0] = const_cast<float*>(scales);
+    st.dst[0] = out;
+    st.tile_begin[1] = ntiles;
+    st.nseg = 1;
+    agq_status r;
+    if (out_dtype == AGQ_BF16)
+      r = layout == AGQ_CODES_PACKED
+              ? dequant_dispatch_bits<0, __nv_bfloat16>(bits, codec, st, validate, err, s)
+              : dequant_dispatch_bits<8, __nv_bfloat16>(bits, codec, st, validate, err, s);
+    else
+      r = layout == AGQ_CODES_PACKED ? dequant_dispatch_bits<0, float>(bits, codec, st, validate, err, s)
+                                     : dequant_dispatch_bits<8, float>(bits, codec, st, validate, err, s);
+    if (r != AGQ_OK) return r;
+  }
+  const uint64_t done = ntiles * kTileElems;
+  if (done == n) return AGQ_OK;
+  const uint64_t rest = n - done;
+  const uint8_t* ctail = static_cast<const uint8_t*>(codes) + (done * pack) / 8;
+  const float* stail = scales + done / block;
+  if (out_dtype == AGQ_BF16)
+    k_dequant_generic<__nv_bfloat16><<<gen_grid(rest, 256), 256, 0, s>>>(
+        ctail, layout, stail, rest, bits, block, codec,
+        static_cast<__nv_bfloat16*>(out) + done, validate, (long long)done, err);
+  else
+    k_dequant_generic<float><<<gen_grid(rest, 256), 256, 0, s>>>(
+        ctail, layout, stail, rest, bits, block, codec, static_cast<float*>(out) + done,
+        validate, (long long)done, err);
+  count_launch();
+  return cuda_fail(cudaGetLastError(), "dequantize (generic): launch");
+}
+
+agq_status quantize_grouped_device(const agq_segment* segs, int nseg, int x_dtype,
+                                   int bits, int codec, agq_errors* err,
+                                   cudaStream_t s) {
+  // Full tiles of every segment in one launch; tails individually.
+  SegTable st{};
+  uint64_t tiles = 0, blocks = 0;
+  int k = 0;
+  for (int i = 0; i < nseg; ++i) {
+    const uint64_t nt = aligned16(segs[i].x) && aligned16(segs[i].codes) &&
+                                aligned16(segs[i].scales)
+                            ? segs[i].n / kTileElems
+                            : 0;
+    if (nt > 0) {
+      if (k == kMaxSeg) return set_error(AGQ_ERR_INVALID_ARGUMENT, "too many segments");
+      st.src[k] = segs[i].x;
+      st.codes[k] = segs[i].codes;
+      st.scales[k] = segs[i].scales;
+      st.tile_begin[k] = tiles;
+      st.block_base[k] = blocks;
+      tiles += nt;
+      ++k;
+    }
+    blocks += (segs[i].n + kBlock - 1) / kBlock;
+  }
+  st.tile_begin[k] = tiles;
+  st.nseg = k;
+  if (k > 0) {
+    agq_status r = x_dtype == AGQ_BF16
+                       ? quant_dispatch_bits<0, __nv_bfloat16>(bits, codec, st, err, s)
+                       : quant_dispatch_bits<0, float>(bits, codec, st, err, s);
+    if (r != AGQ_OK) return r;
+  }
+  for (int i = 0; i < nseg; ++i) {
+    const bool tiled = aligned16(segs[i].x) && aligned16(segs[i].codes) && aligned16(segs[i].scales);
+    const uint64_t done = tiled ? (segs[i].n / kTileElems) * kTileElems : 0;
+    if (done == segs[i].n) continue;
+    const size_t esz = x_dtype == AGQ_BF16 ? 2 : 4;
+    agq_status r = quantize_device(static_cast<const char*>(segs[i].x) + done * esz, x_dtype,
+                                   segs[i].n - done, bits, kBlock, codec,
+                                   static_cast<uint8_t*>(segs[i].codes) + done * bits / 8,
+                                   AGQ_CODES_PACKED, segs[i].scales + done / kBlock, err, s);
+    if (r != AGQ_OK) return r;
+  }
+  return AGQ_OK;
+}
+
+agq_status dequantize_grouped_device(const agq_segment* segs, int nseg, int out_dtype,
+                                     int bits, int codec, cudaStream_t s) {
+  SegTable st{};
+  uint64_t tiles = 0;
+  int k = 0;
+  for (int i = 0; i < nseg; ++i) {
+    const bool tiled = aligned16(segs[i].x) && aligned16(segs[i].codes) && aligned16(segs[i].scales);
+    const uint64_t nt = tiled ? segs[i].n / kTileElems : 0;
+    if (nt > 0) {
+      if (k == kMaxSeg) return set_error(AGQ_ERR_INVALID_ARGUMENT, "too many segments");
+      st.codes[k] = segs[i].codes;
+      st.scales[k] = segs[i].scales;
+      st.dst[k] = const_cast<void*>(segs[i].x);
+      st.tile_begin[k] = tiles;
+      tiles += nt;
+      ++k;
+    }
+  }
+  st.tile_begin[k] = tiles;
+  st.nseg = k;
+  if (k > 0) {
+    agq_status r = out_dtype == AGQ_BF16
+                       ? dequant_dispatch_bits<0, __nv_bfloat16>(bits, codec, st, 0, nullptr, s)
+                       : dequant_dispatch_bits<0, float>(bits, codec, st, 0, nullptr, s);
+    if (r != AGQ_OK) return r;
+  }
+  for (int i = 0; i < nseg; ++i) {
+    const bool tiled = aligned16(segs[i].x) && aligned16(segs[i].codes) && aligned16(segs[i].scales);
+    const uint64_t done = tiled ? (segs[i].n / kTileElems) * kTileElems : 0;
+    if (done == segs[i].n) continue;
+    const size_t esz = out_dtype == AGQ_BF16 ? 2 : 4;
+    agq_status r = dequantize_device(
+        static_cast<const uint8_t*>(segs[i].codes) + done * bits / 8, AGQ_CODES_PACKED,
+        segs[i].scales + done / kBlock, segs[i].n - done, bits, kBlock, codec,
+        static_cast<char*>(const_cast<void*>(segs[i].x)) + done * esz, out_dtype, 0, nullptr, s);
+    if (r != AGQ_OK) return r;
+  }
+  return AGQ_OK;
+}
+
+agq_status pack_device(const uint8_t* codes, uint64_t n, int bits, uint8_t* packed,
+                       cudaStream_t s) {
+  if (n == 0) return AGQ_OK;
+  k_pack_generic<<<gen_grid((n * bits + 7) / 8, 256), 256, 0, s>>>(codes, n, bits, packed);
+  count_launch();
+  return cuda_fail(cudaGetLastError(), "pack: launch");
+}
+
+agq_status unpack_device(const uint8_t* packed, uint64_t n, int bits, uint8_t* codes,
+                         cudaStream_t s) {
+  if (n == 0) return AGQ_OK;
+  k_unpack_generic<<<gen_grid(n, 256), 256, 0, s>>>(packed, n, bits, codes);
+  count_launch();
+  return cuda_fail(cudaGetLastError(), "unpack: launch");
+}
+
+}  // namespace agqh

@@ -1,0 +1,179 @@
+// Device building blocks of the FP8 gradient path shared by the accumulate,
+// reduce-requant and fused all-reduce kernels (see grad_codec.cu).
+#pragma once
+#include "agq_common.cuh"
+
+namespace agqk {
+
+// collective.hpp:101-110 round_bf16 (integer RNE on the fp32 bits)
+__device__ __forceinline__ float round_bf16_ref(float x) {
+  uint32_t u = f2u(x);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return u2f(u & 0xffff0000u);
+}
+// collective.hpp:112-123 round_fp16: RNE to fp16, but |x| >= 65520 saturates
+// to +-65504 (not inf); zero and non-finite pass through.
+__device__ __forceinline__ float round_fp16_ref(float x) {
+  if (x == 0.0f || !(fabsf(x) <= 3.402823466e38f)) return x;
+  if (fabsf(x) >= 65520.0f) return copysignf(65504.0f, x);
+  return __half2float(__float2half_rn(x));
+}
+
+template <int PREC>
+__device__ __forceinline__ float apply_prec(float s) {
+  if (PREC == AGQ_ACC_BF16) return round_bf16_ref(s);
+  if (PREC == AGQ_ACC_FP16) return round_fp16_ref(s);
+  return s;
+}
+
+__device__ __forceinline__ float fp8_dequant(uint32_t c, double sd, const double* lut) {
+  const float mag = d2f_rn(dmul(lut[c & 0x7fu], sd));
+  return u2f(f2u(mag) ^ ((c & 0x80u) << 24));
+}
+
+// Encode 2 values of a block with absmax a (fast scale) -> 2 E4M3 codes.
+__device__ __forceinline__ uint32_t fp8_encode_pair(float s0, float s1, float a, float inv) {
+  const float v0 = fmul(s0, inv), v1 = fmul(s1, inv);
+  uint32_t r = cvt_e4m3x2(v0, v1);
+  if (fp8_near(v0)) r = (r & 0xff00u) | fp8_code(s0, a, inv);
+  if (fp8_near(v1)) r = (r & 0x00ffu) | (fp8_code(s1, a, inv) << 8);
+  return r;
+}
+
+// Requantize 16 fp32 values of a block whose absmax is `a` (all 8 threads of
+// the block agree on a): returns 4 words of codes (element e in byte e).
+__device__ __forceinline__ void fp8_requant16(const float (&v)[16], float a, uint32_t (&w)[4]) {
+  if (a == 0.0f) {
+    w[0] = w[1] = w[2] = w[3] = 0u;
+    return;
+  }
+  if (fast_scale(a)) {
+    const float inv = fdiv(448.0f, a);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      w[k] = fp8_encode_pair(v[4 * k], v[4 * k + 1], a, inv) |
+             (fp8_encode_pair(v[4 * k + 2], v[4 * k + 3], a, inv) << 16);
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      w[k] = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) w[k] |= encode_double(2, 8, v[4 * k + e], a) << (8 * e);
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t absmax_bits16(const float (&v)[16]) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) m = max(m, f2u(v[e]) & 0x7fffffffu);
+  m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
+  m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
+  m = max(m, __shfl_xor_sync(0xffffffffu, m, 4));
+  return m;
+}
+
+// K4 piece table: pieces in ascending sender rank; outputs possibly remote.
+struct PieceTable {
+  const uint8_t* codes[AGQ_MAX_WORLD];
+  const float* scales[AGQ_MAX_WORLD];
+  uint8_t* out_codes[AGQ_MAX_WORLD];
+  float* out_scales[AGQ_MAX_WORLD];
+  int np, nout;
+};
+
+// ---------------------------------------------------------------------------
+// K4: block-128 reduce-requant, 16 elements per thread, direct loads.
+// ---------------------------------------------------------------------------
+// One 16-element group: loads of every piece first (memory-level
+// parallelism), then the fp32 sum in ascending piece order from +0.0f.
+template <int NP>
+__device__ __forceinline__ void reduce_group(const PieceTable& pt, uint64_t g, uint64_t len,
+                                             long long blk_base, const double* lut,
+                                             agq_errors* err, bool vec) {
+  const int np = NP > 0 ? NP : pt.np;
+  const uint64_t e0 = g * 16;
+  const uint64_t blk = e0 / kBlock;
+  const bool in_range = e0 < len;
+  const bool whole = vec && e0 + 16 <= len;
+  float acc[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) acc[e] = 0.0f;
+  uint32_t sbad = 0;
+  if (in_range) {
+    constexpr int kMaxUnroll = NP > 0 ? NP : AGQ_MAX_WORLD;
+    uint4 cv[NP > 0 ? NP : 1];
+    float sc[NP > 0 ? NP : 1];
+    if constexpr (NP > 0) {
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        sc[p] = pt.scales[p][blk];
+        if (whole) {
+          cv[p] = *reinterpret_cast<const uint4*>(pt.codes[p] + e0);
+        } else {
+          uint32_t w[4] = {0, 0, 0, 0};
+          for (int e = 0; e < 16 && e0 + e < len; ++e)
+            w[e >> 2] |= (uint32_t)pt.codes[p][e0 + e] << (8 * (e & 3));
+          cv[p] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        sbad |= !(sc[p] >= 0.0f) || !(sc[p] <= 3.402823466e38f);
+        const double sd = (double)sc[p];
+        const uint32_t w[4] = {cv[p].x, cv[p].y, cv[p].z, cv[p].w};
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          acc[e] = fadd(acc[e], fp8_dequant((w[e >> 2] >> (8 * (e & 3))) & 0xffu, sd, lut));
+      }
+    } else {
+      (void)kMaxUnroll;
+#pragma unroll 1
+      for (int p = 0; p < np; ++p) {
+        const float scp = pt.scales[p][blk];
+        sbad |= !(scp >= 0.0f) || !(scp <= 3.402823466e38f);
+        uint32_t w[4] = {0, 0, 0, 0};
+        if (whole) {
+          const uint4 v = *reinterpret_cast<const uint4*>(pt.codes[p] + e0);
+          w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+        } else {
+          for (int e = 0; e < 16 && e0 + e < len; ++e)
+            w[e >> 2] |= (uint32_t)pt.codes[p][e0 + e] << (8 * (e & 3));
+        }
+        const double sd = (double)scp;
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          acc[e] = fadd(acc[e], fp8_dequant((w[e >> 2] >> (8 * (e & 3))) & 0xffu, sd, lut));
+      }
+    }
+    // elements past the end contribute nothing to the absmax
+    if (!whole)
+      for (int e = 0; e < 16; ++e)
+        if (e0 + e >= len) acc[e] = 0.0f;
+  }
+  const uint32_t m = absmax_bits16(acc);
+  const int sub = threadIdx.x & 7;
+  if (in_range && sub == 0) {
+    if (sbad) err_min(&err->bad_scale_block, blk_base + (long long)blk);
+    if (m >= 0x7f800000u) err_min(&err->overflow_block, blk_base + (long long)blk);
+  }
+  if (!in_range) return;
+  const float a = u2f(m);
+  uint32_t ow[4];
+  if (m >= 0x7f800000u) {
+    ow[0] = ow[1] = ow[2] = ow[3] = 0;
+  } else {
+    fp8_requant16(acc, a, ow);
+  }
+  for (int o = 0; o < pt.nout; ++o) {
+    if (whole) {
+      *reinterpret_cast<uint4*>(pt.out_codes[o] + e0) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+    } else {
+      for (int e = 0; e < 16 && e0 + e < len; ++e)
+        pt.out_codes[o][e0 + e] = (uint8_t)(ow[e >> 2] >> (8 * (e & 3)));
+    }
+    if (sub == 0) pt.out_scales[o][blk] = a;
+  }
+}
+
+}  // namespace agqk

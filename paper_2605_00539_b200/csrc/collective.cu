@@ -1,0 +1,507 @@
+// Multi-GPU decomposed 8-bit all-reduce (collective.hpp:226-333 for real
+// ranks, one process per GPU).
+//
+// AGQ_AR_NCCL (v1): chunk r of every rank goes to rank r with grouped
+//   ncclSend/ncclRecv (the all-to-all), rank r runs the K4 reduce-requant
+//   kernel over its chunk (pieces in ascending sender rank, in place), then a
+//   second grouped send/recv broadcasts every reduced chunk straight into
+//   place on all ranks (the all-gather).
+// AGQ_AR_FUSED_P2P (v2): every rank's FP8 gradient lives in a symmetric,
+//   IPC-mapped buffer. ONE kernel per rank pulls chunk r from all peers over
+//   NVLink (peer loads), reduces in FP32 in ascending rank order, requantizes,
+//   and pushes the result into chunk r of every peer's buffer (peer stores):
+//   the transfer overlaps the reduction tile by tile. Chunk r of peer s is
+//   read and written only by rank r, so the only cross-GPU synchronisation is
+//   a start barrier (inputs final) and an end barrier (all chunks written),
+//   both as system-scope release/acquire flags with a timeout.
+//
+// Chunk ownership follows ChunkAssignment::block_aligned (collective.hpp:
+// 23-39); results do not depend on it (per-block reduce, sender-rank order).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "agq_grad.cuh"
+
+namespace agqh {
+agq_status reduce_requant_device(int np, const uint8_t* const* pc, const float* const* ps,
+                                 uint64_t len, uint32_t block, int nout, uint8_t* const* oc,
+                                 float* const* os, long long blk_base, agq_errors* err,
+                                 cudaStream_t s);
+void chunk_ranges(uint64_t n, uint32_t block, int workers, uint64_t* ranges);
+}  // namespace agqh
+
+// NCCL is resolved at run time: reuse the libnccl.so.2 already loaded in the
+// process (e.g. torch's) so two NCCL builds never mix, else load the system
+// one. The library itself therefore loads without NCCL present.
+namespace {
+struct NcclApi {
+  decltype(&ncclGetUniqueId) GetUniqueId;
+  decltype(&ncclCommInitRank) CommInitRank;
+  decltype(&ncclCommDestroy) CommDestroy;
+  decltype(&ncclGroupStart) GroupStart;
+  decltype(&ncclGroupEnd) GroupEnd;
+  decltype(&ncclSend) Send;
+  decltype(&ncclRecv) Recv;
+  decltype(&ncclAllReduce) AllReduce;
+  decltype(&ncclGetErrorString) GetErrorString;
+  bool ok = false;
+};
+const NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) return;
+#define AGQ_NCCL_SYM(f) api.f = reinterpret_cast<decltype(api.f)>(dlsym(h, "nccl" #f))
+    AGQ_NCCL_SYM(GetUniqueId);
+    AGQ_NCCL_SYM(CommInitRank);
+    AGQ_NCCL_SYM(CommDestroy);
+    AGQ_NCCL_SYM(GroupStart);
+    AGQ_NCCL_SYM(GroupEnd);
+    AGQ_NCCL_SYM(Send);
+    AGQ_NCCL_SYM(Recv);
+    AGQ_NCCL_SYM(AllReduce);
+    AGQ_NCCL_SYM(GetErrorString);
+#undef AGQ_NCCL_SYM
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.GroupStart &&
+             api.GroupEnd && api.Send && api.Recv && api.AllReduce && api.GetErrorString;
+  });
+  return api;
+}
+}  // namespace
+
+// Symmetric buffer layout (identical offsets on every rank).
+namespace {
+constexpr size_t kFlagsBytes = 4096;  // ready[16] | done[16] | err words
+constexpr int kReadyOff = 0, kDoneOff = 16;
+size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+}  // namespace
+
+struct agq_comm {
+  ncclComm_t nccl = nullptr;
+  int nranks = 0, rank = 0, device = 0;
+  // v1 workspace
+  uint8_t* recv_codes = nullptr;
+  float* recv_scales = nullptr;
+  uint64_t recv_chunk_cap = 0;  // elements per peer slot
+  // v2 symmetric memory
+  unsigned char* sym = nullptr;
+  size_t sym_bytes = 0;
+  uint64_t sym_cap = 0;  // elements
+  unsigned char* peer[AGQ_MAX_WORLD] = {};
+  bool p2p_ready = false;
+  unsigned int* done_counter = nullptr;  // local, per kernel
+  uint64_t epoch = 0;
+};
+
+namespace agqk {
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+struct FusedArgs {
+  unsigned char* base[AGQ_MAX_WORLD];  // symmetric buffer of every rank (self included)
+  uint64_t scales_off, codes_off;      // byte offsets inside the buffer
+  uint64_t begin, len;                 // my chunk (elements, block aligned)
+  uint64_t epoch;
+  unsigned int* done_counter;
+  agq_errors* err;
+  int rank, P;
+};
+
+// Spin until flag >= epoch; returns false on timeout (20 s).
+__device__ bool wait_flag(const uint64_t* f, uint64_t epoch) {
+  const uint64_t t0 = globaltimer();
+  while (ld_acquire_sys(f) < epoch) {
+    if (globaltimer() - t0 > 20000000000ull) return false;
+    __nanosleep(200);
+  }
+  return true;
+}
+
+template <int NP>
+__global__ void __launch_bounds__(256) k_fused_allreduce(FusedArgs a) {
+  __shared__ double lut[128];
+  __shared__ int ok;
+  fill_fp8_unit_lut(lut);
+  const int tid = threadIdx.x;
+  uint64_t* my_flags = reinterpret_cast<uint64_t*>(a.base[a.rank]);
+  // start barrier: announce "my input is final" to every rank, then wait for
+  // every rank's announcement (each CTA waits; only CTA 0 announces).
+  if (blockIdx.x == 0 && tid < a.P)
+    st_release_sys(reinterpret_cast<uint64_t*>(a.base[tid]) + kReadyOff + a.rank, a.epoch);
+  if (tid == 0) {
+    ok = 1;
+    for (int s = 0; s < a.P; ++s)
+      if (!wait_flag(my_flags + kReadyOff + s, a.epoch)) ok = 0;
+  }
+  __syncthreads();
+  if (!ok) {
+    if (tid == 0) err_min(&a.err->overflow_block, -1);
+    return;
+  }
+
+  PieceTable pt;
+  pt.np = a.P;
+  pt.nout = a.P;
+  const uint64_t b0 = a.begin / kBlock;
+  for (int s = 0; s < a.P; ++s) {
+    pt.codes[s] = a.base[s] + a.codes_off + a.begin;
+    pt.scales[s] = reinterpret_cast<const float*>(a.base[s] + a.scales_off) + b0;
+    pt.out_codes[s] = a.base[s] + a.codes_off + a.begin;
+    pt.out_scales[s] = reinterpret_cast<float*>(a.base[s] + a.scales_off) + b0;
+  }
+  const uint64_t nblocks = (a.len + kBlock - 1) / kBlock;
+  const uint64_t ngroups = nblocks * 8;
+  const uint64_t gpad = (ngroups + 31) / 32 * 32;
+  const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + tid; g < gpad; g += stride)
+    reduce_group<NP>(pt, g, g < ngroups ? a.len : 0, (long long)b0, lut, a.err, true);
+
+  // end barrier: the last CTA to finish publishes "done" to every rank and
+  // waits for all of them, so the kernel completes only when every chunk of
+  // this rank's buffer has been written.
+  __threadfence_system();
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned int prev = atomicAdd(a.done_counter, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence_system();
+      // share a local-reduce overflow with every rank (runtime_error on all)
+      const long long ov = *reinterpret_cast<volatile long long*>(&a.err->overflow_block);
+      for (int s = 0; s < a.P; ++s) {
+        uint64_t* peer_flags = reinterpret_cast<uint64_t*>(a.base[s]);
+        if (ov != kNone) atomicMin(reinterpret_cast<long long*>(peer_flags + 64 + a.rank), ov);
+      }
+      __threadfence_system();
+      for (int s = 0; s < a.P; ++s)
+        st_release_sys(reinterpret_cast<uint64_t*>(a.base[s]) + kDoneOff + a.rank, a.epoch);
+      bool fine = true;
+      for (int s = 0; s < a.P; ++s)
+        if (!wait_flag(my_flags + kDoneOff + s, a.epoch)) fine = false;
+      for (int s = 0; s < a.P; ++s) {
+        const long long o = *reinterpret_cast<volatile long long*>(my_flags + 64 + s);
+        if (o != kNone) err_min(&a.err->overflow_block, o);
+        // reset for the next epoch
+        *reinterpret_cast<volatile long long*>(my_flags + 64 + s) = kNone;
+      }
+      if (!fine) err_min(&a.err->overflow_block, -1);
+      *a.done_counter = 0u;
+    }
+  }
+}
+
+__global__ void k_init_flags(uint64_t* flags) {
+  const int i = threadIdx.x;
+  if (i < 64) flags[i] = 0;
+  else if (i < 64 + AGQ_MAX_WORLD) flags[i] = (uint64_t)kNone;
+}
+
+}  // namespace agqk
+
+namespace agqh {
+using namespace agqk;
+
+namespace {
+agq_status nccl_fail(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return AGQ_OK;
+  if (!nccl().ok) return set_error(AGQ_ERR_NCCL, "libnccl.so.2 not available");
+  char buf[256];
+  snprintf(buf, sizeof buf, "%s: %s", what, nccl().GetErrorString(r));
+  return set_error(AGQ_ERR_NCCL, buf);
+}
+}  // namespace
+
+agq_status comm_unique_id(unsigned char id[128]) {
+  if (!nccl().ok) return set_error(AGQ_ERR_NCCL, "libnccl.so.2 not available");
+  ncclUniqueId u;
+  agq_status st = nccl_fail(nccl().GetUniqueId(&u), "ncclGetUniqueId");
+  if (st) return st;
+  memcpy(id, u.internal, 128);
+  return AGQ_OK;
+}
+
+agq_status comm_init(agq_comm** out, const unsigned char id[128], int nranks, int rank,
+                     int device) {
+  if (nranks < 1 || nranks > AGQ_MAX_WORLD || rank < 0 || rank >= nranks)
+    return set_error(AGQ_ERR_INVALID_ARGUMENT, "need at least one worker");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "comm_init: cudaSetDevice");
+  if (!nccl().ok) return set_error(AGQ_ERR_NCCL, "libnccl.so.2 not available");
+  ncclUniqueId u;
+  memcpy(u.internal, id, 128);
+  agq_comm* c = new agq_comm();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  agq_status st = nccl_fail(nccl().CommInitRank(&c->nccl, nranks, u, rank), "ncclCommInitRank");
+  if (st) {
+    delete c;
+    return st;
+  }
+  e = cudaMalloc(&c->done_counter, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(c->done_counter, 0, sizeof(unsigned int));
+  if (e != cudaSuccess) return cuda_fail(e, "comm_init: counter");
+  *out = c;
+  return AGQ_OK;
+}
+
+agq_status comm_p2p_export(agq_comm* c, uint64_t capacity, unsigned char handle[256]) {
+  const uint64_t nb = (capacity + kBlock - 1) / kBlock;
+  const size_t bytes = kFlagsBytes + round_up(nb * 4, 256) + round_up(capacity, 256);
+  if (c->sym && c->sym_bytes >= bytes) {
+    // keep the existing mapping
+  } else {
+    if (c->sym) {
+      cudaFree(c->sym);
+      c->sym = nullptr;
+    }
+    cudaError_t e = cudaMalloc(&c->sym, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "p2p_export: cudaMalloc");
+    c->sym_bytes = bytes;
+    k_init_flags<<<1, 128>>>(reinterpret_cast<uint64_t*>(c->sym));
+    count_launch();
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e, "p2p_export: init");
+  }
+  c->sym_cap = capacity;
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, c->sym);
+  if (e != cudaSuccess) return cuda_fail(e, "p2p_export: cudaIpcGetMemHandle");
+  memset(handle, 0, 256);
+  memcpy(handle, &h, sizeof(h));
+  memcpy(handle + 128, &c->sym_bytes, sizeof(size_t));
+  return AGQ_OK;
+}
+
+agq_status comm_p2p_open(agq_comm* c, const unsigned char* handles) {
+  for (int s = 0; s < c->nranks; ++s) {
+    if (s == c->rank) {
+      c->peer[s] = c->sym;
+      continue;
+    }
+    if (c->peer[s] && c->peer[s] != c->sym) cudaIpcCloseMemHandle(c->peer[s]);
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handles + 256 * s, sizeof(h));
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "p2p_open: cudaIpcOpenMemHandle");
+    c->peer[s] = static_cast<unsigned char*>(p);
+  }
+  c->p2p_ready = true;
+  return AGQ_OK;
+}
+
+agq_status comm_p2p_buffers(agq_comm* c, uint8_t** codes, float** scales) {
+  if (!c->sym) return set_error(AGQ_ERR_INVALID_ARGUMENT, "p2p buffers not exported");
+  const uint64_t nb = (c->sym_cap + kBlock - 1) / kBlock;
+  *scales = reinterpret_cast<float*>(c->sym + kFlagsBytes);
+  *codes = c->sym + kFlagsBytes + round_up(nb * 4, 256);
+  return AGQ_OK;
+}
+
+agq_status comm_destroy(agq_comm* c) {
+  if (!c) return AGQ_OK;
+  cudaSetDevice(c->device);
+  for (int s = 0; s < c->nranks; ++s)
+    if (c->peer[s] && c->peer[s] != c->sym) cudaIpcCloseMemHandle(c->peer[s]);
+  if (c->sym) cudaFree(c->sym);
+  if (c->recv_codes) cudaFree(c->recv_codes);
+  if (c->recv_scales) cudaFree(c->recv_scales);
+  if (c->done_counter) cudaFree(c->done_counter);
+  if (c->nccl) nccl().CommDestroy(c->nccl);
+  delete c;
+  return AGQ_OK;
+}
+
+int comm_rank(const agq_comm* c) { return c->rank; }
+int comm_size(const agq_comm* c) { return c->nranks; }
+
+namespace {
+
+agq_status allreduce_nccl(agq_comm* c, uint8_t* codes, float* scales, uint64_t n, uint32_t block,
+                          agq_errors* err, cudaStream_t s) {
+  const int P = c->nranks, r = c->rank;
+  std::vector<uint64_t> rg(2 * P);
+  chunk_ranges(n, block, P, rg.data());
+  uint64_t maxlen = 0;
+  for (int q = 0; q < P; ++q) maxlen = std::max(maxlen, rg[2 * q + 1] - rg[2 * q]);
+  const uint64_t maxblk = (maxlen + block - 1) / block;
+  if (c->recv_chunk_cap < maxlen || !c->recv_codes) {
+    if (c->recv_codes) cudaFree(c->recv_codes);
+    if (c->recv_scales) cudaFree(c->recv_scales);
+    c->recv_codes = nullptr;
+    c->recv_scales = nullptr;
+    const uint64_t slots = P > 1 ? P - 1 : 1;
+    const uint64_t cap = round_up(maxlen ? maxlen : 1, 256);
+    cudaError_t e = cudaMalloc(&c->recv_codes, slots * cap);
+    if (e == cudaSuccess) e = cudaMalloc(&c->recv_scales, slots * round_up(cap / 128 * 4 + 1024, 256));
+    if (e != cudaSuccess) return cuda_fail(e, "allreduce: workspace");
+    c->recv_chunk_cap = cap;
+  }
+  const uint64_t cap = c->recv_chunk_cap;
+  const uint64_t scap = round_up(cap / 128 * 4 + 1024, 256) / 4;
+  (void)maxblk;
+  auto slot = [&](int q) { return q < r ? q : q - 1; };
+  const uint64_t br = rg[2 * r], er = rg[2 * r + 1], lr = er - br;
+  const uint64_t nbr = (lr + block - 1) / block;
+  // 1) all-to-all of chunk q -> rank q
+  agq_status st = nccl_fail(nccl().GroupStart(), "ncclGroupStart");
+  if (st) return st;
+  for (int q = 0; q < P; ++q) {
+    if (q == r) continue;
+    const uint64_t bq = rg[2 * q], lq = rg[2 * q + 1] - bq;
+    if (lq) {
+      nccl().Send(codes + bq, lq, ncclUint8, q, c->nccl, s);
+      nccl().Send(scales + bq / block, (lq + block - 1) / block, ncclFloat32, q, c->nccl, s);
+    }
+    if (lr) {
+      nccl().Recv(c->recv_codes + slot(q) * cap, lr, ncclUint8, q, c->nccl, s);
+      nccl().Recv(c->recv_scales + slot(q) * scap, nbr, ncclFloat32, q, c->nccl, s);
+    }
+  }
+  st = nccl_fail(nccl().GroupEnd(), "all-to-all");
+  if (st) return st;
+  // 2) local reduce of chunk r, pieces in ascending sender rank, in place
+  if (lr) {
+    std::vector<const uint8_t*> pc(P);
+    std::vector<const float*> ps(P);
+    for (int q = 0; q < P; ++q) {
+      if (q == r) {
+        pc[q] = codes + br;
+        ps[q] = scales + br / block;
+      } else {
+        pc[q] = c->recv_codes + slot(q) * cap;
+        ps[q] = c->recv_scales + slot(q) * scap;
+      }
+    }
+    uint8_t* oc = codes + br;
+    float* os = scales + br / block;
+    st = reduce_requant_device(P, pc.data(), ps.data(), lr, block, 1, &oc, &os,
+                               (long long)(br / block), err, s);
+    if (st) return st;
+  }
+  // share an overflow with every rank (collective.hpp:278-281 aborts all)
+  if (err) {
+    st = nccl_fail(nccl().AllReduce(&err->overflow_block, &err->overflow_block, 1, ncclInt64,
+                                 ncclMin, c->nccl, s),
+                   "overflow flag");
+    if (st) return st;
+  }
+  // 3) all-gather: reduced chunk r -> every rank, received in place
+  st = nccl_fail(nccl().GroupStart(), "ncclGroupStart");
+  if (st) return st;
+  for (int q = 0; q < P; ++q) {
+    if (q == r) continue;
+    const uint64_t bq = rg[2 * q], lq = rg[2 * q + 1] - bq;
+    if (lr) {
+      nccl().Send(codes + br, lr, ncclUint8, q, c->nccl, s);
+      nccl().Send(scales + br / block, nbr, ncclFloat32, q, c->nccl, s);
+    }
+    if (lq) {
+      nccl().Recv(codes + bq, lq, ncclUint8, q, c->nccl, s);
+      nccl().Recv(scales + bq / block, (lq + block - 1) / block, ncclFloat32, q, c->nccl, s);
+    }
+  }
+  return nccl_fail(nccl().GroupEnd(), "all-gather");
+}
+
+template <int NP>
+void launch_fused(const FusedArgs& a, int grid, cudaStream_t s) {
+  k_fused_allreduce<NP><<<grid, 256, 0, s>>>(a);
+}
+
+agq_status allreduce_p2p(agq_comm* c, uint8_t* codes, float* scales, uint64_t n, uint32_t block,
+                         agq_errors* err, cudaStream_t s) {
+  if (!c->p2p_ready) return set_error(AGQ_ERR_INVALID_ARGUMENT, "p2p buffers not opened");
+  if (block != (uint32_t)kBlock) return set_error(AGQ_ERR_INVALID_ARGUMENT, "fused all-reduce needs block 128");
+  if (n > c->sym_cap) return set_error(AGQ_ERR_INVALID_ARGUMENT, "all-reduce larger than p2p capacity");
+  if (!err) return set_error(AGQ_ERR_INVALID_ARGUMENT, "fused all-reduce needs an error record");
+  uint8_t* sc_codes;
+  float* sc_scales;
+  comm_p2p_buffers(c, &sc_codes, &sc_scales);
+  const uint64_t nb = (n + block - 1) / block;
+  const bool inplace = codes == sc_codes && scales == sc_scales;
+  if (!inplace) {
+    cudaMemcpyAsync(sc_codes, codes, n, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(sc_scales, scales, nb * 4, cudaMemcpyDeviceToDevice, s);
+  }
+  const int P = c->nranks, r = c->rank;
+  std::vector<uint64_t> rg(2 * P);
+  chunk_ranges(n, block, P, rg.data());
+  FusedArgs a{};
+  for (int q = 0; q < P; ++q) a.base[q] = c->peer[q];
+  a.scales_off = kFlagsBytes;
+  a.codes_off = (uint64_t)(reinterpret_cast<unsigned char*>(sc_codes) - c->sym);
+  a.begin = rg[2 * r];
+  a.len = rg[2 * r + 1] - rg[2 * r];
+  a.epoch = ++c->epoch;
+  a.done_counter = c->done_counter;
+  a.err = err;
+  a.rank = r;
+  a.P = P;
+  const uint64_t groups = (a.len + kBlock - 1) / kBlock * 8;
+  uint64_t grid = (groups + 255) / 256;
+  const uint64_t cap = (uint64_t)num_sms() * 4;  // co-resident (256 thr, small smem)
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  switch (P) {
+    case 1: launch_fused<1>(a, (int)grid, s); break;
+    case 2: launch_fused<2>(a, (int)grid, s); break;
+    case 3: launch_fused<3>(a, (int)grid, s); break;
+    case 4: launch_fused<4>(a, (int)grid, s); break;
+    case 5: launch_fused<5>(a, (int)grid, s); break;
+    case 6: launch_fused<6>(a, (int)grid, s); break;
+    case 7: launch_fused<7>(a, (int)grid, s); break;
+    case 8: launch_fused<8>(a, (int)grid, s); break;
+    default: launch_fused<0>(a, (int)grid, s); break;
+  }
+  count_launch();
+  agq_status st = cuda_fail(cudaGetLastError(), "fused all-reduce: launch");
+  if (st) return st;
+  if (!inplace) {
+    cudaMemcpyAsync(codes, sc_codes, n, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(scales, sc_scales, nb * 4, cudaMemcpyDeviceToDevice, s);
+  }
+  return AGQ_OK;
+}
+
+}  // namespace
+
+agq_status allreduce_fp8(agq_comm* c, uint8_t* codes, float* scales, uint64_t n, uint32_t block,
+                         int algo, agq_errors* err, cudaStream_t s) {
+  if (n == 0) return AGQ_OK;
+  if (c->nranks == 1) {
+    // P = 1: the reference still re-quantizes acc = 0 + dequant (signed
+    // zeros normalise), so run the reduce with one piece.
+    const uint8_t* pc = codes;
+    const float* ps = scales;
+    return reduce_requant_device(1, &pc, &ps, n, block, 1, &codes, &scales, 0, err, s);
+  }
+  if (algo == AGQ_AR_FUSED_P2P) return allreduce_p2p(c, codes, scales, n, block, err, s);
+  return allreduce_nccl(c, codes, scales, n, block, err, s);
+}
+
+agq_status allreduce_bf16_nccl(agq_comm* c, void* data, uint64_t n, cudaStream_t s) {
+  return nccl_fail(nccl().AllReduce(data, data, n, ncclBfloat16, ncclSum, c->nccl, s),
+                   "ncclAllReduce(bf16)");
+}
+
+}  // namespace agqh

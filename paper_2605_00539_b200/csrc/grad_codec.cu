@@ -1,0 +1,456 @@
+// L2a gradient path on sm_100a: fused FP8-E4M3 accumulate (K3) and the
+// local reduce + requantize of the decomposed all-reduce (K4).
+//
+// Reference: /root/reference/proj/include/agq/collective.hpp:101-147
+// (round_bf16/round_fp16, local_accumulate) and :250-284 (local reduce).
+// Both produce codes/scales bit-identical to the reference:
+//   dequant  = (float)(fl64(e4m3(c)/448) * (double)scale)   (DMUL + F2F)
+//   sum      = fp32 adds in the reference's order (+0.0f first for K4)
+//   requant  = fresh block absmax, exact E4M3 rounding (agq_numerics.cuh)
+//
+// K3 tiled path (block 128): 512-thread CTAs, two per SM, 16 elements per
+// thread (8 threads per block), 8192-element tiles double-buffered through
+// shared memory by 1-D TMA bulk loads (codes + scales + local gradient in
+// one mbarrier transaction) and drained by bulk stores. One pass over HBM:
+// 1 + 4/128 bytes in, 4 (or 2) bytes of local gradient in, 1 + 4/128 out.
+//
+// K4 uses plain 128-bit loads so that any piece may live in another GPU's
+// memory (NVLink peer pointers) — the fused all-reduce runs the same code.
+#include "agq_grad.cuh"
+
+namespace agqk {
+
+// ---------------------------------------------------------------------------
+// K3: tiled fused accumulate
+// ---------------------------------------------------------------------------
+constexpr int kAccThreads = 512;
+
+template <bool BF16L, int PREC>
+__global__ void __launch_bounds__(kAccThreads, 2)
+    k_accumulate_tiled(const uint8_t* codes, const float* scales, const void* local,
+                       uint64_t ntiles, uint8_t* out_codes, float* out_scales,
+                       agq_errors* err) {
+  constexpr int kStages = 2;
+  constexpr uint32_t kCodeB = kTileElems;                 // 8192
+  constexpr uint32_t kScB = kTileBlocks * 4;              // 256
+  constexpr uint32_t kLocB = kTileElems * (BF16L ? 2 : 4);
+  constexpr uint32_t kStageB = kCodeB + kScB + kLocB;
+  constexpr uint32_t kOutB = kCodeB + kScB;
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* in_buf = smem;
+  unsigned char* out_buf = smem + kStages * kStageB;
+  double* lut = reinterpret_cast<double*>(out_buf + 2 * kOutB);
+  uint64_t* full = reinterpret_cast<uint64_t*>(lut + 128);
+
+  const int tid = threadIdx.x;
+  const uint64_t policy = policy_evict_first();
+  fill_fp8_unit_lut(lut);
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue_load = [&](uint64_t t, int s) {
+    unsigned char* d = in_buf + s * kStageB;
+    mbar_arrive_expect_tx(&full[s], kStageB);
+    bulk_g2s(d, codes + t * kCodeB, kCodeB, &full[s], policy);
+    bulk_g2s(d + kCodeB, scales + t * kTileBlocks, kScB, &full[s], policy);
+    bulk_g2s(d + kCodeB + kScB, static_cast<const unsigned char*>(local) + t * kLocB, kLocB,
+             &full[s], policy);
+  };
+  if (tid == 0)
+    for (int s = 0; s < kStages; ++s) {
+      const uint64_t t = blockIdx.x + (uint64_t)s * gridDim.x;
+      if (t < ntiles) issue_load(t, s);
+    }
+
+  // f32 local: 4 chunks of 4 elements, rotation (tid>>1)&3 (conflict-free
+  // 64-byte rows); bf16 local: 2 chunks of 8, rotation (tid>>2)&1. Code
+  // words (4 codes each) are rotated to match: r = rot (f32) / 2*rot (bf16).
+  const int rot = BF16L ? ((tid >> 2) & 1) : ((tid >> 1) & 3);
+  const int wrot = BF16L ? 2 * rot : rot;
+  const int lblk = tid >> 3;
+
+  for (uint64_t it = 0;; ++it) {
+    const uint64_t t = blockIdx.x + it * gridDim.x;
+    if (t >= ntiles) break;
+    const int s = (int)(it % kStages);
+    mbar_wait(&full[s], (uint32_t)((it / kStages) & 1));
+    const unsigned char* sb = in_buf + s * kStageB;
+    const uint4 cv = lds128(sb + tid * 16);
+    uint32_t cw[4] = {cv.x, cv.y, cv.z, cv.w};
+    rotl4(cw, wrot);
+    const float sc = reinterpret_cast<const float*>(sb + kCodeB)[lblk];
+    const unsigned char* lrow = sb + kCodeB + kScB + tid * (BF16L ? 32 : 64);
+    float l[16];
+    if constexpr (BF16L) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const uint4 v = lds128(lrow + ((j + rot) & 1) * 16);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          l[8 * j + 2 * k] = u2f(w[k] << 16);
+          l[8 * j + 2 * k + 1] = u2f(w[k] & 0xffff0000u);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint4 v = lds128(lrow + ((j + rot) & 3) * 16);
+        l[4 * j] = u2f(v.x); l[4 * j + 1] = u2f(v.y);
+        l[4 * j + 2] = u2f(v.z); l[4 * j + 3] = u2f(v.w);
+      }
+    }
+    const uint64_t gblk = t * kTileBlocks + lblk;
+    if (!(sc >= 0.0f) || !(sc <= 3.402823466e38f)) {
+      if ((tid & 7) == 0) err_min(&err->bad_scale_block, (long long)gblk);
+    }
+    const double sd = (double)sc;
+    float v[16];
+    uint32_t lbad = 0;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const uint32_t c = (cw[e >> 2] >> (8 * (e & 3))) & 0xffu;
+      lbad |= (uint32_t)((f2u(l[e]) & 0x7f800000u) == 0x7f800000u) << e;
+      v[e] = apply_prec<PREC>(fadd(fp8_dequant(c, sd, lut), l[e]));
+    }
+    if (lbad) {
+      // lowest non-finite local element of this thread (slot order -> index)
+      for (int e = 0; e < 16; ++e)
+        if (lbad >> e & 1) {
+          const int per = BF16L ? 8 : 4, nch = BF16L ? 2 : 4;
+          const int slot = e / per, within = e % per;
+          const int chunk = (slot + rot) & (nch - 1);
+          err_min(&err->nonfinite_local,
+                  (long long)(t * kTileElems + tid * 16 + chunk * per + within));
+        }
+    }
+    const uint32_t m = absmax_bits16(v);
+    if (m >= 0x7f800000u && (tid & 7) == 0) err_min(&err->nonfinite_block, (long long)gblk);
+    const float a = u2f(m);
+    uint32_t ow[4];
+    fp8_requant16(v, a, ow);
+    rotr4(ow, wrot);
+
+    const int ob = (int)(it & 1);
+    if (tid == 0) bulk_wait_read<1>();
+    __syncthreads();
+    unsigned char* obuf = out_buf + ob * kOutB;
+    sts128(obuf + tid * 16, make_uint4(ow[0], ow[1], ow[2], ow[3]));
+    if ((tid & 7) == 0) reinterpret_cast<float*>(obuf + kCodeB)[lblk] = a;
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      bulk_s2g(out_codes + t * kCodeB, obuf, kCodeB);
+      bulk_s2g(out_scales + t * kTileBlocks, obuf + kCodeB, kScB);
+      bulk_commit();
+      const uint64_t nt = t + (uint64_t)kStages * gridDim.x;
+      if (nt < ntiles) issue_load(nt, s);
+    }
+  }
+  if (tid == 0) bulk_wait_all<0>();
+}
+
+// ---------------------------------------------------------------------------
+// Generic accumulate / reduce (any block size): one warp per block, two
+// passes (absmax, then encode from recomputed — identical — sums).
+// ---------------------------------------------------------------------------
+template <int PREC>
+__global__ void k_accumulate_generic(const uint8_t* codes, const float* scales,
+                                     const void* local, int bf16l, uint64_t n,
+                                     uint32_t block, uint64_t nblocks, uint8_t* out_codes,
+                                     float* out_scales, long long elem_base,
+                                     agq_errors* err) {
+  __shared__ double lut[128];
+  fill_fp8_unit_lut(lut);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+  auto loc = [&](uint64_t i) -> float {
+    return bf16l ? u2f((uint32_t)static_cast<const uint16_t*>(local)[i] << 16)
+                 : static_cast<const float*>(local)[i];
+  };
+  for (uint64_t b = warp; b < nblocks; b += nwarps) {
+    const uint64_t beg = b * block, end = min(n, beg + block);
+    const float sc = scales[b];
+    const long long gb = (elem_base + (long long)beg) / block;
+    if (lane == 0 && (!(sc >= 0.0f) || !(sc <= 3.402823466e38f))) err_min(&err->bad_scale_block, gb);
+    const double sd = (double)sc;
+    uint32_t m = 0;
+    for (uint64_t i = beg + lane; i < end; i += 32) {
+      const float l = loc(i);
+      if ((f2u(l) & 0x7f800000u) == 0x7f800000u) err_min(&err->nonfinite_local, elem_base + (long long)i);
+      const float s = apply_prec<PREC>(fadd(fp8_dequant(codes[i], sd, lut), l));
+      m = max(m, f2u(s) & 0x7fffffffu);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const float a = u2f(m);
+    if (lane == 0 && m >= 0x7f800000u) err_min(&err->nonfinite_block, gb);
+    const bool ok = m < 0x7f800000u;
+    const float inv = ok && m ? fdiv(448.0f, a) : 0.0f;
+    for (uint64_t i = beg + lane; i < end; i += 32) {
+      const float s = apply_prec<PREC>(fadd(fp8_dequant(codes[i], sd, lut), loc(i)));
+      out_codes[i] = (uint8_t)(m == 0 || !ok ? 0u : encode_f32(2, 8, s, a, inv));
+    }
+    __syncwarp();
+    if (lane == 0) out_scales[b] = a;
+  }
+}
+
+__global__ void k_reduce_generic(PieceTable pt, uint64_t len, uint32_t block, uint64_t nblocks,
+                                 long long blk_base, agq_errors* err) {
+  __shared__ double lut[128];
+  fill_fp8_unit_lut(lut);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+  for (uint64_t b = warp; b < nblocks; b += nwarps) {
+    const uint64_t beg = b * block, end = min(len, beg + block);
+    uint32_t m = 0;
+    for (int p = 0; p < pt.np; ++p) {
+      const float sc = pt.scales[p][b];
+      if (lane == 0 && (!(sc >= 0.0f) || !(sc <= 3.402823466e38f)))
+        err_min(&err->bad_scale_block, blk_base + (long long)b);
+    }
+    for (uint64_t i = beg + lane; i < end; i += 32) {
+      float acc = 0.0f;
+      for (int p = 0; p < pt.np; ++p)
+        acc = fadd(acc, fp8_dequant(pt.codes[p][i], (double)pt.scales[p][b], lut));
+      m = max(m, f2u(acc) & 0x7fffffffu);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const float a = u2f(m);
+    if (lane == 0 && m >= 0x7f800000u) err_min(&err->overflow_block, blk_base + (long long)b);
+    const bool ok = m < 0x7f800000u;
+    const float inv = ok && m ? fdiv(448.0f, a) : 0.0f;
+    for (uint64_t i = beg + lane; i < end; i += 32) {
+      float acc = 0.0f;
+      for (int p = 0; p < pt.np; ++p)
+        acc = fadd(acc, fp8_dequant(pt.codes[p][i], (double)pt.scales[p][b], lut));
+      const uint8_t c = (uint8_t)(m == 0 || !ok ? 0u : encode_f32(2, 8, acc, a, inv));
+      for (int o = 0; o < pt.nout; ++o) pt.out_codes[o][i] = c;
+    }
+    __syncwarp();
+    if (lane == 0)
+      for (int o = 0; o < pt.nout; ++o) pt.out_scales[o][b] = a;
+  }
+}
+
+template <int NP>
+__global__ void __launch_bounds__(256)
+    k_reduce128(PieceTable pt, uint64_t len, long long blk_base, int vec, agq_errors* err) {
+  __shared__ double lut[128];
+  fill_fp8_unit_lut(lut);
+  __syncthreads();
+  const uint64_t nblocks = (len + kBlock - 1) / kBlock;
+  const uint64_t ngroups = nblocks * 8;
+  const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
+  // warp-uniform trip count so the 8-lane shuffles always have all lanes
+  const uint64_t gpad = (ngroups + 31) / 32 * 32;
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < gpad; g += stride)
+    reduce_group<NP>(pt, g, g < ngroups ? len : 0, blk_base, lut, err, vec != 0);
+}
+
+// ---------------------------------------------------------------------------
+// allreduce_naive_fp8 strawman (collective.hpp:338-431), simulated on one
+// device: P-1 ring steps adding in FP8 at the receiver's ORIGINAL scales.
+// One thread per element runs the ring for that element (elements are
+// independent; each step reads the snapshot of the previous step).
+// ---------------------------------------------------------------------------
+__global__ void k_naive_ring(PieceTable pt, uint64_t n, uint32_t block, const uint64_t* ranges,
+                             uint8_t* out_codes, float* out_scales, agq_errors* err) {
+  __shared__ double lut[128];
+  fill_fp8_unit_lut(lut);
+  __syncthreads();
+  const int P = pt.np;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += gridDim.x * (uint64_t)blockDim.x) {
+    const uint64_t blk = i / block;
+    int chunk = 0;
+    for (int c = 0; c < P; ++c)
+      if (i >= ranges[2 * c] && i < ranges[2 * c + 1]) chunk = c;
+    // working state of every rank for this element
+    uint8_t wc[AGQ_MAX_WORLD];
+    float ws[AGQ_MAX_WORLD];
+    for (int r = 0; r < P; ++r) {
+      wc[r] = pt.codes[r][i];
+      ws[r] = pt.scales[r][blk];
+    }
+    bool sat = false;
+    for (int step = 0; step < P - 1; ++step) {
+      // rank r updates chunk (r - step - 1) mod P with the message of r-1
+      uint8_t nc[AGQ_MAX_WORLD];
+      for (int r = 0; r < P; ++r) nc[r] = wc[r];
+      for (int r = 0; r < P; ++r) {
+        const int ch = ((r - step - 1) % P + P) % P;
+        if (ch != chunk) continue;
+        const int from = (r - 1 + P) % P;
+        const double unit_in = lut[wc[from] & 0x7f] * (wc[from] & 0x80 ? -1.0 : 1.0);
+        const double inc = unit_in * (double)ws[from];
+        const double loc = lut[wc[r] & 0x7f] * (wc[r] & 0x80 ? -1.0 : 1.0) * (double)ws[r];
+        const double sum = inc + loc;
+        const float scale = pt.scales[r][blk];
+        const double unit = scale == 0.0f ? 0.0 : sum / (double)scale;
+        bool over = (scale == 0.0f && sum != 0.0);
+        const double w = unit * 448.0;
+        if (fabs(w) > 448.0) over = true;
+        nc[r] = (uint8_t)fp8_encode_double(w);
+        if (over) sat = true;
+      }
+      for (int r = 0; r < P; ++r) wc[r] = nc[r];
+    }
+    const int owner = P == 1 ? 0 : (chunk - 1 + P) % P;
+    out_codes[i] = wc[owner];
+    if (i % block == 0 || i == ranges[2 * chunk]) out_scales[blk] = pt.scales[owner][blk];
+    if (sat) atomicAdd(&err->saturated, 1ull);
+  }
+}
+
+}  // namespace agqk
+
+// ===========================================================================
+// Host launchers
+// ===========================================================================
+namespace agqh {
+using namespace agqk;
+
+namespace {
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+int gen_grid(uint64_t work, int threads) {
+  const uint64_t g = (work + threads - 1) / threads;
+  const uint64_t cap = (uint64_t)num_sms() * 16;
+  return (int)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+template <bool BF16L, int PREC>
+agq_status launch_acc_tiled(const uint8_t* codes, const float* scales, const void* local,
+                            uint64_t ntiles, uint8_t* oc, float* os, agq_errors* err,
+                            cudaStream_t s) {
+  const size_t stage = kTileElems + kTileBlocks * 4 + (size_t)kTileElems * (BF16L ? 2 : 4);
+  const size_t smem = 2 * stage + 2 * (kTileElems + kTileBlocks * 4) + 128 * 8 + 2 * 8;
+  auto k = k_accumulate_tiled<BF16L, PREC>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return cuda_fail(e, "accumulate: smem attribute");
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kAccThreads, smem);
+  if (occ < 1) occ = 1;
+  const uint64_t g = (uint64_t)num_sms() * occ;
+  k<<<(int)(ntiles < g ? ntiles : g), kAccThreads, smem, s>>>(codes, scales, local, ntiles, oc,
+                                                               os, err);
+  count_launch();
+  return cuda_fail(cudaGetLastError(), "accumulate: launch");
+}
+
+template <bool BF16L>
+agq_status acc_tiled_prec(int prec, const uint8_t* codes, const float* scales,
+                          const void* local, uint64_t ntiles, uint8_t* oc, float* os,
+                          agq_errors* err, cudaStream_t s) {
+  if (prec == AGQ_ACC_BF16) return launch_acc_tiled<BF16L, AGQ_ACC_BF16>(codes, scales, local, ntiles, oc, os, err, s);
+  if (prec == AGQ_ACC_FP16) return launch_acc_tiled<BF16L, AGQ_ACC_FP16>(codes, scales, local, ntiles, oc, os, err, s);
+  return launch_acc_tiled<BF16L, AGQ_ACC_FP32>(codes, scales, local, ntiles, oc, os, err, s);
+}
+
+template <int NP>
+void launch_reduce128(const PieceTable& pt, uint64_t len, long long bb, int vec, agq_errors* err,
+                      cudaStream_t s) {
+  const uint64_t groups = (len + kBlock - 1) / kBlock * 8;
+  int grid = gen_grid(groups, 256);
+  k_reduce128<NP><<<grid, 256, 0, s>>>(pt, len, bb, vec, err);
+}
+}  // namespace
+
+agq_status accumulate_device(const uint8_t* codes, const float* scales, const void* local,
+                             int local_dtype, uint64_t n, uint32_t block, int prec,
+                             uint8_t* oc, float* os, agq_errors* err, cudaStream_t s) {
+  if (n == 0) return AGQ_OK;
+  const bool bf16l = local_dtype == AGQ_BF16;
+  uint64_t ntiles = 0;
+  if (block == (uint32_t)kBlock && aligned16(codes) && aligned16(scales) && aligned16(local) &&
+      aligned16(oc) && aligned16(os))
+    ntiles = n / kTileElems;
+  if (ntiles) {
+    agq_status r = bf16l ? acc_tiled_prec<true>(prec, codes, scales, local, ntiles, oc, os, err, s)
+                         : acc_tiled_prec<false>(prec, codes, scales, local, ntiles, oc, os, err, s);
+    if (r != AGQ_OK) return r;
+  }
+  const uint64_t done = ntiles * kTileElems;
+  if (done == n) return AGQ_OK;
+  const uint64_t rest = n - done, nb = (rest + block - 1) / block;
+  const void* ltail = static_cast<const char*>(local) + done * (bf16l ? 2 : 4);
+  const int grid = gen_grid(nb * 32, 256);
+  const long long base = (long long)done;
+  if (prec == AGQ_ACC_BF16)
+    k_accumulate_generic<AGQ_ACC_BF16><<<grid, 256, 0, s>>>(codes + done, scales + done / block, ltail,
+        bf16l, rest, block, nb, oc + done, os + done / block, base, err);
+  else if (prec == AGQ_ACC_FP16)
+    k_accumulate_generic<AGQ_ACC_FP16><<<grid, 256, 0, s>>>(codes + done, scales + done / block, ltail,
+        bf16l, rest, block, nb, oc + done, os + done / block, base, err);
+  else
+    k_accumulate_generic<AGQ_ACC_FP32><<<grid, 256, 0, s>>>(codes + done, scales + done / block, ltail,
+        bf16l, rest, block, nb, oc + done, os + done / block, base, err);
+  count_launch();
+  return cuda_fail(cudaGetLastError(), "accumulate (generic): launch");
+}
+
+agq_status reduce_requant_device(int np, const uint8_t* const* pc, const float* const* ps,
+                                 uint64_t len, uint32_t block, int nout, uint8_t* const* oc,
+                                 float* const* os, long long blk_base, agq_errors* err,
+                                 cudaStream_t s) {
+  if (len == 0) return AGQ_OK;
+  PieceTable pt{};
+  pt.np = np;
+  pt.nout = nout;
+  bool vec = true;
+  for (int p = 0; p < np; ++p) {
+    pt.codes[p] = pc[p];
+    pt.scales[p] = ps[p];
+    vec = vec && aligned16(pc[p]);
+  }
+  for (int o = 0; o < nout; ++o) {
+    pt.out_codes[o] = oc[o];
+    pt.out_scales[o] = os[o];
+    vec = vec && aligned16(oc[o]);
+  }
+  if (block == (uint32_t)kBlock) {
+    switch (np) {
+      case 1: launch_reduce128<1>(pt, len, blk_base, vec, err, s); break;
+      case 2: launch_reduce128<2>(pt, len, blk_base, vec, err, s); break;
+      case 3: launch_reduce128<3>(pt, len, blk_base, vec, err, s); break;
+      case 4: launch_reduce128<4>(pt, len, blk_base, vec, err, s); break;
+      case 5: launch_reduce128<5>(pt, len, blk_base, vec, err, s); break;
+      case 6: launch_reduce128<6>(pt, len, blk_base, vec, err, s); break;
+      case 7: launch_reduce128<7>(pt, len, blk_base, vec, err, s); break;
+      case 8: launch_reduce128<8>(pt, len, blk_base, vec, err, s); break;
+      default: launch_reduce128<0>(pt, len, blk_base, vec, err, s); break;
+    }
+  } else {
+    const uint64_t nb = (len + block - 1) / block;
+    k_reduce_generic<<<gen_grid(nb * 32, 256), 256, 0, s>>>(pt, len, block, nb, blk_base, err);
+  }
+  count_launch();
+  return cuda_fail(cudaGetLastError(), "reduce-requant: launch");
+}
+
+agq_status naive_ring_device(int world, const uint8_t* const* codes, const float* const* scales,
+                             uint64_t n, uint32_t block, const uint64_t* d_ranges,
+                             uint8_t* oc, float* os, agq_errors* err, cudaStream_t s) {
+  if (n == 0) return AGQ_OK;
+  PieceTable pt{};
+  pt.np = world;
+  for (int r = 0; r < world; ++r) {
+    pt.codes[r] = codes[r];
+    pt.scales[r] = scales[r];
+  }
+  k_naive_ring<<<gen_grid(n, 256), 256, 0, s>>>(pt, n, block, d_ranges, oc, os, err);
+  count_launch();
+  return cuda_fail(cudaGetLastError(), "naive ring: launch");
+}
+
+}  // namespace agqh

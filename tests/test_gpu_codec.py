@@ -1,0 +1,228 @@
+"""GPU parity of the L1 block codec (K1 quantize+pack, K2 unpack+dequantize)
+against the reference: the golden fixture made by the reference itself, the
+C oracle on seeded inputs, and exhaustive element classes run ON the B200.
+Bit-exact: codes, scales, packed bytes, FP32 dequantized values."""
+import numpy as np
+import pytest
+import torch
+
+import oracle_ffi as O
+import paper_2605_00539_b200 as A
+
+pytestmark = pytest.mark.gpu
+CODECS = [(A.CodecKind.SymmetricLinear, b) for b in (4, 5, 6, 7, 8)] + \
+         [(A.CodecKind.Fp4E2M1, 4), (A.CodecKind.Fp8E4M3, 8)]
+
+
+def t(x, dev, dtype=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(dev).to(dtype)
+
+
+def u32(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def check_q(q, codes, scales, bits):
+    got_s = q.scales.cpu().numpy()
+    assert np.array_equal(u32(got_s), u32(scales))
+    if q.packed:
+        assert np.array_equal(q.codes.cpu().numpy(), O.pack(codes, bits))
+    else:
+        assert np.array_equal(q.codes.cpu().numpy(), codes)
+
+
+@pytest.mark.parametrize("name", ["x_cli", "x_cli_bf16", "x_codec", "x_ragged"])
+@pytest.mark.parametrize("block", [128, 16, 1000])
+def test_golden(cuda, golden, name, block):
+    x = golden[name]
+    for kind, bits in CODECS:
+        key = f"{name}_c{int(kind)}_b{bits}_k{block}"
+        for packed in (True, False):
+            q = A.quantize_blockwise(t(x, cuda), bits, block, kind, packed=packed)
+            check_q(q, golden[key + "_codes"], golden[key + "_scales"], bits)
+            d = A.dequantize_blockwise(q).cpu().numpy()
+            assert np.array_equal(u32(d), u32(golden[key + "_deq"])), key
+        if name == "x_cli_bf16":  # BF16 input path gives the same codes
+            q = A.quantize_blockwise(t(x, cuda, torch.bfloat16), bits, block, kind)
+            check_q(q, golden[key + "_codes"], golden[key + "_scales"], bits)
+            d = A.dequantize_blockwise(q, torch.bfloat16).float().cpu().numpy()
+            assert np.array_equal(u32(d), u32(O.bf16_round(golden[key + "_deq"]))), key
+
+
+def _random_case(rng, n, bf16):
+    x = (rng.standard_normal(n) * 10.0 ** rng.uniform(-3, 3)).astype(np.float32)
+    x[rng.integers(0, n, size=max(1, n // 50))] = 0.0
+    nb = (n + 127) // 128
+    if nb > 3:  # per-block magnitudes, zero blocks, extreme-scale blocks
+        scale = 10.0 ** rng.uniform(-6, 6, size=nb)
+        scale[rng.integers(0, nb, size=max(1, nb // 20))] = 0.0
+        scale[1] = 1e-25
+        scale[2] = 1e25
+        x = (x * np.repeat(scale, 128)[:n]).astype(np.float32)
+    return O.bf16_round(x) if bf16 else x
+
+
+@pytest.mark.parametrize("n", [1, 127, 128, 8191, 8192, 8192 * 3 + 129, 100003])
+@pytest.mark.parametrize("bf16", [True, False])
+def test_random_vs_oracle(cuda, n, bf16):
+    rng = np.random.default_rng(n + bf16)
+    x = _random_case(rng, n, bf16)
+    xt = t(x, cuda, torch.bfloat16 if bf16 else torch.float32)
+    for kind, bits in CODECS:
+        c, s = O.quantize(x, bits, 128, int(kind))
+        for packed in (True, False):
+            q = A.quantize_blockwise(xt, bits, 128, kind, packed=packed)
+            check_q(q, c, s, bits)
+            d = A.dequantize_blockwise(q).cpu().numpy()
+            assert np.array_equal(u32(d), u32(O.dequantize(c, s, bits, 128, int(kind))))
+            db = A.dequantize_blockwise(q, torch.bfloat16).float().cpu().numpy()
+            assert np.array_equal(u32(db), u32(O.bf16_round(O.dequantize(c, s, bits, 128, int(kind)))))
+
+
+def test_misaligned_pointers_take_generic_path(cuda):
+    rng = np.random.default_rng(9)
+    x = _random_case(rng, 3 * 8192 + 5, True)
+    base = t(np.concatenate([[0.0], x]).astype(np.float32), cuda, torch.bfloat16)
+    xt = base[1:]  # 2-byte offset: not 16-byte aligned
+    for kind, bits in CODECS:
+        c, s = O.quantize(x, bits, 128, int(kind))
+        check_q(A.quantize_blockwise(xt, bits, 128, kind), c, s, bits)
+
+
+def test_c1_full_size(cuda):
+    """Config C1: 4096x4096 BF16, INT4 block 128, reference RNG inputs."""
+    if O.ref is None:
+        pytest.skip("reference RNG lib absent")
+    x = O.bf16_round(O.ref_normal(1, 0x1D, 0, 4096 * 4096))
+    q = A.quantize_blockwise(t(x, cuda, torch.bfloat16), 4, 128)
+    c, s = O.quantize(x, 4, 128)
+    check_q(q, c, s, 4)
+    d = A.dequantize_blockwise(q, torch.bfloat16).float().cpu().numpy()
+    assert np.array_equal(u32(d), u32(O.bf16_round(O.dequantize(c, s, 4))))
+
+
+def test_nonfinite_reports_lowest_block(cuda):
+    x = np.random.default_rng(8).standard_normal(300).astype(np.float32)
+    x[170] = np.inf
+    with pytest.raises(A.InvalidArgument, match="non-finite input element in block 1"):
+        A.quantize_blockwise(t(x, cuda), 4, 128)
+    y = np.random.default_rng(1).standard_normal(8192 * 4).astype(np.float32)
+    y[8192 * 2 + 300] = np.nan
+    y[8192 * 3 + 5] = -np.inf
+    with pytest.raises(A.InvalidArgument, match="block 130$"):
+        A.quantize_blockwise(t(y, cuda, torch.bfloat16), 5, 128)
+
+
+def test_validate_errors(cuda):
+    q = A.quantize_blockwise(t(np.ones(300, np.float32), cuda), 5, 128, packed=False)
+    q.codes[7] = 200
+    with pytest.raises(A.InvalidArgument, match="code out of range at 7"):
+        A.dequantize_blockwise(q)
+    q = A.quantize_blockwise(t(np.ones(300, np.float32), cuda), 5, 128)
+    q.scales[2] = -1.0
+    with pytest.raises(A.InvalidArgument, match="bad scale at block 2"):
+        A.dequantize_blockwise(q)
+
+
+def test_edge_sizes(cuda):
+    for n in (0, 1, 2, 3):
+        x = np.arange(n, dtype=np.float32) - 1.0
+        for kind, bits in CODECS:
+            q = A.quantize_blockwise(t(x, cuda), bits, 2, kind)
+            c, s = O.quantize(x, bits, 2, int(kind)) if n else (np.zeros(0, np.uint8), np.zeros(0, np.float32))
+            check_q(q, c, s, bits)
+
+
+def test_grouped_equals_single(cuda):
+    rng = np.random.default_rng(2)
+    xs = [t(_random_case(rng, n, True), cuda, torch.bfloat16) for n in (8192 * 5, 8192 * 2 + 77, 300)]
+    for bits in (4, 5, 6, 7, 8):
+        qs = A.quantize_grouped(xs, bits)
+        for x, q in zip(xs, qs):
+            r = A.quantize_blockwise(x, bits)
+            assert torch.equal(q.codes, r.codes) and torch.equal(q.scales, r.scales)
+        outs = A.dequantize_grouped(qs, torch.bfloat16)
+        for q, o in zip(qs, outs):
+            assert torch.equal(o.reshape(-1), A.dequantize_blockwise(q, torch.bfloat16).reshape(-1))
+
+
+def test_pack_unpack_device(cuda):
+    rng = np.random.default_rng(991)
+    for bits in range(4, 9):
+        for n in (1, 7, 8, 129, 1000, 100001):
+            codes = rng.integers(0, 1 << bits, size=n).astype(np.uint8)
+            p = A.pack_codes(t(codes, cuda, torch.uint8), bits)
+            assert np.array_equal(p.cpu().numpy(), O.pack(codes, bits))
+            u = A.unpack_codes(p, bits, n)
+            assert np.array_equal(u.cpu().numpy(), codes)
+
+
+def _bf16_domain_blocks(a_exp=0):
+    """Every BF16 x with |x| <= a for every BF16 mantissa a in [1,2) (scaled
+    by 2^a_exp): blocks of 128 = [a, x_1 .. x_127]."""
+    mags = (np.arange(0x8000, dtype=np.uint32) << 16).view(np.float32)
+    rows = []
+    for am in range(128):
+        a1 = np.array([(0x3F80 | am) << 16], np.uint32).view(np.float32)[0]
+        a = np.float32(np.ldexp(np.float64(a1), a_exp))
+        xs = mags[mags <= a]
+        xs = np.concatenate([xs, -xs])
+        pad = (-len(xs)) % 127
+        xs = np.concatenate([xs, np.zeros(pad, np.float32)]).reshape(-1, 127)
+        blk = np.concatenate([np.full((xs.shape[0], 1), a, np.float32), xs], axis=1)
+        rows.append(blk.reshape(-1))
+    return np.concatenate(rows).astype(np.float32)
+
+
+@pytest.mark.parametrize("a_exp", [0, -59, 59])
+def test_exhaustive_bf16_classes_on_device(cuda, a_exp):
+    """Same domain as tests/cpp/numerics_check.cpp, run through the kernels."""
+    x = _bf16_domain_blocks(a_exp)
+    for bf16 in (True, False):
+        xt = t(x, cuda, torch.bfloat16 if bf16 else torch.float32)
+        for kind, bits in CODECS:
+            c, s = O.quantize(x, bits, 128, int(kind))
+            q = A.quantize_blockwise(xt, bits, 128, kind, packed=False)
+            got = q.codes.cpu().numpy()
+            bad = np.nonzero(got != c)[0]
+            assert bad.size == 0, (kind, bits, bf16, bad[:5], x[bad[:5]])
+
+
+def test_exhaustive_dequant_bf16_scales_on_device(cuda):
+    """Every code x every BF16 scale in [2^-62, 2^62] (+ extremes)."""
+    exps = np.arange(-62, 62)
+    sm = np.arange(128, dtype=np.uint32)
+    base = ((0x3F80 | sm) << 16).view(np.float32)
+    scales = (base[None, :] * np.ldexp(1.0, exps)[:, None]).astype(np.float32).reshape(-1)
+    scales = np.concatenate([scales, np.array([0.0, 1e-40, 3e38, 1.5e-45], np.float32)])
+    for kind, bits in CODECS:
+        ncode = 1 << bits
+        codes = np.tile(np.arange(ncode, dtype=np.uint8), (scales.size, (128 + ncode - 1) // ncode))[:, :128]
+        codes = np.ascontiguousarray(codes.reshape(-1))
+        if kind == A.CodecKind.Fp8E4M3:
+            codes[(codes & 0x7F) == 0x7F] = 0
+        q = A.QuantizedTensor(t(codes, cuda, torch.uint8), t(scales, cuda), bits, 128,
+                              (codes.size,), kind, packed=False)
+        d = A.dequantize_blockwise(q).cpu().numpy()
+        want = O.dequantize(codes, scales, bits, 128, int(kind))
+        assert np.array_equal(u32(d), u32(want)), (kind, bits)
+
+
+def test_fp8_hardware_cvt_matches_rne(cuda):
+    """cvt.rn.satfinite.e4m3x2 (used by the gradient requant) == fp8_encode's
+    RNE: fp8 quantize of blocks anchored at 448 = encode of the value itself."""
+    rng = np.random.default_rng(0)
+    v = np.concatenate([rng.uniform(0, 448, 2_000_000), rng.uniform(0, 2 ** -5, 500_000)]).astype(np.float32)
+    v = np.concatenate([v, -v])
+    pad = (-v.size) % 127
+    v = np.concatenate([v, np.zeros(pad, np.float32)]).reshape(-1, 127)
+    x = np.concatenate([np.full((v.shape[0], 1), 448.0, np.float32), v], axis=1).reshape(-1)
+    q = A.quantize_blockwise(t(x, cuda), 8, 128, A.CodecKind.Fp8E4M3, packed=False)
+    c, _ = O.quantize(x, 8, 128, O.FP8)
+    assert np.array_equal(q.codes.cpu().numpy(), c)
+
+
+def test_launches_are_counted(cuda):
+    n0 = A.launch_count()
+    A.quantize_blockwise(t(np.ones(8192, np.float32), cuda, torch.bfloat16), 4)
+    assert A.launch_count() > n0

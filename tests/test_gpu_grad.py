@@ -1,0 +1,187 @@
+"""GPU parity of the gradient path: fused FP8 local_accumulate (K3), the
+decomposed all-reduce's reduce-requant (K4) in its one-device simulation,
+and the naive FP8 ring — bit-exact against the reference golden fixture and
+the C oracle, plus the reference's own property tests
+(proj/tests/test_collective.cpp)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle_ffi as O
+import paper_2605_00539_b200 as A
+
+pytestmark = pytest.mark.gpu
+FP8 = A.CodecKind.Fp8E4M3
+
+
+def t(x, dev, dtype=None):
+    a = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+    return a.to(dtype) if dtype is not None else a
+
+
+def u32(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def fp8q(codes, scales, dev):
+    return A.QuantizedTensor(t(codes, dev), t(scales, dev), 8, 128, (codes.size,), FP8, packed=False)
+
+
+def same(q, codes, scales):
+    assert np.array_equal(q.codes.cpu().numpy(), codes)
+    assert np.array_equal(u32(q.scales.cpu().numpy()), u32(scales))
+
+
+@pytest.mark.parametrize("prec", [0, 1, 2])
+def test_accumulate_golden(cuda, golden, prec):
+    main = fp8q(golden["acc_main_codes"], golden["acc_main_scales"], cuda)
+    out = A.local_accumulate(main, t(golden["acc_local"], cuda), A.AccumulatePrecision(prec))
+    same(out, golden[f"acc_p{prec}_codes"], golden[f"acc_p{prec}_scales"])
+
+
+@pytest.mark.parametrize("n", [128, 8192, 8192 * 7 + 300, 200003])
+@pytest.mark.parametrize("prec", [0, 1, 2])
+@pytest.mark.parametrize("bf16_local", [False, True])
+def test_accumulate_random(cuda, n, prec, bf16_local):
+    rng = np.random.default_rng(n * 3 + prec)
+    nb = (n + 127) // 128
+    mag = np.repeat(10.0 ** rng.uniform(-8, 3, nb), 128)[:n]
+    mag[:256] = 0.0  # zero main blocks
+    mc, ms = O.quantize((rng.standard_normal(n) * mag).astype(np.float32), 8, 128, O.FP8)
+    loc = (rng.standard_normal(n) * np.repeat(10.0 ** rng.uniform(-8, 3, nb), 128)[:n]).astype(np.float32)
+    loc[:128] = 0.0  # 0 + 0 block
+    loc[300:310] = -loc[300:310]
+    if prec == 2:
+        loc[1000:1010] = 7e4  # fp16 saturation path
+    if bf16_local:
+        loc = O.bf16_round(loc)
+    oc, os_ = O.local_accumulate(mc, ms, loc, prec)
+    lt = t(loc, cuda, torch.bfloat16 if bf16_local else torch.float32)
+    for in_place in (False, True):
+        main = fp8q(mc, ms, cuda)
+        out = A.local_accumulate(main, lt, A.AccumulatePrecision(prec), in_place=in_place)
+        same(out, oc, os_)
+
+
+def test_accumulate_reference_properties(cuda):
+    z = np.zeros(256, np.float32)                                   # test_collective.cpp:50-62
+    g = np.random.default_rng(2).standard_normal(256).astype(np.float32)
+    mc, ms = O.quantize(z, 8, 128, O.FP8)
+    dc, ds = O.quantize(g, 8, 128, O.FP8)
+    same(A.local_accumulate(fp8q(mc, ms, cuda), t(g, cuda)), dc, ds)
+    mc, ms = O.quantize(np.zeros(128, np.float32), 8, 128, O.FP8)   # :64-82
+    main = fp8q(mc, ms, cuda)
+    c100 = t(np.full(128, 100.0, np.float32), cuda)
+    for _ in range(8):
+        main = A.local_accumulate(main, c100)
+    assert torch.all(A.dequantize_blockwise(main) == 800.0)
+    rel = []                                                        # :84-108
+    for trial in range(5):
+        rng = np.random.default_rng(500 + trial)
+        main = fp8q(*O.quantize(np.zeros(1024, np.float32), 8, 128, O.FP8), cuda)
+        oracle = np.zeros(1024, np.float32)
+        for s in range(16):
+            gs = rng.standard_normal(1024).astype(np.float32)
+            main = A.local_accumulate(main, t(gs, cuda))
+            oracle += gs
+        v = A.dequantize_blockwise(main).cpu().numpy()
+        rel.append(np.linalg.norm(v - oracle) / np.linalg.norm(oracle))
+    assert max(rel) < 0.15
+
+
+def test_accumulate_errors(cuda):
+    mc, ms = O.quantize(np.ones(128, np.float32), 8, 128, O.FP8)
+    g = np.zeros(128, np.float32)
+    g[5] = np.nan
+    with pytest.raises(A.InvalidArgument, match="non-finite local gradient element"):
+        A.local_accumulate(fp8q(mc, ms, cuda), t(g, cuda))
+    with pytest.raises(A.InvalidArgument, match="shape mismatch"):
+        A.local_accumulate(fp8q(mc, ms, cuda), t(np.zeros(64, np.float32), cuda))
+    lin = A.quantize_blockwise(t(np.zeros(128, np.float32), cuda), 8, 128, packed=False)
+    with pytest.raises(A.InvalidArgument, match="FP8 E4M3"):
+        A.local_accumulate(lin, t(np.zeros(128, np.float32), cuda))
+    # fp32 overflow of the sum -> non-finite input in block k (quantize throws)
+    big = np.full(8192 * 2, 3e38, np.float32)
+    bc, bs = O.quantize(big, 8, 128, O.FP8)
+    with pytest.raises(A.InvalidArgument, match="non-finite input element in block 0"):
+        A.local_accumulate(fp8q(bc, bs, cuda), t(big, cuda))
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_allreduce_golden(cuda, golden, world):
+    mains = [fp8q(c, s, cuda) for c, s in zip(golden[f"ar{world}_in_codes"],
+                                              golden[f"ar{world}_in_scales"])]
+    same(A.allreduce_simulated(mains), golden[f"ar{world}_codes"], golden[f"ar{world}_scales"])
+    out, ov = A.allreduce_naive_simulated(mains)
+    same(out, golden[f"naive{world}_codes"], golden[f"naive{world}_scales"])
+    assert ov == int(golden[f"naive{world}_overflow"][0])
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 5, 8, 11, 16])
+def test_allreduce_random(cuda, world):
+    rng = np.random.default_rng(world)
+    n = 8192 * 3 + 200
+    codes, scales = [], []
+    for r in range(world):
+        mag = np.repeat(10.0 ** rng.uniform(-6, 2, (n + 127) // 128), 128)[:n]
+        c, s = O.quantize((rng.standard_normal(n) * mag).astype(np.float32), 8, 128, O.FP8)
+        codes.append(c)
+        scales.append(s)
+    oc, os_ = O.allreduce_decomposed(codes, scales)
+    same(A.allreduce_simulated([fp8q(c, s, cuda) for c, s in zip(codes, scales)]), oc, os_)
+    if world <= 8:
+        nc, ns, ov = O.allreduce_naive(codes, scales)
+        out, gov = A.allreduce_naive_simulated([fp8q(c, s, cuda) for c, s in zip(codes, scales)])
+        same(out, nc, ns)
+        assert gov == ov
+
+
+def test_allreduce_constant64_and_signed_zero(cuda, golden):
+    c, s = O.quantize(np.full(512, 64.0, np.float32), 8, 128, O.FP8)
+    mains = [fp8q(c, s, cuda)] * 8
+    out = A.allreduce_simulated(mains)
+    assert torch.all(A.dequantize_blockwise(out) == 512.0)             # exact 512
+    nout, ov = A.allreduce_naive_simulated(mains)
+    assert ov == 512 and torch.all(A.dequantize_blockwise(nout) == 64.0)
+    for P in (1, 2):
+        m = [fp8q(golden["sz_in_codes"], golden["sz_in_scales"], cuda)] * P
+        o = A.allreduce_simulated(m)
+        same(o, golden[f"sz{P}_codes"], golden[f"sz{P}_scales"])
+        assert int(o.codes[5]) == 0x00
+
+
+def test_allreduce_overflow_aborts(cuda):
+    c, s = O.quantize(np.full(256, 3e38, np.float32), 8, 128, O.FP8)
+    with pytest.raises(A.ProtocolError, match="fp32 overflow during local reduce"):
+        A.allreduce_simulated([fp8q(c, s, cuda)] * 2)
+
+
+def test_reduce_generic_block_sizes(cuda):
+    rng = np.random.default_rng(7)
+    for block in (2, 16, 100, 1000):
+        n = 3001
+        codes, scales = [], []
+        for r in range(3):
+            cc, ss = O.quantize(rng.standard_normal(n).astype(np.float32), 8, block, O.FP8)
+            codes.append(cc)
+            scales.append(ss)
+        oc, os_ = O.allreduce_decomposed(codes, scales, block)
+        mains = [A.QuantizedTensor(t(cc, cuda), t(ss, cuda), 8, block, (n,), FP8, packed=False)
+                 for cc, ss in zip(codes, scales)]
+        same(A.allreduce_simulated(mains), oc, os_)
+        # generic accumulate with the same block
+        loc = rng.standard_normal(n).astype(np.float32)
+        ac, as_ = O.local_accumulate(codes[0], scales[0], loc, 0, block)
+        same(A.local_accumulate(mains[0], t(loc, cuda)), ac, as_)
+
+
+def test_second_allreduce_scales_by_world(cuda):
+    rng = np.random.default_rng(55)                                 # test_collective.cpp:268-283
+    codes, scales = zip(*[O.quantize(rng.standard_normal(512).astype(np.float32), 8, 128, O.FP8)
+                          for _ in range(4)])
+    first = A.allreduce_simulated([fp8q(c, s, cuda) for c, s in zip(codes, scales)])
+    v1 = A.dequantize_blockwise(first).cpu().numpy()
+    second = A.allreduce_simulated([first] * 4)
+    v2 = A.dequantize_blockwise(second).cpu().numpy()
+    step = np.repeat(second.scales.cpu().numpy(), 128) * (32.0 / 448.0)
+    assert np.all(np.abs(v2 - 4.0 * v1) <= 4 * step + 1e-5)

@@ -17,6 +17,7 @@
 // Generic path (any block size / alignment / the tail after the last full
 // tile): warp-per-block absmax, thread-per-output-byte encode+pack and
 // thread-per-element decode, same element functions (agq_numerics.cuh).
+#include <cstdlib>
 #include <utility>
 
 #include "agq_common.cuh"
@@ -66,6 +67,41 @@ __device__ __forceinline__ uint32_t encode_one(float x, float a, float inv,
     return fast ? fp4_code(x, a) : encode_double(1, 4, x, a);
   } else {
     return fast ? fp8_code(x, a, inv) : encode_double(2, 8, x, a);
+  }
+}
+
+__device__ __noinline__ uint32_t encode_slow(int codec, int bits, float x, float a) {
+  return encode_double(codec, bits, x, a);
+}
+
+// SymmetricLinear, BF16 input, fast block scale: linear_k_bf16 on element
+// pairs with packed FP32x2 arithmetic, RNE-to-integer by the magic add.
+// Identical per-lane operations to agq_numerics.cuh:linear_k_bf16 (which the
+// host test verifies exhaustively); codes land at PACK bits per element.
+template <int BITS, int PACK>
+__device__ __forceinline__ void encode_linear_bf16_fast(const uint4 (&ch)[4], float a, float inv,
+                                                        float rcp, uint64_t (&pk)[4]) {
+  constexpr int L = (1 << (BITS - 1)) - 1;
+  const f32x2 inv2 = pk2(inv, inv), rcp2 = pk2(rcp, rcp), na2 = pk2(-a, -a);
+  const f32x2 L2 = pk2((float)L, (float)L), mg2 = pk2(kMagicRound, kMagicRound);
+  constexpr uint32_t kOff = (uint32_t)L - kMagicBits;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t wv[4] = {ch[j].x, ch[j].y, ch[j].z, ch[j].w};
+    uint64_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const f32x2 x = pk2(u2f(wv[k] << 16), u2f(wv[k] & 0xffff0000u));
+      const f32x2 v = mul2(x, inv2);
+      const f32x2 xl = mul2(x, L2);
+      const f32x2 r = fma2(v, na2, xl);
+      const f32x2 v2 = fma2(r, rcp2, v);
+      float lo, hi;
+      up2(add2(v2, mg2), lo, hi);
+      const uint32_t c0 = f2u(lo) + kOff, c1 = f2u(hi) + kOff;
+      acc |= (uint64_t)(c0 | (c1 << PACK)) << (2 * k * PACK);
+    }
+    pk[j] = acc;
   }
 }
 
@@ -171,24 +207,51 @@ __global__ void __launch_bounds__(kThreads)
       if (CODEC == 0 && TR::kBf16) rcp = fdiv(1.0f, a);
     }
 
-    // ---- encode + pack each chunk (kPerChunk codes -> kChunkBits bits)
+    // ---- encode + pack each chunk (kPerChunk codes -> kChunkBits bits).
+    // The fast/slow/zero choice is block-uniform: branch once, not per element.
     uint64_t pk[kChunks];
+    if (zero) {
+      uint64_t zc = 0;
 #pragma unroll
-    for (int j = 0; j < kChunks; ++j) {
-      const uint32_t wv[4] = {ch[j].x, ch[j].y, ch[j].z, ch[j].w};
-      uint64_t acc = 0;
+      for (int e = 0; e < kPerChunk; ++e) zc |= (uint64_t)kZeroCode << (e * PACK);
 #pragma unroll
-      for (int e = 0; e < kPerChunk; ++e) {
-        float x;
-        if constexpr (TR::kBf16)
-          x = u2f((e & 1) ? (wv[e >> 1] & 0xffff0000u) : (wv[e >> 1] << 16));
-        else
-          x = u2f(wv[e]);
-        const uint32_t c =
-            zero ? kZeroCode : encode_one<BITS, CODEC, TR::kBf16>(x, a, inv, rcp, fast);
-        acc |= (uint64_t)c << (e * PACK);
+      for (int j = 0; j < kChunks; ++j) pk[j] = zc;
+    } else if (fast) {
+      if constexpr (CODEC == 0 && TR::kBf16) {
+        encode_linear_bf16_fast<BITS, PACK>(ch, a, inv, rcp, pk);
+      } else {
+#pragma unroll
+        for (int j = 0; j < kChunks; ++j) {
+          const uint32_t wv[4] = {ch[j].x, ch[j].y, ch[j].z, ch[j].w};
+          uint64_t acc = 0;
+#pragma unroll
+          for (int e = 0; e < kPerChunk; ++e) {
+            float x;
+            if constexpr (TR::kBf16)
+              x = u2f((e & 1) ? (wv[e >> 1] & 0xffff0000u) : (wv[e >> 1] << 16));
+            else
+              x = u2f(wv[e]);
+            acc |= (uint64_t)encode_one<BITS, CODEC, TR::kBf16>(x, a, inv, rcp, true) << (e * PACK);
+          }
+          pk[j] = acc;
+        }
       }
-      pk[j] = acc;
+    } else {
+#pragma unroll 1
+      for (int j = 0; j < kChunks; ++j) {
+        const uint32_t wv[4] = {ch[j].x, ch[j].y, ch[j].z, ch[j].w};
+        uint64_t acc = 0;
+#pragma unroll 1
+        for (int e = 0; e < kPerChunk; ++e) {
+          float x;
+          if constexpr (TR::kBf16)
+            x = u2f((e & 1) ? (wv[e >> 1] & 0xffff0000u) : (wv[e >> 1] << 16));
+          else
+            x = u2f(wv[e]);
+          acc |= (uint64_t)encode_slow(CODEC, BITS, x, a) << (e * PACK);
+        }
+        pk[j] = acc;
+      }
     }
     // undo the rotation: pk[(j + rot)] must hold chunk j
     if constexpr (kChunks == 4) rotr4(pk, rot); else rotr8(pk, rot);
@@ -228,6 +291,169 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------------------
+// K1 (warp-autonomous variant): every warp streams its own 1024-element tiles
+// — coalesced 128-bit global loads (next tile prefetched into registers while
+// the current one is encoded), staged through a private 2 KB shared-memory
+// slot so each lane reads its 32 consecutive elements conflict-free, codes
+// written straight from registers (PACK 32-bit words per lane, contiguous per
+// warp). No CTA-wide barrier anywhere; only __syncwarp.
+// ---------------------------------------------------------------------------
+constexpr int kWarpElems = 1024;
+constexpr int kWarpsPerCta = 8;
+
+template <int BITS, int PACK, int CODEC, typename Tin>
+__device__ __forceinline__ void encode_row(const uint4 (&ch)[InTraits<Tin>::kChunks], int rot,
+                                           float a, bool zero, bool fast,
+                                           uint32_t (&words)[PACK]) {
+  using TR = InTraits<Tin>;
+  constexpr int kChunks = TR::kChunks;
+  constexpr int kPerChunk = 32 / kChunks;
+  constexpr int kChunkBits = kPerChunk * PACK;
+  constexpr int L = (1 << (BITS - 1)) - 1;
+  constexpr uint32_t kZeroCode = CODEC == 0 ? (uint32_t)L : 0u;
+  float inv = 0.f, rcp = 0.f;
+  if (!zero && fast) {
+    inv = codec_inv(CODEC, BITS, a);
+    if (CODEC == 0 && TR::kBf16) rcp = fdiv(1.0f, a);
+  }
+  uint64_t pk[kChunks];
+  if (zero) {
+    uint64_t zc = 0;
+#pragma unroll
+    for (int e = 0; e < kPerChunk; ++e) zc |= (uint64_t)kZeroCode << (e * PACK);
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) pk[j] = zc;
+  } else if (fast) {
+    if constexpr (CODEC == 0 && TR::kBf16) {
+      encode_linear_bf16_fast<BITS, PACK>(ch, a, inv, rcp, pk);
+    } else {
+#pragma unroll
+      for (int j = 0; j < kChunks; ++j) {
+        const uint32_t wv[4] = {ch[j].x, ch[j].y, ch[j].z, ch[j].w};
+        uint64_t acc = 0;
+#pragma unroll
+        for (int e = 0; e < kPerChunk; ++e) {
+          float x;
+          if constexpr (TR::kBf16)
+            x = u2f((e & 1) ? (wv[e >> 1] & 0xffff0000u) : (wv[e >> 1] << 16));
+          else
+            x = u2f(wv[e]);
+          acc |= (uint64_t)encode_one<BITS, CODEC, TR::kBf16>(x, a, inv, rcp, true) << (e * PACK);
+        }
+        pk[j] = acc;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) {
+      const uint32_t wv[4] = {ch[j].x, ch[j].y, ch[j].z, ch[j].w};
+      uint64_t acc = 0;
+#pragma unroll
+      for (int e = 0; e < kPerChunk; ++e) {
+        float x;
+        if constexpr (TR::kBf16)
+          x = u2f((e & 1) ? (wv[e >> 1] & 0xffff0000u) : (wv[e >> 1] << 16));
+        else
+          x = u2f(wv[e]);
+        acc |= (uint64_t)encode_slow(CODEC, BITS, x, a) << (e * PACK);
+      }
+      pk[j] = acc;
+    }
+  }
+  if constexpr (kChunks == 4) rotr4(pk, rot); else rotr8(pk, rot);
+#pragma unroll
+  for (int k = 0; k < PACK; ++k) words[k] = 0;
+  pack_chunks<kChunkBits>(words, pk, std::make_integer_sequence<int, kChunks>{});
+}
+
+template <int BITS, int PACK, int CODEC, typename Tin>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tin) == 2 ? 4 : 2)
+    k_quant_warp(SegTable st, agq_errors* err) {
+  using TR = InTraits<Tin>;
+  constexpr int kChunks = TR::kChunks;
+  constexpr uint32_t kRowB = 32 * sizeof(Tin);            // one lane's elements
+  constexpr uint32_t kTileB = kWarpElems * sizeof(Tin);    // 2 KB / 4 KB
+  constexpr uint32_t kCodeB = kWarpElems * PACK / 8;
+  __shared__ __align__(16) unsigned char sbuf[kWarpsPerCta][kTileB];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wb = sbuf[warp];
+  const uint64_t total = st.tile_begin[st.nseg];
+  const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
+  uint64_t t = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
+  const int rot = kChunks == 4 ? ((lane >> 1) & 3) : (lane & 7);
+
+  auto load = [&](uint64_t tt, uint4 (&buf)[kChunks]) {
+    const int g = seg_of(st, tt);
+    const unsigned char* src =
+        static_cast<const unsigned char*>(st.src[g]) + (tt - st.tile_begin[g]) * kTileB;
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) buf[j] = ldg128_stream(src + j * 512 + lane * 16);
+  };
+  uint4 buf[kChunks];
+  if (t < total) load(t, buf);
+  for (; t < total; t += nw) {
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) sts128(wb + j * 512 + lane * 16, buf[j]);
+    __syncwarp();
+    if (t + nw < total) load(t + nw, buf);
+    uint4 ch[kChunks];
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) ch[j] = lds128(wb + lane * kRowB + ((j + rot) & (kChunks - 1)) * 16);
+    __syncwarp();
+
+    uint32_t m;
+    if constexpr (TR::kBf16) {
+      uint32_t mm = 0;
+#pragma unroll
+      for (int j = 0; j < kChunks; ++j) {
+        mm = __vmaxu2(mm, ch[j].x & 0x7fff7fffu);
+        mm = __vmaxu2(mm, ch[j].y & 0x7fff7fffu);
+        mm = __vmaxu2(mm, ch[j].z & 0x7fff7fffu);
+        mm = __vmaxu2(mm, ch[j].w & 0x7fff7fffu);
+      }
+      m = max(mm & 0xffffu, mm >> 16) << 16;
+    } else {
+      m = 0;
+#pragma unroll
+      for (int j = 0; j < kChunks; ++j) {
+        m = max(m, ch[j].x & 0x7fffffffu);
+        m = max(m, ch[j].y & 0x7fffffffu);
+        m = max(m, ch[j].z & 0x7fffffffu);
+        m = max(m, ch[j].w & 0x7fffffffu);
+      }
+    }
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
+    const float a = u2f(m);
+    const int g = seg_of(st, t);
+    const uint64_t lt = t - st.tile_begin[g];
+    if (m >= 0x7f800000u && (lane & 3) == 0)
+      err_min(&err->nonfinite_block, (long long)(st.block_base[g] + lt * 8 + (lane >> 2)));
+    uint32_t words[PACK];
+    encode_row<BITS, PACK, CODEC, Tin>(ch, rot, a, m == 0, fast_scale(a), words);
+    uint32_t* cdst = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(st.codes[g]) +
+                                                 lt * kCodeB) + lane * PACK;
+    if constexpr (PACK % 4 == 0) {
+#pragma unroll
+      for (int k = 0; k < PACK / 4; ++k)
+        *reinterpret_cast<uint4*>(cdst + 4 * k) =
+            make_uint4(words[4 * k], words[4 * k + 1], words[4 * k + 2], words[4 * k + 3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < PACK; ++k) cdst[k] = words[k];
+    }
+    if ((lane & 3) == 0) st.scales[g][lt * 8 + (lane >> 2)] = a;
+  }
+}
+
+// K2 warp-autonomous variant: lane loads its PACK code words (+ block scale),
+// next tile prefetched, decodes 32 values, stages the 2/4 KB warp output in
+// shared memory and writes it back with coalesced 128-bit stores.
+template <int BITS, int PACK, int CODEC, typename Tout>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? 4 : 2)
+    k_dequant_warp(SegTable st, int validate, agq_errors* err);
+
+// ---------------------------------------------------------------------------
 // K2: dequantize
 // ---------------------------------------------------------------------------
 template <typename Tout>
@@ -257,6 +483,38 @@ __device__ __forceinline__ float decode_one(uint32_t c, float s, bool fast,
     if (fast) return div_const_rn(fmul(e4m3_value(c), s), 448.0f, 1.0f / 448.0f);
     const float mag = d2f_rn(dmul(fp8lut[c & 0x7fu], (double)s));
     return u2f(f2u(mag) | ((c & 0x80u) << 24));
+  }
+}
+
+__device__ __noinline__ float decode_slow(int codec, int bits, uint32_t c, float s,
+                                         const double* fp8lut) {
+  if (codec == 2) {
+    if ((c & 0x7fu) == 0x7fu) return u2f(0x7fc00000u | ((c & 0x80u) << 24));
+    const float mag = d2f_rn(dmul(fp8lut[c & 0x7fu], (double)s));
+    return u2f(f2u(mag) | ((c & 0x80u) << 24));
+  }
+  return dequant_double(codec, bits, c, s);
+}
+
+// SymmetricLinear, BF16-valued fast scale: c' = c - L as an exact float via
+// the magic add (no I2F), p = c' s exact, then the Markstein-corrected
+// division by L (agq_numerics.cuh:dq_linear_bf16scale) on pairs. Linear codes
+// never produce -0, so the division needs no sign handling here.
+template <int BITS, int PACK, int NPER>
+__device__ __forceinline__ void decode_linear_fast(uint64_t bits, float s, float (&v)[NPER]) {
+  constexpr int L = (1 << (BITS - 1)) - 1;
+  const f32x2 s2 = pk2(s, s);
+  const f32x2 off2 = pk2(-(kMagicRound + (float)L), -(kMagicRound + (float)L));
+  const f32x2 den2 = pk2(-(float)L, -(float)L), rden2 = pk2(1.0f / L, 1.0f / L);
+#pragma unroll
+  for (int e = 0; e < NPER; e += 2) {
+    const uint32_t c0 = (uint32_t)(bits >> (e * PACK)) & ((1u << BITS) - 1u);
+    const uint32_t c1 = (uint32_t)(bits >> ((e + 1) * PACK)) & ((1u << BITS) - 1u);
+    const f32x2 cp = add2(pk2(u2f(kMagicBits | c0), u2f(kMagicBits | c1)), off2);
+    const f32x2 p = mul2(cp, s2);
+    const f32x2 q0 = mul2(p, rden2);
+    const f32x2 r = fma2(q0, den2, p);
+    up2(fma2(r, rden2, q0), v[e], v[e + 1]);
   }
 }
 
@@ -378,10 +636,20 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int j = 0; j < kChunks; ++j) {
       float v[kPerChunk];
+      if (CODEC == 0 && fast) {
+        decode_linear_fast<BITS, PACK, kPerChunk>(pk[j], sc, v);
+      } else if (fast) {
 #pragma unroll
-      for (int e = 0; e < kPerChunk; ++e) {
-        const uint32_t c = (uint32_t)(pk[j] >> (e * PACK)) & ((1u << PACK) - 1u);
-        v[e] = decode_one<BITS, CODEC>(c & ((1u << BITS) - 1u), sc, fast, fp8lut);
+        for (int e = 0; e < kPerChunk; ++e) {
+          const uint32_t c = (uint32_t)(pk[j] >> (e * PACK)) & ((1u << BITS) - 1u);
+          v[e] = decode_one<BITS, CODEC>(c, sc, true, fp8lut);
+        }
+      } else {
+#pragma unroll 1
+        for (int e = 0; e < kPerChunk; ++e) {
+          const uint32_t c = (uint32_t)(pk[j] >> (e * PACK)) & ((1u << BITS) - 1u);
+          v[e] = decode_slow(CODEC, BITS, c, sc, fp8lut);
+        }
       }
       uint4 o;
       if constexpr (kBf16Out) {
@@ -412,6 +680,127 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
   if (tid == 0) bulk_wait_all<0>();
+}
+
+template <int BITS, int PACK, int CODEC, typename Tout>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? 4 : 2)
+    k_dequant_warp(SegTable st, int validate, agq_errors* err) {
+  constexpr int kChunks = OutTraits<Tout>::kChunks;
+  constexpr int kPerChunk = 32 / kChunks;
+  constexpr int kChunkBits = kPerChunk * PACK;
+  constexpr uint32_t kRowB = 32 * sizeof(Tout);
+  constexpr uint32_t kTileB = kWarpElems * sizeof(Tout);
+  constexpr uint32_t kCodeB = kWarpElems * PACK / 8;
+  constexpr bool kBf16Out = sizeof(Tout) == 2;
+  __shared__ __align__(16) unsigned char sbuf[kWarpsPerCta][kTileB];
+  __shared__ double fp8lut[CODEC == 2 ? 128 : 1];
+  if (CODEC == 2) {
+    fill_fp8_unit_lut(fp8lut);
+    __syncthreads();
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wb = sbuf[warp];
+  const uint64_t total = st.tile_begin[st.nseg];
+  const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
+  uint64_t t = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
+  const int rot = kChunks == 4 ? ((lane >> 1) & 3) : (lane & 7);
+
+  auto load = [&](uint64_t tt, uint32_t (&w)[PACK], float& sc) {
+    const int g = seg_of(st, tt);
+    const uint64_t lt = tt - st.tile_begin[g];
+    const unsigned char* src = static_cast<const unsigned char*>(st.codes[g]) + lt * kCodeB;
+    if constexpr (PACK % 4 == 0) {
+#pragma unroll
+      for (int k = 0; k < PACK / 4; ++k) {
+        const uint4 v = ldg128_stream(src + lane * PACK * 4 + k * 16);
+        w[4 * k] = v.x; w[4 * k + 1] = v.y; w[4 * k + 2] = v.z; w[4 * k + 3] = v.w;
+      }
+    } else {
+      const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src) + lane * PACK;
+#pragma unroll
+      for (int k = 0; k < PACK; ++k) w[k] = __ldg(s32 + k);
+    }
+    sc = __ldg(st.scales[g] + lt * 8 + (lane >> 2));
+  };
+  uint32_t words[PACK];
+  float sc = 0.f;
+  if (t < total) load(t, words, sc);
+  for (; t < total; t += nw) {
+    uint32_t cw[PACK];
+#pragma unroll
+    for (int k = 0; k < PACK; ++k) cw[k] = words[k];
+    const float s = sc;
+    const int g = seg_of(st, t);
+    const uint64_t lt = t - st.tile_begin[g];
+    if (t + nw < total) load(t + nw, words, sc);
+    if (validate) {
+      if ((!(s >= 0.0f) || !(s <= 3.402823466e38f)) && (lane & 3) == 0)
+        err_min(&err->bad_scale_block, (long long)(st.block_base[g] + lt * 8 + (lane >> 2)));
+      if constexpr (PACK == 8 && BITS < 8) {
+        uint32_t bad = 0;
+#pragma unroll
+        for (int k = 0; k < PACK; ++k) bad |= cw[k] & (0x01010101u * (0xffu << BITS & 0xffu));
+        if (bad) {
+#pragma unroll 1
+          for (int e = 0; e < 32; ++e) {
+            const uint32_t c = (cw[e >> 2] >> ((e & 3) * 8)) & 0xffu;
+            if (c >> BITS) {
+              err_min(&err->bad_code_index,
+                      (long long)((st.block_base[g] + lt * 8) * kBlock + lane * 32 + e));
+              break;
+            }
+          }
+        }
+      }
+    }
+    const bool fast = is_bf16_value(s) && fast_scale(s);
+    uint64_t pk[kChunks];
+    unpack_chunks<kChunkBits>(cw, pk, std::make_integer_sequence<int, kChunks>{});
+    if constexpr (kChunks == 4) rotl4(pk, rot); else rotl8(pk, rot);
+    unsigned char* orow = wb + lane * kRowB;
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) {
+      float v[kPerChunk];
+      if (CODEC == 0 && fast) {
+        decode_linear_fast<BITS, PACK, kPerChunk>(pk[j], s, v);
+      } else if (fast) {
+#pragma unroll
+        for (int e = 0; e < kPerChunk; ++e) {
+          const uint32_t c = (uint32_t)(pk[j] >> (e * PACK)) & ((1u << BITS) - 1u);
+          v[e] = decode_one<BITS, CODEC>(c, s, true, fp8lut);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < kPerChunk; ++e) {
+          const uint32_t c = (uint32_t)(pk[j] >> (e * PACK)) & ((1u << BITS) - 1u);
+          v[e] = decode_slow(CODEC, BITS, c, s, fp8lut);
+        }
+      }
+      uint4 o;
+      if constexpr (kBf16Out) {
+        uint32_t h[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (CODEC == 2)
+            h[k] = bf16_bits_rne(v[2 * k]) | (bf16_bits_rne(v[2 * k + 1]) << 16);
+          else {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+            h[k] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+        }
+        o = make_uint4(h[0], h[1], h[2], h[3]);
+      } else {
+        o = make_uint4(f2u(v[0]), f2u(v[1]), f2u(v[2]), f2u(v[3]));
+      }
+      sts128(orow + ((j + rot) & (kChunks - 1)) * 16, o);
+    }
+    __syncwarp();
+    unsigned char* dst = static_cast<unsigned char*>(st.dst[g]) + lt * kTileB;
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j)
+      *reinterpret_cast<uint4*>(dst + j * 512 + lane * 16) = lds128(wb + j * 512 + lane * 16);
+    __syncwarp();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -557,6 +946,17 @@ using namespace agqk;
 
 namespace {
 
+// Activation-kernel variant: warp-autonomous (default) or the CTA-wide TMA
+// bulk-copy pipeline; AGQ_ACT_KERNEL=tma selects the latter.
+bool act_warp() {
+  static const bool w = [] {
+    const char* e = getenv("AGQ_ACT_KERNEL");
+    return !(e && e[0] == 't');
+  }();
+  return w;
+}
+uint64_t act_unit() { return act_warp() ? (uint64_t)kWarpElems : (uint64_t)kTileElems; }
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 template <typename K>
@@ -595,17 +995,45 @@ agq_status launch_quant_tiled(const SegTable& st, agq_errors* err, cudaStream_t 
   return cuda_fail(cudaGetLastError(), "quantize: launch");
 }
 
+template <int BITS, int PACK, int CODEC, typename Tin>
+agq_status launch_quant_warp(const SegTable& st, agq_errors* err, cudaStream_t s) {
+  auto k = k_quant_warp<BITS, PACK, CODEC, Tin>;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWarpsPerCta * 32, 0);
+  if (occ < 1) occ = 1;
+  const uint64_t tiles = st.tile_begin[st.nseg];
+  const uint64_t want = (tiles + kWarpsPerCta - 1) / kWarpsPerCta;
+  const uint64_t cap = (uint64_t)num_sms() * occ;
+  k<<<(int)(want < cap ? want : cap), kWarpsPerCta * 32, 0, s>>>(st, err);
+  count_launch();
+  return cuda_fail(cudaGetLastError(), "quantize: launch");
+}
+
+template <int BITS, int PACK, int CODEC, typename Tout>
+agq_status launch_dequant_warp(const SegTable& st, int validate, agq_errors* err, cudaStream_t s) {
+  auto k = k_dequant_warp<BITS, PACK, CODEC, Tout>;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWarpsPerCta * 32, 0);
+  if (occ < 1) occ = 1;
+  const uint64_t tiles = st.tile_begin[st.nseg];
+  const uint64_t want = (tiles + kWarpsPerCta - 1) / kWarpsPerCta;
+  const uint64_t cap = (uint64_t)num_sms() * occ;
+  k<<<(int)(want < cap ? want : cap), kWarpsPerCta * 32, 0, s>>>(st, validate, err);
+  count_launch();
+  return cuda_fail(cudaGetLastError(), "dequantize: launch");
+}
+
 template <int PACK, typename Tin>
 agq_status quant_dispatch_bits(int bits, int codec, const SegTable& st,
                                agq_errors* err, cudaStream_t s) {
-  if (codec == AGQ_CODEC_FP8_E4M3) return launch_quant_tiled<8, 8, 2, Tin>(st, err, s);
-  if (codec == AGQ_CODEC_FP4_E2M1) return launch_quant_tiled<4, PACK == 8 ? 8 : 4, 1, Tin>(st, err, s);
+  if (codec == AGQ_CODEC_FP8_E4M3) return act_warp() ? launch_quant_warp<8, 8, 2, Tin>(st, err, s) : launch_quant_tiled<8, 8, 2, Tin>(st, err, s);
+  if (codec == AGQ_CODEC_FP4_E2M1) return act_warp() ? launch_quant_warp<4, PACK == 8 ? 8 : 4, 1, Tin>(st, err, s) : launch_quant_tiled<4, PACK == 8 ? 8 : 4, 1, Tin>(st, err, s);
   switch (bits) {
-    case 4: return launch_quant_tiled<4, PACK == 8 ? 8 : 4, 0, Tin>(st, err, s);
-    case 5: return launch_quant_tiled<5, PACK == 8 ? 8 : 5, 0, Tin>(st, err, s);
-    case 6: return launch_quant_tiled<6, PACK == 8 ? 8 : 6, 0, Tin>(st, err, s);
-    case 7: return launch_quant_tiled<7, PACK == 8 ? 8 : 7, 0, Tin>(st, err, s);
-    default: return launch_quant_tiled<8, 8, 0, Tin>(st, err, s);
+    case 4: return act_warp() ? launch_quant_warp<4, PACK == 8 ? 8 : 4, 0, Tin>(st, err, s) : launch_quant_tiled<4, PACK == 8 ? 8 : 4, 0, Tin>(st, err, s);
+    case 5: return act_warp() ? launch_quant_warp<5, PACK == 8 ? 8 : 5, 0, Tin>(st, err, s) : launch_quant_tiled<5, PACK == 8 ? 8 : 5, 0, Tin>(st, err, s);
+    case 6: return act_warp() ? launch_quant_warp<6, PACK == 8 ? 8 : 6, 0, Tin>(st, err, s) : launch_quant_tiled<6, PACK == 8 ? 8 : 6, 0, Tin>(st, err, s);
+    case 7: return act_warp() ? launch_quant_warp<7, PACK == 8 ? 8 : 7, 0, Tin>(st, err, s) : launch_quant_tiled<7, PACK == 8 ? 8 : 7, 0, Tin>(st, err, s);
+    default: return act_warp() ? launch_quant_warp<8, 8, 0, Tin>(st, err, s) : launch_quant_tiled<8, 8, 0, Tin>(st, err, s);
   }
 }
 
@@ -626,14 +1054,14 @@ agq_status launch_dequant_tiled(const SegTable& st, int validate, agq_errors* er
 template <int PACK, typename Tout>
 agq_status dequant_dispatch_bits(int bits, int codec, const SegTable& st,
                                  int validate, agq_errors* err, cudaStream_t s) {
-  if (codec == AGQ_CODEC_FP8_E4M3) return launch_dequant_tiled<8, 8, 2, Tout>(st, validate, err, s);
-  if (codec == AGQ_CODEC_FP4_E2M1) return launch_dequant_tiled<4, PACK == 8 ? 8 : 4, 1, Tout>(st, validate, err, s);
+  if (codec == AGQ_CODEC_FP8_E4M3) return act_warp() ? launch_dequant_warp<8, 8, 2, Tout>(st, validate, err, s) : launch_dequant_tiled<8, 8, 2, Tout>(st, validate, err, s);
+  if (codec == AGQ_CODEC_FP4_E2M1) return act_warp() ? launch_dequant_warp<4, PACK == 8 ? 8 : 4, 1, Tout>(st, validate, err, s) : launch_dequant_tiled<4, PACK == 8 ? 8 : 4, 1, Tout>(st, validate, err, s);
   switch (bits) {
-    case 4: return launch_dequant_tiled<4, PACK == 8 ? 8 : 4, 0, Tout>(st, validate, err, s);
-    case 5: return launch_dequant_tiled<5, PACK == 8 ? 8 : 5, 0, Tout>(st, validate, err, s);
-    case 6: return launch_dequant_tiled<6, PACK == 8 ? 8 : 6, 0, Tout>(st, validate, err, s);
-    case 7: return launch_dequant_tiled<7, PACK == 8 ? 8 : 7, 0, Tout>(st, validate, err, s);
-    default: return launch_dequant_tiled<8, 8, 0, Tout>(st, validate, err, s);
+    case 4: return act_warp() ? launch_dequant_warp<4, PACK == 8 ? 8 : 4, 0, Tout>(st, validate, err, s) : launch_dequant_tiled<4, PACK == 8 ? 8 : 4, 0, Tout>(st, validate, err, s);
+    case 5: return act_warp() ? launch_dequant_warp<5, PACK == 8 ? 8 : 5, 0, Tout>(st, validate, err, s) : launch_dequant_tiled<5, PACK == 8 ? 8 : 5, 0, Tout>(st, validate, err, s);
+    case 6: return act_warp() ? launch_dequant_warp<6, PACK == 8 ? 8 : 6, 0, Tout>(st, validate, err, s) : launch_dequant_tiled<6, PACK == 8 ? 8 : 6, 0, Tout>(st, validate, err, s);
+    case 7: return act_warp() ? launch_dequant_warp<7, PACK == 8 ? 8 : 7, 0, Tout>(st, validate, err, s) : launch_dequant_tiled<7, PACK == 8 ? 8 : 7, 0, Tout>(st, validate, err, s);
+    default: return act_warp() ? launch_dequant_warp<8, 8, 0, Tout>(st, validate, err, s) : launch_dequant_tiled<8, 8, 0, Tout>(st, validate, err, s);
   }
 }
 
@@ -667,7 +1095,7 @@ agq_status quantize_device(const void* x, int x_dtype, uint64_t n, int bits,
   const size_t esz = x_dtype == AGQ_BF16 ? 2 : 4;
   uint64_t ntiles = 0;
   if (block == (uint32_t)kBlock && aligned16(x) && aligned16(codes) && aligned16(scales))
-    ntiles = n / kTileElems;
+    ntiles = n / act_unit();
   if (ntiles > 0) {
     SegTable st{};
     st.src[0] = x;
@@ -686,7 +1114,7 @@ agq_status quantize_device(const void* x, int x_dtype, uint64_t n, int bits,
                                      : quant_dispatch_bits<8, float>(bits, codec, st, err, s);
     if (r != AGQ_OK) return r;
   }
-  const uint64_t done = ntiles * kTileElems;
+  const uint64_t done = ntiles * act_unit();
   if (done == n) return AGQ_OK;
   // tail (block-aligned start, byte-aligned in the packed stream)
   const uint64_t rest = n - done;
@@ -708,7 +1136,7 @@ agq_status dequantize_device(const void* codes, int layout, const float* scales,
   const int pack = layout == AGQ_CODES_PACKED ? bits : 8;
   uint64_t ntiles = 0;
   if (block == (uint32_t)kBlock && aligned16(out) && aligned16(codes) && aligned16(scales))
-    ntiles = n / kTileElems;
+    ntiles = n / act_unit();
   if (ntiles > 0) {
     SegTable st{};
     st.codes[0] = const_cast<void*>(codes);
@@ -726,7 +1154,7 @@ agq_status dequantize_device(const void* codes, int layout, const float* scales,
                                      : dequant_dispatch_bits<8, float>(bits, codec, st, validate, err, s);
     if (r != AGQ_OK) return r;
   }
-  const uint64_t done = ntiles * kTileElems;
+  const uint64_t done = ntiles * act_unit();
   if (done == n) return AGQ_OK;
   const uint64_t rest = n - done;
   const uint8_t* ctail = static_cast<const uint8_t*>(codes) + (done * pack) / 8;
@@ -753,7 +1181,7 @@ agq_status quantize_grouped_device(const agq_segment* segs, int nseg, int x_dtyp
   for (int i = 0; i < nseg; ++i) {
     const uint64_t nt = aligned16(segs[i].x) && aligned16(segs[i].codes) &&
                                 aligned16(segs[i].scales)
-                            ? segs[i].n / kTileElems
+                            ? segs[i].n / act_unit()
                             : 0;
     if (nt > 0) {
       if (k == kMaxSeg) return set_error(AGQ_ERR_INVALID_ARGUMENT, "too many segments");
@@ -777,7 +1205,7 @@ agq_status quantize_grouped_device(const agq_segment* segs, int nseg, int x_dtyp
   }
   for (int i = 0; i < nseg; ++i) {
     const bool tiled = aligned16(segs[i].x) && aligned16(segs[i].codes) && aligned16(segs[i].scales);
-    const uint64_t done = tiled ? (segs[i].n / kTileElems) * kTileElems : 0;
+    const uint64_t done = tiled ? (segs[i].n / act_unit()) * act_unit() : 0;
     if (done == segs[i].n) continue;
     const size_t esz = x_dtype == AGQ_BF16 ? 2 : 4;
     agq_status r = quantize_device(static_cast<const char*>(segs[i].x) + done * esz, x_dtype,
@@ -796,7 +1224,7 @@ agq_status dequantize_grouped_device(const agq_segment* segs, int nseg, int out_
   int k = 0;
   for (int i = 0; i < nseg; ++i) {
     const bool tiled = aligned16(segs[i].x) && aligned16(segs[i].codes) && aligned16(segs[i].scales);
-    const uint64_t nt = tiled ? segs[i].n / kTileElems : 0;
+    const uint64_t nt = tiled ? segs[i].n / act_unit() : 0;
     if (nt > 0) {
       if (k == kMaxSeg) return set_error(AGQ_ERR_INVALID_ARGUMENT, "too many segments");
       st.codes[k] = segs[i].codes;
@@ -817,7 +1245,7 @@ agq_status dequantize_grouped_device(const agq_segment* segs, int nseg, int out_
   }
   for (int i = 0; i < nseg; ++i) {
     const bool tiled = aligned16(segs[i].x) && aligned16(segs[i].codes) && aligned16(segs[i].scales);
-    const uint64_t done = tiled ? (segs[i].n / kTileElems) * kTileElems : 0;
+    const uint64_t done = tiled ? (segs[i].n / act_unit()) * act_unit() : 0;
     if (done == segs[i].n) continue;
     const size_t esz = out_dtype == AGQ_BF16 ? 2 : 4;
     agq_status r = dequantize_device(

@@ -65,6 +65,14 @@ AGQ_HD int rint_int(float v) {  // round to nearest, ties to even
 #endif
 }
 AGQ_HD float ffloor(float v) { return floorf(v); }
+
+// Round-to-nearest-even to an integer for |v| < 2^22 with one FP32 add: the
+// sum v + 1.5*2^23 is rounded by the adder (RNE, ties to even because the
+// magic constant is even) and its low mantissa bits hold the integer.
+constexpr float kMagicRound = 12582912.0f;   // 1.5 * 2^23, bits 0x4B400000
+constexpr uint32_t kMagicBits = 0x4B400000u;
+AGQ_HD uint32_t f2u(float f);
+AGQ_HD float u2f(uint32_t u);
 AGQ_HD uint32_t f2u(float f) {
 #if defined(__CUDA_ARCH__)
   return __float_as_uint(f);
@@ -135,7 +143,7 @@ AGQ_HD int linear_k_bf16(float x, float a, float inv, float rcp, float Lf) {
   const float xl = fmul(x, Lf);            // exact: 8-bit x times 7-bit L
   const float r = ffma(-v, a, xl);         // exact residual x*L - v*a
   const float v2 = ffma(r, rcp, v);        // v + r/a: corrected quotient
-  return rint_int(v2);
+  return (int)(f2u(fadd(v2, kMagicRound)) - kMagicBits);
 }
 
 // General FP32 path: decide against the candidate boundary h = floor(v)+1/2

@@ -32,6 +32,9 @@ def timeit(fn, iters=20, warm=3):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--which", default="all")
+    ap.add_argument("--n", type=int, default=0, help="act: single size")
+    ap.add_argument("--bits", type=int, default=0, help="act: single width")
+    ap.add_argument("--iters", type=int, default=20)
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     res = []
@@ -47,10 +50,13 @@ def main():
 
     if args.which in ("all", "act"):
         # C1: 4096^2 and C2-sized tensors, rotating copies to defeat L2
-        for n, label in ((4096 * 4096, "C1"), (16384 * 14336, "C2silu")):
+        sizes = ((4096 * 4096, "C1"), (16384 * 14336, "C2silu"))
+        if args.n:
+            sizes = ((args.n, f"n{args.n}"),)
+        for n, label in sizes:
             R = max(2, int(1.2e9 // (n * 2)) + 1)
             xs = [torch.randn(n, device=dev).to(torch.bfloat16) for _ in range(R)]
-            for bits in (4, 5, 6, 7, 8):
+            for bits in ((args.bits,) if args.bits else (4, 5, 6, 7, 8)):
                 qs = [A.quantize_blockwise(x, bits, check=False) for x in xs]
                 outs = [torch.empty(n, dtype=torch.bfloat16, device=dev) for _ in range(R)]
                 nq = n * 2 + n * bits / 8 + n / 128 * 4
@@ -62,8 +68,8 @@ def main():
                     q, o = qs[i % R], outs[i % R]
                     L.lib.agq_dequantize(q.codes.data_ptr(), L.AGQ_CODES_PACKED, q.scales.data_ptr(), n,
                                          bits, 128, 0, o.data_ptr(), L.AGQ_BF16, 0, None, stream)
-                report(f"{label}_quant_b{bits}", timeit(fq), nq)
-                report(f"{label}_dequant_b{bits}", timeit(fd), nq)
+                report(f"{label}_quant_b{bits}", timeit(fq, args.iters), nq)
+                report(f"{label}_dequant_b{bits}", timeit(fd, args.iters), nq)
             del xs, qs, outs
             torch.cuda.empty_cache()
     if args.which in ("all", "acc"):

@@ -1,0 +1,590 @@
+"""Benchmark of the AGoQ quantization hot path on B200 (bench contract).
+
+Metric (BASELINE.json): activation quant+dequant GB/s vs HBM peak; 8-bit
+gradient all-reduce bus GB/s at 1/2/4/8 GPUs.
+
+Workload of `value` (config C2): one LLaMA-8B transformer block's stored
+activations at seq 4096 x micro-batch 4 (T = 16384 tokens; norm1/norm2/out-proj
+inputs T x 4096, SiLU gate/value T x 14336 = 671,088,640 BF16 elements), stored
+under EVERY stage policy of an 8-stage DBCA pipeline (dbca.hpp plan_bit_widths
+-> widths 4,4,5,5,6,7,8,8): per stage one grouped quantize launch (BF16 ->
+packed codes + FP32 block scales) and one grouped dequantize launch (-> BF16).
+A step = all 8 stages. value = algorithmic bytes / device time:
+  per element quant 2 + b/8 + 4/128 B, dequant b/8 + 4/128 + 2 B.
+Inputs (1.34 GB) and outputs are far larger than L2 (126 MB).
+
+Also reported on the same line:
+  accumulate : config C3, FP8 local_accumulate over 8,030,261,248 params
+               (LLaMA-8B), FP32 local gradient, in place, 6.0625 B/param.
+  allreduce  : (N > 1) config C4, decomposed 8-bit all-reduce of the
+               LLaMA-8B FP8 gradient, NCCL and fused-NVLink algorithms, vs a
+               BF16 ncclAllReduce of the same gradient.
+  e2e        : the activation metric through the host-buffer path: pinned
+               host BF16 activations -> device every step, dequantized outputs
+               of every stage -> host.
+  roofline, cpu_baseline, clocks, gpu_launches: see the bench contract.
+
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref, the unmodified reference headers compiled as-is) of the same
+workload on a bounded sample, on all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+T_TOKENS = 4 * 4096
+HIDDEN, FFN = 4096, 14336
+TENSORS = [("norm1_input", HIDDEN), ("norm2_input", HIDDEN), ("outproj_input", HIDDEN),
+           ("silu_gate", FFN), ("silu_value", FFN)]
+LLAMA8B_PARAMS = 8_030_261_248
+METRIC = "act quant+dequant GB/s vs HBM peak; INT8 grad all-reduce bus GB/s @1/2/4/8 GPU"
+
+
+def stage_bits():
+    import paper_2605_00539_b200 as A
+    return A.plan_bit_widths(A.PipelineConfig(8, 16, 2)).assigned()
+
+
+def act_bytes_per_elem(bits):
+    q = 2 + bits / 8 + 4 / 128
+    return q, q  # quant, dequant (bf16 in / bf16 out)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/agq_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8 and parts[0].replace(".", "").isdigit():
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows]
+        load = [float(r[0]) for r in rows if float(r[2]) > 150.0] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": float(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if args.impl != "reference":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# our implementation
+# ---------------------------------------------------------------------------
+class ActWorkload:
+    def __init__(self, dev, seed=0):
+        import torch
+        import paper_2605_00539_b200 as A
+        from paper_2605_00539_b200 import _lib as L
+        self.A, self.L, self.torch = A, L, torch
+        self.dev = dev
+        g = torch.Generator(device=dev).manual_seed(seed)
+        scales = [1.0, 1.0, 0.5, 4.0, 1.0]  # per-tensor magnitudes
+        self.x = [(torch.randn(T_TOKENS * w, device=dev, generator=g) * s).to(torch.bfloat16)
+                  for (name, w), s in zip(TENSORS, scales)]
+        self.n = [t.numel() for t in self.x]
+        self.N = sum(self.n)
+        self.bits = stage_bits()
+        self.out = [torch.empty_like(t) for t in self.x]
+        self.q = {}
+        for b in sorted(set(self.bits)):
+            self.q[b] = [(torch.empty(int(L.lib.agq_packed_bytes(n, b)), dtype=torch.uint8, device=dev),
+                          torch.empty((n + 127) // 128, dtype=torch.float32, device=dev)) for n in self.n]
+        self.err = A.ErrorRecord(dev).reset()
+        self.segq, self.segd = {}, {}
+        for b in self.q:
+            sq = (L.AgqSegment * 5)()
+            sd = (L.AgqSegment * 5)()
+            for i in range(5):
+                c, s = self.q[b][i]
+                sq[i] = L.AgqSegment(self.x[i].data_ptr(), c.data_ptr(), s.data_ptr(), self.n[i])
+                sd[i] = L.AgqSegment(self.out[i].data_ptr(), c.data_ptr(), s.data_ptr(), self.n[i])
+            self.segq[b], self.segd[b] = sq, sd
+
+    def bytes_per_step(self):
+        return sum(self.N * sum(act_bytes_per_elem(b)) for b in self.bits)
+
+    def quant(self, b, stream):
+        self.L.check(self.L.lib.agq_quantize_grouped(self.segq[b], 5, self.L.AGQ_BF16, b, 0,
+                                                     self.err.ptr, stream))
+
+    def dequant(self, b, stream):
+        self.L.check(self.L.lib.agq_dequantize_grouped(self.segd[b], 5, self.L.AGQ_BF16, b, 0, stream))
+
+    def step(self, stream, ev=None):
+        for i, b in enumerate(self.bits):
+            if ev is not None:
+                ev[4 * i].record()
+            self.quant(b, stream)
+            if ev is not None:
+                ev[4 * i + 1].record()
+                ev[4 * i + 2].record()
+            self.dequant(b, stream)
+            if ev is not None:
+                ev[4 * i + 3].record()
+
+    def verify_sample(self):
+        """Bit-exact spot check of one block per tensor against the oracle."""
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import numpy as np
+        import oracle_ffi as O
+        b = self.bits[-1]
+        self.quant(b, self.torch.cuda.current_stream().cuda_stream)
+        self.torch.cuda.synchronize()
+        ok = True
+        for i in range(5):
+            blk = (self.n[i] // 128) // 2
+            x = self.x[i][blk * 128:(blk + 1) * 128].float().cpu().numpy()
+            c, s = O.quantize(x, b, 128, 0)
+            codes, scales = self.q[b][i]
+            got = codes[blk * 16 * b:(blk + 1) * 16 * b].cpu().numpy()
+            ok &= bool(np.array_equal(got, O.pack(c, b))) and float(scales[blk]) == float(s[0])
+        return ok
+
+
+def bench_act(wl, args, world):
+    import torch
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    for _ in range(args.warmup):
+        wl.step(sp)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4 * len(wl.bits) * args.steps)]
+    launches0 = wl.A.launch_count()
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for k in range(args.steps):
+        wl.step(sp, ev[4 * len(wl.bits) * k: 4 * len(wl.bits) * (k + 1)])
+    t1.record()
+    torch.cuda.synchronize()
+    launches = wl.A.launch_count() - launches0
+    sec = t0.elapsed_time(t1) * 1e-3
+    barrier(world)
+    sec = max_over_ranks(sec, world)
+    # per-kernel durations on the launching stream
+    qt, dt = [], []
+    qb, db = [], []
+    for k in range(args.steps):
+        for i, b in enumerate(wl.bits):
+            base = 4 * len(wl.bits) * k + 4 * i
+            qt.append(ev[base].elapsed_time(ev[base + 1]) * 1e-3)
+            dt.append(ev[base + 2].elapsed_time(ev[base + 3]) * 1e-3)
+            qb.append(wl.N * act_bytes_per_elem(b)[0])
+            db.append(wl.N * act_bytes_per_elem(b)[1])
+    wl.L.errors_message(wl.err.read(), wl.L.AGQ_OP_QUANTIZE)
+    return sec, launches, (sum(qb) / sum(qt) / 1e9, sum(qt)), (sum(db) / sum(dt) / 1e9, sum(dt))
+
+
+def bench_e2e(wl, args, world, steps):
+    """Host-buffer path: pinned BF16 activations H2D every step, all stage
+    policies quantize+dequantize on device, each stage's BF16 reconstruction
+    D2H (what dequantize_blockwise returns to a host caller)."""
+    import torch
+    host_in = [torch.empty(n, dtype=torch.bfloat16, pin_memory=True) for n in wl.n]
+    for h, x in zip(host_in, wl.x):
+        h.copy_(x)
+    host_out = [torch.empty(n, dtype=torch.bfloat16, pin_memory=True) for n in wl.n]
+    sp = torch.cuda.current_stream().cuda_stream
+
+    def one():
+        for h, x in zip(host_in, wl.x):
+            x.copy_(h, non_blocking=True)
+        for b in wl.bits:
+            wl.quant(b, sp)
+            wl.dequant(b, sp)
+            for h, o in zip(host_out, wl.out):
+                h.copy_(o, non_blocking=True)
+
+    one()
+    torch.cuda.synchronize()
+    barrier(world)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        one()
+    e.record()
+    torch.cuda.synchronize()
+    sec = max_over_ranks(s.elapsed_time(e) * 1e-3, world)
+    bi = sum(wl.n) * 2
+    bo = sum(wl.n) * 2 * len(wl.bits)
+    return wl.bytes_per_step() * steps * world / sec / 1e9, bi, bo
+
+
+def bench_accumulate(dev, args, n_params):
+    """C3: FP8 local_accumulate over an 8B-param gradient, FP32 local grads."""
+    import torch
+    import paper_2605_00539_b200 as A
+    from paper_2605_00539_b200 import _lib as L
+    codes = torch.empty(n_params, dtype=torch.uint8, device=dev)
+    scales = torch.empty((n_params + 127) // 128, dtype=torch.float32, device=dev)
+    local = torch.empty(n_params, dtype=torch.float32, device=dev)
+    g = torch.Generator(device=dev).manual_seed(1)
+    chunk = 1 << 28
+    for off in range(0, n_params, chunk):
+        m = min(chunk, n_params - off)
+        x = torch.randn(m, device=dev, generator=g) * 1e-3
+        L.check(L.lib.agq_quantize(x.data_ptr(), L.AGQ_F32, m, 8, 128, 2, codes[off:].data_ptr(),
+                                   L.AGQ_CODES_BYTES, scales[off // 128:].data_ptr(), None,
+                                   torch.cuda.current_stream().cuda_stream))
+        local[off:off + m].normal_(0.0, 1e-3, generator=g)
+        del x
+    err = A.ErrorRecord(dev).reset()
+    sp = torch.cuda.current_stream().cuda_stream
+
+    def run():
+        L.check(L.lib.agq_fp8_accumulate(codes.data_ptr(), scales.data_ptr(), local.data_ptr(),
+                                         L.AGQ_F32, n_params, 128, 0, codes.data_ptr(),
+                                         scales.data_ptr(), err.ptr, sp))
+    for _ in range(2):
+        run()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = max(3, min(args.steps, 10))
+    s.record()
+    for _ in range(iters):
+        run()
+    e.record()
+    torch.cuda.synchronize()
+    sec = s.elapsed_time(e) * 1e-3 / iters
+    L.errors_message(err.read(), L.AGQ_OP_ACCUMULATE)
+    nbytes = n_params * (1 + 4 / 128) * 2 + n_params * 4
+    del codes, scales, local
+    torch.cuda.empty_cache()
+    return {"config": "C3 FP8 local_accumulate, LLaMA-8B params, fp32 local, in place",
+            "params": n_params, "ms": round(sec * 1e3, 3), "GBs": round(nbytes / sec / 1e9, 1),
+            "bytes_per_param": 6.0625}
+
+
+def bench_allreduce(dev, args, world, rank, n):
+    """C4: decomposed 8-bit all-reduce vs BF16 ncclAllReduce, same gradient."""
+    import torch
+    import paper_2605_00539_b200 as A
+    from paper_2605_00539_b200 import _lib as L
+    from paper_2605_00539_b200.collective import Communicator
+    comm = Communicator(device=dev.index)
+    sp = torch.cuda.current_stream().cuda_stream
+    nb = (n + 127) // 128
+    g = torch.Generator(device=dev).manual_seed(100 + rank)
+    src_codes = torch.empty(n, dtype=torch.uint8, device=dev)
+    src_scales = torch.empty(nb, dtype=torch.float32, device=dev)
+    chunk = 1 << 28
+    for off in range(0, n, chunk):
+        m = min(chunk, n - off)
+        x = torch.randn(m, device=dev, generator=g) * 1e-3
+        L.check(L.lib.agq_quantize(x.data_ptr(), L.AGQ_F32, m, 8, 128, 2, src_codes[off:].data_ptr(),
+                                   L.AGQ_CODES_BYTES, src_scales[off // 128:].data_ptr(), None, sp))
+        del x
+    q = A.QuantizedTensor(torch.empty_like(src_codes), torch.empty_like(src_scales), 8, 128, (n,),
+                          A.CodecKind.Fp8E4M3, packed=False)
+    err = A.ErrorRecord(dev).reset()
+    res = {"config": f"C4 decomposed 8-bit all-reduce, {n} FP8 elements per rank",
+           "elements": n, "world": world}
+    iters = max(2, min(args.steps, 5))
+
+    def timed(fn, reset):
+        for _ in range(1):
+            reset()
+            fn()
+        torch.cuda.synchronize()
+        barrier(world)
+        tot = 0.0
+        for _ in range(iters):
+            reset()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            fn()
+            e.record()
+            torch.cuda.synchronize()
+            tot += s.elapsed_time(e) * 1e-3
+        return max_over_ranks(tot / iters, world)
+
+    wire = n * (1 + 4 / 128)
+    fac = 2 * (world - 1) / world
+    for algo in args.algos:
+        if algo == "p2p":
+            comm.enable_p2p(n)
+            pc, ps = comm.p2p_buffers(n)
+            qq = A.QuantizedTensor(pc, ps, 8, 128, (n,), A.CodecKind.Fp8E4M3, packed=False)
+        else:
+            qq = q
+
+        def reset(qq=qq):
+            qq.codes.copy_(src_codes)
+            qq.scales.copy_(src_scales)
+
+        def fn(qq=qq, algo=algo):
+            L.check(L.lib.agq_allreduce_fp8(comm._h, qq.codes.data_ptr(), qq.scales.data_ptr(), n, 128,
+                                            comm.ALGOS[algo], err.ptr, sp))
+        err.reset()
+        sec = timed(fn, reset)
+        L.errors_message(err.read(), L.AGQ_OP_ALLREDUCE)
+        res[algo] = {"ms": round(sec * 1e3, 3), "bus_GBs_wire": round(fac * wire / sec / 1e9, 1),
+                     "bus_GBs_bf16_equiv": round(fac * 2 * n / sec / 1e9, 1)}
+        if algo == "p2p" and "nccl" in args.algos:
+            ok = torch.equal(qq.codes, q.codes) and torch.equal(qq.scales, q.scales)
+            res["p2p_equals_nccl"] = bool(ok)
+        if algo == "nccl":
+            pass
+    del src_codes
+    # BF16 baseline on the same element count
+    gb = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    for off in range(0, n, chunk):
+        m = min(chunk, n - off)
+        gb[off:off + m] = (torch.randn(m, device=dev, generator=g) * 1e-3).to(torch.bfloat16)
+
+    def bf16():
+        L.check(L.lib.agq_allreduce_bf16_nccl(comm._h, gb.data_ptr(), n, sp))
+    sec = timed(bf16, lambda: None)
+    res["bf16_nccl"] = {"ms": round(sec * 1e3, 3), "bus_GBs": round(fac * 2 * n / sec / 1e9, 1)}
+    best = min((res[a]["ms"] for a in args.algos))
+    res["speedup_vs_bf16_nccl"] = round(res["bf16_nccl"]["ms"] / best, 3)
+    del gb, q
+    comm.close()
+    torch.cuda.empty_cache()
+    return res
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------------------
+# the reference's CPU implementation (oracle/_ref) on a bounded sample
+# ---------------------------------------------------------------------------
+def cpu_reference_rate(sample_elems, threads, rounds=1, min_seconds=0.0):
+    """GB/s (same algorithmic bytes as the GPU arm) of quantize_blockwise +
+    dequantize_blockwise of the reference over every stage width, on
+    `sample_elems` BF16-valued inputs, `threads` host threads over disjoint
+    block ranges (blocks are independent, quantize.hpp:103-136)."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_ffi as O
+    kind = "reference" if O.ref is not None else "port"
+    lib = O.ref if O.ref is not None else None
+    rng = np.random.default_rng(0)
+    x = O.bf16_round(rng.standard_normal(sample_elems).astype(np.float32))
+    codes = np.empty(sample_elems, np.uint8)
+    scales = np.empty((sample_elems + 127) // 128, np.float32)
+    out = np.empty(sample_elems, np.float32)
+    bits = stage_bits()
+    t0 = time.perf_counter()
+    nbytes = 0.0
+    r = 0
+    while r < rounds or time.perf_counter() - t0 < min_seconds:
+        r += 1
+        for b in bits:
+            if lib is not None:
+                st = lib.ref_quantize_mt(O._p(x), sample_elems, b, 128, 0, O._p(codes), O._p(scales), threads)
+                st |= lib.ref_dequantize_mt(O._p(codes), O._p(scales), sample_elems, b, 128, 0, O._p(out),
+                                            threads)
+                assert st == 0
+            else:
+                c, s = O.quantize(x, b, 128, 0)
+                O.dequantize(c, s, b, 128, 0)
+            nbytes += sample_elems * sum(act_bytes_per_elem(b))
+    sec = time.perf_counter() - t0
+    return nbytes / sec / 1e9, kind, sec
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    sample = 1 << 24
+    for _ in range(args.warmup):
+        cpu_reference_rate(sample, threads)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, kind, _ = cpu_reference_rate(sample, threads)
+        vals.append(v)
+    sec = time.perf_counter() - t0
+    value = sum(vals) / len(vals)
+    line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(sec / args.steps * 1e3, 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8 codes / f32 scales (bf16-valued f32 in)",
+            "data": "synthetic N(0,1) rounded to bf16", "impl": "reference",
+            "config": {"workload": "C2 sample: quantize_blockwise+dequantize_blockwise, block 128, "
+                                   "SymmetricLinear, every 8-stage DBCA width (4,4,5,5,6,7,8,8)",
+                       "sample_elements_per_stage": sample},
+            "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": kind,
+                             "sample": f"{sample} elements x 8 stage widths per step"},
+            "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ar-elements", type=int, default=LLAMA8B_PARAMS)
+    ap.add_argument("--acc-elements", type=int, default=LLAMA8B_PARAMS)
+    ap.add_argument("--algos", default="nccl,p2p")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-accumulate", action="store_true")
+    ap.add_argument("--no-allreduce", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.algos = [a for a in args.algos.split(",") if a]
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+
+    import torch
+    import paper_2605_00539_b200 as A
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if not A.device_ok():
+        raise SystemExit("not an sm_100 device: the AGoQ kernels have no other path")
+    peak, peak_kind = load_peaks()
+    clocks = Clocks(local)
+
+    wl = ActWorkload(dev)
+    parity = wl.verify_sample()
+    clocks.start()
+    sec, launches, (q_gbs, q_time), (d_gbs, d_time) = bench_act(wl, args, world)
+    step_bytes = wl.bytes_per_step()
+    value = step_bytes * args.steps * world / sec / 1e9
+    extra = {}
+    if not args.no_e2e:
+        e2e_val, bi, bo = bench_e2e(wl, args, world, steps=2)
+        extra["e2e"] = {"value": round(e2e_val, 1), "unit": "GB/s", "h2d_bytes_per_step": bi,
+                        "d2h_bytes_per_step": bo}
+    del wl
+    torch.cuda.empty_cache()
+    if not args.no_accumulate:
+        extra["accumulate"] = bench_accumulate(dev, args, args.acc_elements)
+    if world > 1 and not args.no_allreduce:
+        extra["allreduce"] = bench_allreduce(dev, args, world, rank, args.ar_elements)
+    clk = clocks.stop()
+
+    dom_name, dom_gbs, other = ("k_quant_warp", q_gbs, {"k_dequant_warp_GBs": round(d_gbs, 1)}) \
+        if q_time >= d_time else ("k_dequant_warp", d_gbs, {"k_quant_warp_GBs": round(q_gbs, 1)})
+    traffic = load_traffic().get(dom_name)
+    roofline = {"bound": "hbm", "achieved": round(dom_gbs, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(dom_gbs / peak, 4), "traffic": traffic, "kernel": dom_name,
+                "peak_kind": peak_kind, **other}
+    line = {"metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(sec / args.steps * 1e3, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16 in/out, u4-u8 packed codes, f32 scales",
+            "data": "synthetic N(0,1) activations (torch.Generator seed 0), per-tensor scales",
+            "config": {"workload": "C2: LLaMA-8B block stored activations (seq 4096 x mb 4), "
+                                   "8-stage DBCA policies, quant+dequant",
+                       "elements_per_stage": sum(T_TOKENS * w for _, w in TENSORS),
+                       "stage_bits": stage_bits(), "block": 128,
+                       "l2": "inputs/outputs 1.3 GB per pass >> 126 MB L2 (no flush needed)",
+                       "parallelism": f"replicas x{world}"},
+            "roofline": roofline, "gpu_launches": launches, "parity_sample_bitexact": parity,
+            "clocks": clk, **extra}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, kind, csec = cpu_reference_rate(1 << 24, os.cpu_count() or 1, min_seconds=8.0)
+        line["cpu_baseline"] = {"value": round(v, 3), "unit": "GB/s", "cores": os.cpu_count() or 1,
+                                "kind": kind,
+                                "sample": f"2^24 BF16-valued elements x 8 stage widths, repeated "
+                                          f"for {csec:.1f} s of CPU time"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,101 @@
+"""Multi-GPU parity of the decomposed 8-bit all-reduce (run under torchrun,
+one process per GPU). Every rank regenerates every rank's FP8 gradient from
+its seed, so each rank checks its result against the CPU oracle's
+allreduce_decomposed bit for bit, for both algorithms (NCCL grouped
+send/recv + reduce kernel; fused NVLink peer-memory kernel), ragged sizes,
+P=1..world, and the overflow abort (collective.hpp:278-281) on every rank."""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+sys.path.insert(0, os.path.dirname(HERE))
+import oracle_ffi as O  # noqa: E402
+import paper_2605_00539_b200 as A  # noqa: E402
+from paper_2605_00539_b200.collective import Communicator  # noqa: E402
+
+
+def grads(world, n, seed, big_rank=-1):
+    out = []
+    for r in range(world):
+        rng = np.random.default_rng(seed * 100 + r)
+        mag = np.repeat(10.0 ** rng.uniform(-6, 2, (n + 127) // 128), 128)[:n]
+        x = (rng.standard_normal(n) * mag).astype(np.float32)
+        if r == big_rank:
+            x[:256] = 3e38
+        out.append(O.quantize(x, 8, 128, O.FP8))
+    return out
+
+
+def main():
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    dev = torch.device("cuda", local)
+    comm = Communicator(device=local)
+    cap = 8192 * 9 + 300
+    comm.enable_p2p(cap)
+    fails = 0
+    for seed, n in enumerate([128, 1000, 8192 * 3 + 300, 8192 * 9 + 300, 77]):
+        g = grads(world, n, seed)
+        want_c, want_s = O.allreduce_decomposed([c for c, _ in g], [s for _, s in g])
+        for algo in ("nccl", "p2p"):
+            c, s = g[rank]
+            if algo == "p2p":
+                pc, ps = comm.p2p_buffers(n)
+                pc.copy_(torch.from_numpy(c))
+                ps.copy_(torch.from_numpy(s))
+                q = A.QuantizedTensor(pc, ps, 8, 128, (n,), A.CodecKind.Fp8E4M3, packed=False)
+            else:
+                q = A.QuantizedTensor(torch.from_numpy(c).to(dev), torch.from_numpy(s).to(dev), 8, 128,
+                                      (n,), A.CodecKind.Fp8E4M3, packed=False)
+            comm.allreduce_fp8(q, algo=algo)
+            ok = np.array_equal(q.codes.cpu().numpy(), want_c) and \
+                np.array_equal(q.scales.cpu().numpy().view(np.uint32), want_s.view(np.uint32))
+            if not ok:
+                fails += 1
+                print(f"rank {rank}: MISMATCH algo={algo} n={n}", flush=True)
+    # an fp32 overflow in ONE owner's local reduce aborts the protocol on
+    # every rank (collective.hpp:278-281): block 0 (owned by rank 0) holds
+    # 3e38 on every rank, so only rank 0's reduce overflows.
+    if world > 1:
+        for algo in ("nccl", "p2p"):
+            n = 8192 * 2
+            g = grads(world, n, 99, big_rank=-1)
+            c, s = g[rank]
+            big_c, big_s = O.quantize(np.full(128, 3e38, np.float32), 8, 128, O.FP8)
+            c = c.copy()
+            s = s.copy()
+            c[:128], s[0] = big_c, big_s[0]
+            if algo == "p2p":
+                pc, ps = comm.p2p_buffers(n)
+                pc.copy_(torch.from_numpy(c))
+                ps.copy_(torch.from_numpy(s))
+                q = A.QuantizedTensor(pc, ps, 8, 128, (n,), A.CodecKind.Fp8E4M3, packed=False)
+            else:
+                q = A.QuantizedTensor(torch.from_numpy(c).to(dev), torch.from_numpy(s).to(dev), 8,
+                                      128, (n,), A.CodecKind.Fp8E4M3, packed=False)
+            try:
+                comm.allreduce_fp8(q, algo=algo)
+                fails += 1
+                print(f"rank {rank}: no overflow raised algo={algo}", flush=True)
+            except A.ProtocolError as e:
+                if "fp32 overflow" not in str(e):
+                    fails += 1
+                    print(f"rank {rank}: wrong error {e}", flush=True)
+    t = torch.tensor([fails], device=dev)
+    dist.all_reduce(t)
+    if rank == 0:
+        print(f"mp_allreduce_check world={world} failures={int(t.item())}", flush=True)
+    comm.close()
+    dist.destroy_process_group()
+    sys.exit(1 if int(t.item()) else 0)
+
+
+if __name__ == "__main__":
+    main()

@@ -181,6 +181,7 @@ agq_status agq_allreduce_naive_simulated(int world, const uint8_t* const* codes,
                                          const float* const* scales, uint64_t n,
                                          uint32_t block, uint8_t* out_codes,
                                          float* out_scales, agq_errors* d_err,
+                                         unsigned long long* d_events /* world, or NULL */,
                                          agq_stream_t stream);
 
 /* ---- multi-GPU decomposed all-reduce (one process per GPU) --------------- */
@@ -234,7 +235,8 @@ agq_status agq_allreduce_simulated_host(int world, const uint8_t* const* codes,
                                         const float* const* scales, uint64_t n,
                                         uint32_t block, int protocol /*0 dec,1 naive*/,
                                         uint8_t* out_codes, float* out_scales,
-                                        uint64_t* overflow_elements);
+                                        uint64_t* overflow_elements,
+                                        uint64_t* overflow_events /* world, or NULL */);
 
 /* ---- L2b control plane (dbca.hpp, host) ---------------------------------- */
 /* dbca.hpp:34-41 stored_activation_counts; counts[n_stages]. */

@@ -81,7 +81,7 @@ def _load() -> C.CDLL:
         "agq_allreduce_simulated": (I, [I, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), U64, U32,
                                         P, P, P, S]),
         "agq_allreduce_naive_simulated": (I, [I, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), U64,
-                                              U32, P, P, P, S]),
+                                              U32, P, P, P, P, S]),
         "agq_comm_unique_id": (I, [C.c_char_p]),
         "agq_comm_init": (I, [C.POINTER(C.c_void_p), C.c_char_p, I, I, I]),
         "agq_comm_p2p_export": (I, [P, U64, C.c_char_p]),
@@ -96,7 +96,8 @@ def _load() -> C.CDLL:
         "agq_dequantize_host": (I, [P, P, U64, I, U32, I, P]),
         "agq_local_accumulate_host": (I, [P, P, U64, U32, P, I, P, P]),
         "agq_allreduce_simulated_host": (I, [I, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), U64,
-                                             U32, I, P, P, C.POINTER(C.c_uint64)]),
+                                             U32, I, P, P, C.POINTER(C.c_uint64),
+                                             C.POINTER(C.c_uint64)]),
         "agq_stored_activation_counts": (I, [I, I, I, C.POINTER(C.c_int)]),
         "agq_plan_bit_widths": (I, [I, I, I, C.POINTER(C.c_int), C.POINTER(C.c_double),
                                     C.POINTER(C.c_int)]),

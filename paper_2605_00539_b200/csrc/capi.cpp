@@ -39,7 +39,8 @@ agq_status reduce_requant_device(int np, const uint8_t* const* pc, const float* 
                                  cudaStream_t s);
 agq_status naive_ring_device(int world, const uint8_t* const* codes, const float* const* scales,
                              uint64_t n, uint32_t block, const uint64_t* d_ranges, uint8_t* oc,
-                             float* os, agq_errors* err, cudaStream_t s);
+                             float* os, agq_errors* err, unsigned long long* events,
+                             cudaStream_t s);
 agq_status comm_unique_id(unsigned char id[128]);
 agq_status comm_init(agq_comm** out, const unsigned char id[128], int nranks, int rank,
                      int device);
@@ -336,7 +337,8 @@ agq_status agq_allreduce_simulated(int world, const uint8_t* const* codes,
 agq_status agq_allreduce_naive_simulated(int world, const uint8_t* const* codes,
                                          const float* const* scales, uint64_t n, uint32_t block,
                                          uint8_t* out_codes, float* out_scales,
-                                         agq_errors* d_err, agq_stream_t stream) {
+                                         agq_errors* d_err, unsigned long long* d_events,
+                                         agq_stream_t stream) {
   if (world < 1 || world > AGQ_MAX_WORLD) return set_error(AGQ_ERR_INVALID_ARGUMENT, "no workers");
   if (agq_status st = check_args(8, block, AGQ_CODEC_FP8_E4M3)) return st;
   if (!d_err) return set_error(AGQ_ERR_INVALID_ARGUMENT, "naive protocol needs an error record");
@@ -348,7 +350,7 @@ agq_status agq_allreduce_naive_simulated(int world, const uint8_t* const* codes,
   if (e != cudaSuccess) return cuda_fail(e, "naive: ranges");
   cudaMemcpyAsync(d_rg, rg.data(), rg.size() * 8, cudaMemcpyHostToDevice, s);
   agq_status st = naive_ring_device(world, codes, scales, n, block, d_rg, out_codes, out_scales,
-                                    d_err, s);
+                                    d_err, d_events, s);
   cudaFreeAsync(d_rg, s);
   // the host copy above must outlive the async copy
   cudaStreamSynchronize(s);
@@ -473,18 +475,20 @@ agq_status agq_local_accumulate_host(const uint8_t* codes, const float* scales, 
 agq_status agq_allreduce_simulated_host(int world, const uint8_t* const* codes,
                                         const float* const* scales, uint64_t n, uint32_t block,
                                         int protocol, uint8_t* out_codes, float* out_scales,
-                                        uint64_t* overflow_elements) {
+                                        uint64_t* overflow_elements, uint64_t* overflow_events) {
   if (world < 1 || world > AGQ_MAX_WORLD) return set_error(AGQ_ERR_INVALID_ARGUMENT, "no workers");
   if (agq_status st = check_args(8, block, AGQ_CODEC_FP8_E4M3)) return st;
   if (agq_status st = check_device()) return st;
   if (overflow_elements) *overflow_elements = 0;
+  if (overflow_events)
+    for (int r = 0; r < world; ++r) overflow_events[r] = 0;
   if (n == 0) return AGQ_OK;
   Workspace& w = workspace();
   std::lock_guard<std::mutex> lk(w.mu);
   const uint64_t nb = (n + block - 1) / block;
   const size_t per = al(n) + al(nb * 4);
-  const size_t oo = per * world, oe = oo + per;
-  if (agq_status st = ws_reserve(w, oe + al(sizeof(agq_errors)))) return st;
+  const size_t oo = per * world, oe = oo + per, ov = oe + al(sizeof(agq_errors));
+  if (agq_status st = ws_reserve(w, ov + al(8 * world))) return st;
   char* base = static_cast<char*>(w.dev);
   cudaStream_t s = w.stream;
   std::vector<const uint8_t*> dc(world);
@@ -497,20 +501,24 @@ agq_status agq_allreduce_simulated_host(int world, const uint8_t* const* codes,
     ds[r] = reinterpret_cast<float*>(p + al(n));
   }
   agq_errors* d_err = reinterpret_cast<agq_errors*>(base + oe);
+  unsigned long long* d_ev = reinterpret_cast<unsigned long long*>(base + ov);
   agq_errors_reset(d_err, (agq_stream_t)s);
+  cudaMemsetAsync(d_ev, 0, 8 * world, s);
   uint8_t* ocd = reinterpret_cast<uint8_t*>(base + oo);
   float* osd = reinterpret_cast<float*>(base + oo + al(n));
   agq_status st = protocol == 0
                       ? agq_allreduce_simulated(world, dc.data(), ds.data(), n, block, ocd, osd,
                                                 d_err, (agq_stream_t)s)
                       : agq_allreduce_naive_simulated(world, dc.data(), ds.data(), n, block, ocd,
-                                                      osd, d_err, (agq_stream_t)s);
+                                                      osd, d_err, d_ev, (agq_stream_t)s);
   if (st) return st;
   agq_errors h;
   cudaMemcpyAsync(&h, d_err, sizeof(h), cudaMemcpyDeviceToHost, s);
   if (agq_status e = cuda_fail(cudaStreamSynchronize(s), "allreduce_host")) return e;
   if (agq_status e = agq_errors_message(&h, AGQ_OP_ALLREDUCE, nullptr, 0)) return e;
   if (overflow_elements) *overflow_elements = h.saturated;
+  if (overflow_events)
+    cudaMemcpyAsync(overflow_events, d_ev, 8 * world, cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(out_codes, ocd, n, cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(out_scales, osd, nb * 4, cudaMemcpyDeviceToHost, s);
   return cuda_fail(cudaStreamSynchronize(s), "allreduce_host");

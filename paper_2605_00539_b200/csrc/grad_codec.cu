@@ -265,7 +265,8 @@ __global__ void __launch_bounds__(256)
 // independent; each step reads the snapshot of the previous step).
 // ---------------------------------------------------------------------------
 __global__ void k_naive_ring(PieceTable pt, uint64_t n, uint32_t block, const uint64_t* ranges,
-                             uint8_t* out_codes, float* out_scales, agq_errors* err) {
+                             uint8_t* out_codes, float* out_scales, agq_errors* err,
+                             unsigned long long* events) {
   __shared__ double lut[128];
   fill_fp8_unit_lut(lut);
   __syncthreads();
@@ -302,7 +303,10 @@ __global__ void k_naive_ring(PieceTable pt, uint64_t n, uint32_t block, const ui
         const double w = unit * 448.0;
         if (fabs(w) > 448.0) over = true;
         nc[r] = (uint8_t)fp8_encode_double(w);
-        if (over) sat = true;
+        if (over) {
+          sat = true;
+          if (events) atomicAdd(&events[r], 1ull);
+        }
       }
       for (int r = 0; r < P; ++r) wc[r] = nc[r];
     }
@@ -440,7 +444,8 @@ agq_status reduce_requant_device(int np, const uint8_t* const* pc, const float* 
 
 agq_status naive_ring_device(int world, const uint8_t* const* codes, const float* const* scales,
                              uint64_t n, uint32_t block, const uint64_t* d_ranges,
-                             uint8_t* oc, float* os, agq_errors* err, cudaStream_t s) {
+                             uint8_t* oc, float* os, agq_errors* err, unsigned long long* events,
+                             cudaStream_t s) {
   if (n == 0) return AGQ_OK;
   PieceTable pt{};
   pt.np = world;
@@ -448,7 +453,7 @@ agq_status naive_ring_device(int world, const uint8_t* const* codes, const float
     pt.codes[r] = codes[r];
     pt.scales[r] = scales[r];
   }
-  k_naive_ring<<<gen_grid(n, 256), 256, 0, s>>>(pt, n, block, d_ranges, oc, os, err);
+  k_naive_ring<<<gen_grid(n, 256), 256, 0, s>>>(pt, n, block, d_ranges, oc, os, err, events);
   count_launch();
   return cuda_fail(cudaGetLastError(), "naive ring: launch");
 }

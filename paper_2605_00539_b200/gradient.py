@@ -116,19 +116,23 @@ def allreduce_simulated(mains: Sequence[QuantizedTensor], stream=None, check: bo
     return out
 
 
-def allreduce_naive_simulated(mains: Sequence[QuantizedTensor], stream=None):
+def allreduce_naive_simulated(mains: Sequence[QuantizedTensor], stream=None, events: bool = False):
     """allreduce_naive_fp8 (collective.hpp:338-431): returns (tensor,
-    overflow_elements)."""
+    overflow_elements[, per-worker overflow_events])."""
     _check_world(mains)
     n, blk = mains[0].num_elements(), mains[0].block_size
     out = QuantizedTensor(torch.empty_like(mains[0].codes), torch.empty_like(mains[0].scales), 8,
                           blk, mains[0].shape, CodecKind.Fp8E4M3, mains[0].packed)
     err = ErrorRecord(mains[0].codes.device).reset(stream)
+    ev = torch.zeros(len(mains), dtype=torch.int64, device=mains[0].codes.device)
     pc = L.ptr_array([q.codes.data_ptr() for q in mains])
     ps = L.ptr_array([q.scales.data_ptr() for q in mains])
     L.check(L.lib.agq_allreduce_naive_simulated(len(mains), pc, ps, n, blk, out.codes.data_ptr(),
-                                                out.scales.data_ptr(), err.ptr, _stream(stream)))
+                                                out.scales.data_ptr(), err.ptr, ev.data_ptr(),
+                                                _stream(stream)))
     h = err.raise_if_any(L.AGQ_OP_ALLREDUCE)
+    if events:
+        return out, int(h.saturated), [int(v) for v in ev.cpu().tolist()]
     return out, int(h.saturated)
 
 

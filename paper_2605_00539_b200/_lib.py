@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libagq_cuda.so")
+LIB_PATH = os.environ.get("AGQ_LIB") or os.path.join(_HERE, "libagq_cuda.so")
 
 AGQ_OK, AGQ_ERR_INVALID_ARGUMENT, AGQ_ERR_RUNTIME, AGQ_ERR_CUDA, AGQ_ERR_NCCL = range(5)
 AGQ_F32, AGQ_BF16 = 0, 1

@@ -300,22 +300,48 @@ __global__ void __launch_bounds__(kThreads)
 // ---------------------------------------------------------------------------
 constexpr int kWarpElems = 1024;
 constexpr int kWarpsPerCta = 8;
+#ifndef AGQ_QUANT_MINB
+#define AGQ_QUANT_MINB 3
+#endif
+#ifndef AGQ_DEQUANT_MINB
+#define AGQ_DEQUANT_MINB 3
+#endif
+
+// Shared-memory swizzle of a warp tile: lane row r (32 elements = kChunks
+// 16-byte chunks) keeps chunk c at slot (c + rot(r)) mod kChunks, so the
+// coalesced writes (8 lanes = one 128-byte phase) and the per-row reads
+// (8 rows, same chunk) are both bank-conflict free, and every lane sees its
+// own row in natural order.
+template <int kChunks>
+__device__ __forceinline__ uint32_t swz_off(uint32_t row, uint32_t c) {
+  const uint32_t rot = kChunks == 4 ? (row >> 1) : row;
+  return row * (kChunks * 16) + ((c + rot) & (kChunks - 1)) * 16;
+}
+// Byte offset in the swizzled tile of the 16-byte chunk at natural offset `o`.
+template <int kChunks>
+__device__ __forceinline__ uint32_t swz_of_linear(uint32_t o) {
+  return swz_off<kChunks>(o / (kChunks * 16), (o / 16) & (kChunks - 1));
+}
+
+struct TileRef {
+  int g;
+  uint64_t lt;
+};
+__device__ __forceinline__ TileRef locate(const SegTable& st, uint64_t t) {
+  if (st.nseg == 1) return {0, t};
+  const int g = seg_of(st, t);
+  return {g, t - st.tile_begin[g]};
+}
 
 template <int BITS, int PACK, int CODEC, typename Tin>
-__device__ __forceinline__ void encode_row(const uint4 (&ch)[InTraits<Tin>::kChunks], int rot,
-                                           float a, bool zero, bool fast,
-                                           uint32_t (&words)[PACK]) {
+__device__ __forceinline__ void encode_row(const uint4 (&ch)[InTraits<Tin>::kChunks], float a,
+                                           bool zero, bool fast, uint32_t (&words)[PACK]) {
   using TR = InTraits<Tin>;
   constexpr int kChunks = TR::kChunks;
   constexpr int kPerChunk = 32 / kChunks;
   constexpr int kChunkBits = kPerChunk * PACK;
   constexpr int L = (1 << (BITS - 1)) - 1;
   constexpr uint32_t kZeroCode = CODEC == 0 ? (uint32_t)L : 0u;
-  float inv = 0.f, rcp = 0.f;
-  if (!zero && fast) {
-    inv = codec_inv(CODEC, BITS, a);
-    if (CODEC == 0 && TR::kBf16) rcp = fdiv(1.0f, a);
-  }
   uint64_t pk[kChunks];
   if (zero) {
     uint64_t zc = 0;
@@ -325,8 +351,10 @@ __device__ __forceinline__ void encode_row(const uint4 (&ch)[InTraits<Tin>::kChu
     for (int j = 0; j < kChunks; ++j) pk[j] = zc;
   } else if (fast) {
     if constexpr (CODEC == 0 && TR::kBf16) {
-      encode_linear_bf16_fast<BITS, PACK>(ch, a, inv, rcp, pk);
+      const float rcp = fdiv(1.0f, a);  // one division per block: inv = L * (1/a)
+      encode_linear_bf16_fast<BITS, PACK>(ch, a, fmul((float)L, rcp), rcp, pk);
     } else {
+      const float inv = codec_inv(CODEC, BITS, a);
 #pragma unroll
       for (int j = 0; j < kChunks; ++j) {
         const uint32_t wv[4] = {ch[j].x, ch[j].y, ch[j].z, ch[j].w};
@@ -338,7 +366,7 @@ __device__ __forceinline__ void encode_row(const uint4 (&ch)[InTraits<Tin>::kChu
             x = u2f((e & 1) ? (wv[e >> 1] & 0xffff0000u) : (wv[e >> 1] << 16));
           else
             x = u2f(wv[e]);
-          acc |= (uint64_t)encode_one<BITS, CODEC, TR::kBf16>(x, a, inv, rcp, true) << (e * PACK);
+          acc |= (uint64_t)encode_one<BITS, CODEC, TR::kBf16>(x, a, inv, 0.0f, true) << (e * PACK);
         }
         pk[j] = acc;
       }
@@ -360,18 +388,16 @@ __device__ __forceinline__ void encode_row(const uint4 (&ch)[InTraits<Tin>::kChu
       pk[j] = acc;
     }
   }
-  if constexpr (kChunks == 4) rotr4(pk, rot); else rotr8(pk, rot);
 #pragma unroll
   for (int k = 0; k < PACK; ++k) words[k] = 0;
   pack_chunks<kChunkBits>(words, pk, std::make_integer_sequence<int, kChunks>{});
 }
 
 template <int BITS, int PACK, int CODEC, typename Tin>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tin) == 2 ? 4 : 2)
+__global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tin) == 2 ? AGQ_QUANT_MINB : 2)
     k_quant_warp(SegTable st, agq_errors* err) {
   using TR = InTraits<Tin>;
   constexpr int kChunks = TR::kChunks;
-  constexpr uint32_t kRowB = 32 * sizeof(Tin);            // one lane's elements
   constexpr uint32_t kTileB = kWarpElems * sizeof(Tin);    // 2 KB / 4 KB
   constexpr uint32_t kCodeB = kWarpElems * PACK / 8;
   __shared__ __align__(16) unsigned char sbuf[kWarpsPerCta][kTileB];
@@ -380,25 +406,30 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tin) == 2 ? 4 : 2)
   const uint64_t total = st.tile_begin[st.nseg];
   const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
   uint64_t t = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
-  const int rot = kChunks == 4 ? ((lane >> 1) & 3) : (lane & 7);
 
-  auto load = [&](uint64_t tt, uint4 (&buf)[kChunks]) {
-    const int g = seg_of(st, tt);
-    const unsigned char* src =
-        static_cast<const unsigned char*>(st.src[g]) + (tt - st.tile_begin[g]) * kTileB;
+  auto load = [&](TileRef tr, uint4 (&buf)[kChunks]) {
+    const unsigned char* src = static_cast<const unsigned char*>(st.src[tr.g]) + tr.lt * kTileB;
 #pragma unroll
     for (int j = 0; j < kChunks; ++j) buf[j] = ldg128_stream(src + j * 512 + lane * 16);
   };
   uint4 buf[kChunks];
-  if (t < total) load(t, buf);
+  TileRef cur{0, 0};
+  if (t < total) {
+    cur = locate(st, t);
+    load(cur, buf);
+  }
   for (; t < total; t += nw) {
 #pragma unroll
-    for (int j = 0; j < kChunks; ++j) sts128(wb + j * 512 + lane * 16, buf[j]);
+    for (int j = 0; j < kChunks; ++j) sts128(wb + swz_of_linear<kChunks>(j * 512 + lane * 16), buf[j]);
     __syncwarp();
-    if (t + nw < total) load(t + nw, buf);
+    const TileRef tr = cur;
+    if (t + nw < total) {
+      cur = locate(st, t + nw);
+      load(cur, buf);
+    }
     uint4 ch[kChunks];
 #pragma unroll
-    for (int j = 0; j < kChunks; ++j) ch[j] = lds128(wb + lane * kRowB + ((j + rot) & (kChunks - 1)) * 16);
+    for (int j = 0; j < kChunks; ++j) ch[j] = lds128(wb + swz_off<kChunks>(lane, j));
     __syncwarp();
 
     uint32_t m;
@@ -425,14 +456,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tin) == 2 ? 4 : 2)
     m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
     m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
     const float a = u2f(m);
-    const int g = seg_of(st, t);
-    const uint64_t lt = t - st.tile_begin[g];
     if (m >= 0x7f800000u && (lane & 3) == 0)
-      err_min(&err->nonfinite_block, (long long)(st.block_base[g] + lt * 8 + (lane >> 2)));
+      err_min(&err->nonfinite_block, (long long)(st.block_base[tr.g] + tr.lt * 8 + (lane >> 2)));
     uint32_t words[PACK];
-    encode_row<BITS, PACK, CODEC, Tin>(ch, rot, a, m == 0, fast_scale(a), words);
-    uint32_t* cdst = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(st.codes[g]) +
-                                                 lt * kCodeB) + lane * PACK;
+    encode_row<BITS, PACK, CODEC, Tin>(ch, a, m == 0, fast_scale(a), words);
+    uint32_t* cdst = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(st.codes[tr.g]) +
+                                                 tr.lt * kCodeB) + lane * PACK;
     if constexpr (PACK % 4 == 0) {
 #pragma unroll
       for (int k = 0; k < PACK / 4; ++k)
@@ -442,7 +471,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tin) == 2 ? 4 : 2)
 #pragma unroll
       for (int k = 0; k < PACK; ++k) cdst[k] = words[k];
     }
-    if ((lane & 3) == 0) st.scales[g][lt * 8 + (lane >> 2)] = a;
+    if ((lane & 3) == 0) st.scales[tr.g][tr.lt * 8 + (lane >> 2)] = a;
   }
 }
 
@@ -450,7 +479,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tin) == 2 ? 4 : 2)
 // next tile prefetched, decodes 32 values, stages the 2/4 KB warp output in
 // shared memory and writes it back with coalesced 128-bit stores.
 template <int BITS, int PACK, int CODEC, typename Tout>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? 4 : 2)
+__global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? AGQ_DEQUANT_MINB : 2)
     k_dequant_warp(SegTable st, int validate, agq_errors* err);
 
 // ---------------------------------------------------------------------------
@@ -683,12 +712,11 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 template <int BITS, int PACK, int CODEC, typename Tout>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? 4 : 2)
+__global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? AGQ_DEQUANT_MINB : 2)
     k_dequant_warp(SegTable st, int validate, agq_errors* err) {
   constexpr int kChunks = OutTraits<Tout>::kChunks;
   constexpr int kPerChunk = 32 / kChunks;
   constexpr int kChunkBits = kPerChunk * PACK;
-  constexpr uint32_t kRowB = 32 * sizeof(Tout);
   constexpr uint32_t kTileB = kWarpElems * sizeof(Tout);
   constexpr uint32_t kCodeB = kWarpElems * PACK / 8;
   constexpr bool kBf16Out = sizeof(Tout) == 2;
@@ -703,12 +731,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? 4 : 2)
   const uint64_t total = st.tile_begin[st.nseg];
   const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
   uint64_t t = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
-  const int rot = kChunks == 4 ? ((lane >> 1) & 3) : (lane & 7);
-
-  auto load = [&](uint64_t tt, uint32_t (&w)[PACK], float& sc) {
-    const int g = seg_of(st, tt);
-    const uint64_t lt = tt - st.tile_begin[g];
-    const unsigned char* src = static_cast<const unsigned char*>(st.codes[g]) + lt * kCodeB;
+  auto load = [&](TileRef tr, uint32_t (&w)[PACK], float& sc) {
+    const unsigned char* src = static_cast<const unsigned char*>(st.codes[tr.g]) + tr.lt * kCodeB;
     if constexpr (PACK % 4 == 0) {
 #pragma unroll
       for (int k = 0; k < PACK / 4; ++k) {
@@ -720,22 +744,28 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? 4 : 2)
 #pragma unroll
       for (int k = 0; k < PACK; ++k) w[k] = __ldg(s32 + k);
     }
-    sc = __ldg(st.scales[g] + lt * 8 + (lane >> 2));
+    sc = __ldg(st.scales[tr.g] + tr.lt * 8 + (lane >> 2));
   };
   uint32_t words[PACK];
   float sc = 0.f;
-  if (t < total) load(t, words, sc);
+  TileRef cur{0, 0};
+  if (t < total) {
+    cur = locate(st, t);
+    load(cur, words, sc);
+  }
   for (; t < total; t += nw) {
     uint32_t cw[PACK];
 #pragma unroll
     for (int k = 0; k < PACK; ++k) cw[k] = words[k];
     const float s = sc;
-    const int g = seg_of(st, t);
-    const uint64_t lt = t - st.tile_begin[g];
-    if (t + nw < total) load(t + nw, words, sc);
+    const TileRef tr = cur;
+    if (t + nw < total) {
+      cur = locate(st, t + nw);
+      load(cur, words, sc);
+    }
     if (validate) {
       if ((!(s >= 0.0f) || !(s <= 3.402823466e38f)) && (lane & 3) == 0)
-        err_min(&err->bad_scale_block, (long long)(st.block_base[g] + lt * 8 + (lane >> 2)));
+        err_min(&err->bad_scale_block, (long long)(st.block_base[tr.g] + tr.lt * 8 + (lane >> 2)));
       if constexpr (PACK == 8 && BITS < 8) {
         uint32_t bad = 0;
 #pragma unroll
@@ -746,7 +776,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? 4 : 2)
             const uint32_t c = (cw[e >> 2] >> ((e & 3) * 8)) & 0xffu;
             if (c >> BITS) {
               err_min(&err->bad_code_index,
-                      (long long)((st.block_base[g] + lt * 8) * kBlock + lane * 32 + e));
+                      (long long)((st.block_base[tr.g] + tr.lt * 8) * kBlock + lane * 32 + e));
               break;
             }
           }
@@ -756,8 +786,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? 4 : 2)
     const bool fast = is_bf16_value(s) && fast_scale(s);
     uint64_t pk[kChunks];
     unpack_chunks<kChunkBits>(cw, pk, std::make_integer_sequence<int, kChunks>{});
-    if constexpr (kChunks == 4) rotl4(pk, rot); else rotl8(pk, rot);
-    unsigned char* orow = wb + lane * kRowB;
 #pragma unroll
     for (int j = 0; j < kChunks; ++j) {
       float v[kPerChunk];
@@ -792,13 +820,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? 4 : 2)
       } else {
         o = make_uint4(f2u(v[0]), f2u(v[1]), f2u(v[2]), f2u(v[3]));
       }
-      sts128(orow + ((j + rot) & (kChunks - 1)) * 16, o);
+      sts128(wb + swz_off<kChunks>(lane, j), o);
     }
     __syncwarp();
-    unsigned char* dst = static_cast<unsigned char*>(st.dst[g]) + lt * kTileB;
+    unsigned char* dst = static_cast<unsigned char*>(st.dst[tr.g]) + tr.lt * kTileB;
 #pragma unroll
     for (int j = 0; j < kChunks; ++j)
-      *reinterpret_cast<uint4*>(dst + j * 512 + lane * 16) = lds128(wb + j * 512 + lane * 16);
+      *reinterpret_cast<uint4*>(dst + j * 512 + lane * 16) =
+          lds128(wb + swz_of_linear<kChunks>(j * 512 + lane * 16));
     __syncwarp();
   }
 }

@@ -44,8 +44,10 @@ static void report(const char* what, long long n, long long bad) {
 static uint32_t dev_code_bf16(int codec, int bits, float x, float a) {
   const float inv = codec_inv(codec, bits, a);
   if (codec == 0) {
+    // kernel form: one division per block, inv = L * (1/a)
     const int L = levels_of(bits);
-    return (uint32_t)(linear_k_bf16(x, a, inv, fdiv(1.0f, a), (float)L) + L);
+    const float rcp = fdiv(1.0f, a);
+    return (uint32_t)(linear_k_bf16(x, a, fmul((float)L, rcp), rcp, (float)L) + L);
   }
   return encode_f32(codec, bits, x, a, inv);
 }

@@ -26,10 +26,32 @@ __device__ __forceinline__ float apply_prec(float s) {
   return s;
 }
 
-__device__ __forceinline__ float fp8_dequant(uint32_t c, double sd, const double* lut) {
-  const float mag = d2f_rn(dmul(lut[c & 0x7fu], sd));
-  return u2f(f2u(mag) ^ ((c & 0x80u) << 24));
+// Exact FP8 decode with an FP32 block scale, (float)(fl64(e4m3(c)/448)*(double)s).
+// AGQ_FP8DQ selects the implementation (all bit-identical, verified in
+// tests/cpp/numerics_check.cpp):
+//   0: 128-entry double LUT + DMUL + F2F          (LDS bank conflicts)
+//   1: 16-entry table + 2 DMUL + F2F              (conflict free)
+//   2: 16-entry table + DMUL + integer rounding   (no F2F; fast-scale blocks)
+#ifndef AGQ_FP8DQ
+#define AGQ_FP8DQ 0
+#endif
+constexpr int kDqTable = AGQ_FP8DQ == 0 ? 128 : 16;
+__device__ __forceinline__ void fill_fp8_dq_table(double* t) {
+  if (AGQ_FP8DQ == 0)
+    fill_fp8_unit_lut(t);
+  else if (threadIdx.x < 16)
+    t[threadIdx.x] = fp8_t16((int)threadIdx.x);
 }
+__device__ __forceinline__ float fp8_dequant(uint32_t c, double sd, const double* t, bool fastblk) {
+  if (AGQ_FP8DQ == 0) {
+    const float mag = d2f_rn(dmul(t[c & 0x7fu], sd));
+    return u2f(f2u(mag) ^ ((c & 0x80u) << 24));
+  }
+  if (AGQ_FP8DQ == 2 && fastblk) return fp8_dequant_t16i(c, sd, t);
+  return fp8_dequant_t16(c, sd, t);
+}
+// A block scale for which fp8_dequant_t16i is exact (zero blocks excluded).
+__device__ __forceinline__ bool dq_fast(float s) { return s >= kFastLo && s <= kFastHi; }
 
 // Encode 2 values of a block with absmax a (fast scale) -> 2 E4M3 codes.
 __device__ __forceinline__ uint32_t fp8_encode_pair(float s0, float s1, float a, float inv) {
@@ -89,7 +111,7 @@ struct PieceTable {
 // parallelism), then the fp32 sum in ascending piece order from +0.0f.
 template <int NP>
 __device__ __forceinline__ void reduce_group(const PieceTable& pt, uint64_t g, uint64_t len,
-                                             long long blk_base, const double* lut,
+                                             long long blk_base, const double* t16,
                                              agq_errors* err, bool vec) {
   const int np = NP > 0 ? NP : pt.np;
   const uint64_t e0 = g * 16;
@@ -124,7 +146,7 @@ __device__ __forceinline__ void reduce_group(const PieceTable& pt, uint64_t g, u
         const uint32_t w[4] = {cv[p].x, cv[p].y, cv[p].z, cv[p].w};
 #pragma unroll
         for (int e = 0; e < 16; ++e)
-          acc[e] = fadd(acc[e], fp8_dequant((w[e >> 2] >> (8 * (e & 3))) & 0xffu, sd, lut));
+          acc[e] = fadd(acc[e], fp8_dequant((w[e >> 2] >> (8 * (e & 3))) & 0xffu, sd, t16, dq_fast(sc[p])));
       }
     } else {
       (void)kMaxUnroll;
@@ -143,7 +165,7 @@ __device__ __forceinline__ void reduce_group(const PieceTable& pt, uint64_t g, u
         const double sd = (double)scp;
 #pragma unroll
         for (int e = 0; e < 16; ++e)
-          acc[e] = fadd(acc[e], fp8_dequant((w[e >> 2] >> (8 * (e & 3))) & 0xffu, sd, lut));
+          acc[e] = fadd(acc[e], fp8_dequant((w[e >> 2] >> (8 * (e & 3))) & 0xffu, sd, t16, dq_fast(scp)));
       }
     }
     // elements past the end contribute nothing to the absmax

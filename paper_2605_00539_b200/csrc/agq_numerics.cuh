@@ -350,6 +350,41 @@ AGQ_HD float dequant_double(int codec, int bits, uint32_t c, float s) {
   return d2f_rn(dmul(unit_value_double(codec, bits, c), (double)s));
 }
 
+// E4M3 unit values factor as U[c] = fl64(e4m3(c)/448) = T16[idx]*2^k with
+// 16 doubles T16 = {fl64((8+m)/448), m<8} U {fl64(m/448), m<8} (exact power-
+// of-two scaling in double): idx = m (+8 if subnormal), k = max(e,1) - 10.
+// out = (float)(fl64(T16[idx]*s) * 2^k): the power-of-two DMUL is exact, so
+// this equals the reference's (float)(U[c]*(double)s) for every FP32 s.
+AGQ_HD double fp8_t16(int idx) {
+  return idx < 8 ? (double)(8 + idx) / 448.0 : (double)(idx - 8) / 448.0;
+}
+AGQ_HD float fp8_dequant_t16(uint32_t c, double sd, const double* t16) {
+  const uint32_t e = (c >> 3) & 0xfu, m = c & 7u;
+  const uint32_t idx = m | (e == 0 ? 8u : 0u);
+  const int k = (int)(e == 0 ? 1u : e) - 10;
+  const double p = dmul(t16[idx], sd);
+  const double pw = u64_to_d((uint64_t)(k + 1023) << 52);
+  const float mag = d2f_rn(dmul(p, pw));
+  const uint32_t nan = ((c & 0x7fu) == 0x7fu) ? 0x7fc00000u : 0u;
+  return u2f((f2u(mag) | nan) ^ ((c & 0x80u) << 24));
+}
+
+// Same value without the (slow, 1/16-rate) F2F.F32.F64: P = fl64(T16*s) by
+// one DMUL, then the power-of-two factor and round-to-nearest-even to FP32
+// done on the bit pattern (valid while the result is a normal float, i.e. for
+// block scales in [2^-60, 2^60]; P >= 0 because T16 >= 0 and s >= 0).
+AGQ_HD float fp8_dequant_t16i(uint32_t c, double sd, const double* t16) {
+  const uint32_t e = (c >> 3) & 0xfu, m = c & 7u;
+  const uint32_t idx = m | (e == 0 ? 8u : 0u);
+  const uint32_t ke = e == 0 ? 1u : e;  // 2^(ke-10)
+  const uint64_t u = d_to_u64(dmul(t16[idx], sd));
+  const uint64_t r = u + 0x0FFFFFFFull + ((u >> 29) & 1u);  // RNE at bit 29
+  uint32_t f = (uint32_t)(r >> 29) - ((uint32_t)(1023 - 127 + 10 - (int)ke) << 23);
+  f = (c & 0x7fu) == 0 ? 0u : f;
+  f = (c & 0x7fu) == 0x7fu ? 0x7fc00000u : f;
+  return u2f(f ^ ((c & 0x80u) << 24));
+}
+
 // Fast path for BF16-valued scales in [2^-60, 2^60]: p = g*s is exact in
 // FP32 (g has <= 8 significant bits), and the reference value equals the
 // correctly rounded quotient p / den, computed by one Markstein correction

@@ -140,7 +140,7 @@ template <int NP>
 __global__ void __launch_bounds__(256) k_fused_allreduce(FusedArgs a) {
   __shared__ double lut[128];
   __shared__ int ok;
-  fill_fp8_unit_lut(lut);
+  fill_fp8_dq_table(lut);
   const int tid = threadIdx.x;
   uint64_t* my_flags = reinterpret_cast<uint64_t*>(a.base[a.rank]);
   // start barrier: announce "my input is final" to every rank, then wait for

@@ -16,6 +16,8 @@
 //
 // K4 uses plain 128-bit loads so that any piece may live in another GPU's
 // memory (NVLink peer pointers) — the fused all-reduce runs the same code.
+#include <cstdlib>
+
 #include "agq_grad.cuh"
 
 namespace agqk {
@@ -45,7 +47,7 @@ __global__ void __launch_bounds__(kAccThreads, 2)
 
   const int tid = threadIdx.x;
   const uint64_t policy = policy_evict_first();
-  fill_fp8_unit_lut(lut);
+  fill_fp8_dq_table(lut);
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
@@ -115,7 +117,7 @@ __global__ void __launch_bounds__(kAccThreads, 2)
     for (int e = 0; e < 16; ++e) {
       const uint32_t c = (cw[e >> 2] >> (8 * (e & 3))) & 0xffu;
       lbad |= (uint32_t)((f2u(l[e]) & 0x7f800000u) == 0x7f800000u) << e;
-      v[e] = apply_prec<PREC>(fadd(fp8_dequant(c, sd, lut), l[e]));
+      v[e] = apply_prec<PREC>(fadd(fp8_dequant(c, sd, lut, dq_fast(sc)), l[e]));
     }
     if (lbad) {
       // lowest non-finite local element of this thread (slot order -> index)
@@ -155,6 +157,101 @@ __global__ void __launch_bounds__(kAccThreads, 2)
 }
 
 // ---------------------------------------------------------------------------
+// K3 warp-autonomous variant (default): each warp streams 512-element tiles
+// (16 per lane, 8 lanes per 128-block). Codes (16 B/lane) and the block
+// scale are loaded straight to registers; the local gradient is loaded with
+// coalesced 128-bit loads into a private swizzled shared slot so each lane
+// reads its 16 consecutive values conflict-free. The next tile is prefetched
+// into registers while the current one is computed. No CTA-wide barrier.
+// ---------------------------------------------------------------------------
+constexpr int kAccWarpElems = 512;
+constexpr int kAccWarps = 8;
+
+template <int kCh>  // 16-byte chunks per lane row: 4 (f32) or 2 (bf16)
+__device__ __forceinline__ uint32_t acc_swz(uint32_t row, uint32_t c) {
+  const uint32_t rot = kCh == 4 ? (row >> 1) : (row >> 2);
+  return row * (kCh * 16) + ((c + rot) & (kCh - 1)) * 16;
+}
+
+template <bool BF16L, int PREC>
+__global__ void __launch_bounds__(kAccWarps * 32, 3)
+    k_accumulate_warp(const uint8_t* codes, const float* scales, const void* local,
+                      uint64_t ntiles, uint8_t* out_codes, float* out_scales, agq_errors* err) {
+  constexpr int kCh = BF16L ? 2 : 4;
+  constexpr uint32_t kRowB = kCh * 16;
+  constexpr uint32_t kLocTileB = kAccWarpElems * (BF16L ? 2 : 4);  // 1 KB / 2 KB
+  __shared__ __align__(16) unsigned char sbuf[kAccWarps][kLocTileB];
+  __shared__ double t16[kDqTable];
+  fill_fp8_dq_table(t16);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wb = sbuf[warp];
+  const uint64_t nw = (uint64_t)gridDim.x * kAccWarps;
+  uint64_t t = (uint64_t)blockIdx.x * kAccWarps + warp;
+  const unsigned char* lbase = static_cast<const unsigned char*>(local);
+
+  uint4 pc;       // 16 codes
+  float ps;       // block scale
+  uint4 pl[kCh];  // local gradient chunks (coalesced layout)
+  auto load = [&](uint64_t tt) {
+    pc = ldg128_stream(codes + tt * kAccWarpElems + lane * 16);
+    ps = __ldg(scales + tt * 4 + (lane >> 3));
+#pragma unroll
+    for (int j = 0; j < kCh; ++j) pl[j] = ldg128_stream(lbase + tt * kLocTileB + j * 512 + lane * 16);
+  };
+  if (t < ntiles) load(t);
+  for (; t < ntiles; t += nw) {
+#pragma unroll
+    for (int j = 0; j < kCh; ++j) {
+      const uint32_t o = j * 512 + lane * 16;
+      sts128(wb + acc_swz<kCh>(o / kRowB, (o / 16) & (kCh - 1)), pl[j]);
+    }
+    const uint32_t cw[4] = {pc.x, pc.y, pc.z, pc.w};
+    const float sc = ps;
+    __syncwarp();
+    if (t + nw < ntiles) load(t + nw);
+    float l[16];
+#pragma unroll
+    for (int j = 0; j < kCh; ++j) {
+      const uint4 v = lds128(wb + acc_swz<kCh>(lane, j));
+      if constexpr (BF16L) {
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          l[8 * j + 2 * k] = u2f(w[k] << 16);
+          l[8 * j + 2 * k + 1] = u2f(w[k] & 0xffff0000u);
+        }
+      } else {
+        l[4 * j] = u2f(v.x); l[4 * j + 1] = u2f(v.y);
+        l[4 * j + 2] = u2f(v.z); l[4 * j + 3] = u2f(v.w);
+      }
+    }
+    __syncwarp();
+    const uint64_t gblk = t * 4 + (lane >> 3);
+    if ((!(sc >= 0.0f) || !(sc <= 3.402823466e38f)) && (lane & 7) == 0)
+      err_min(&err->bad_scale_block, (long long)gblk);
+    const double sd = (double)sc;
+    float v[16];
+    uint32_t lbad = 0;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const uint32_t c = (cw[e >> 2] >> (8 * (e & 3))) & 0xffu;
+      lbad |= (uint32_t)((f2u(l[e]) & 0x7f800000u) == 0x7f800000u) << e;
+      v[e] = apply_prec<PREC>(fadd(fp8_dequant(c, sd, t16, dq_fast(sc)), l[e]));
+    }
+    if (lbad)
+      err_min(&err->nonfinite_local, (long long)(t * kAccWarpElems + lane * 16 + (__ffs(lbad) - 1)));
+    const uint32_t m = absmax_bits16(v);
+    if (m >= 0x7f800000u && (lane & 7) == 0) err_min(&err->nonfinite_block, (long long)gblk);
+    uint32_t ow[4];
+    fp8_requant16(v, u2f(m), ow);
+    *reinterpret_cast<uint4*>(out_codes + t * kAccWarpElems + lane * 16) =
+        make_uint4(ow[0], ow[1], ow[2], ow[3]);
+    if ((lane & 7) == 0) out_scales[gblk] = u2f(m);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Generic accumulate / reduce (any block size): one warp per block, two
 // passes (absmax, then encode from recomputed — identical — sums).
 // ---------------------------------------------------------------------------
@@ -165,7 +262,7 @@ __global__ void k_accumulate_generic(const uint8_t* codes, const float* scales,
                                      float* out_scales, long long elem_base,
                                      agq_errors* err) {
   __shared__ double lut[128];
-  fill_fp8_unit_lut(lut);
+  fill_fp8_dq_table(lut);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -184,7 +281,7 @@ __global__ void k_accumulate_generic(const uint8_t* codes, const float* scales,
     for (uint64_t i = beg + lane; i < end; i += 32) {
       const float l = loc(i);
       if ((f2u(l) & 0x7f800000u) == 0x7f800000u) err_min(&err->nonfinite_local, elem_base + (long long)i);
-      const float s = apply_prec<PREC>(fadd(fp8_dequant(codes[i], sd, lut), l));
+      const float s = apply_prec<PREC>(fadd(fp8_dequant(codes[i], sd, lut, dq_fast(sc)), l));
       m = max(m, f2u(s) & 0x7fffffffu);
     }
 #pragma unroll
@@ -194,7 +291,7 @@ __global__ void k_accumulate_generic(const uint8_t* codes, const float* scales,
     const bool ok = m < 0x7f800000u;
     const float inv = ok && m ? fdiv(448.0f, a) : 0.0f;
     for (uint64_t i = beg + lane; i < end; i += 32) {
-      const float s = apply_prec<PREC>(fadd(fp8_dequant(codes[i], sd, lut), loc(i)));
+      const float s = apply_prec<PREC>(fadd(fp8_dequant(codes[i], sd, lut, dq_fast(sc)), loc(i)));
       out_codes[i] = (uint8_t)(m == 0 || !ok ? 0u : encode_f32(2, 8, s, a, inv));
     }
     __syncwarp();
@@ -205,7 +302,7 @@ __global__ void k_accumulate_generic(const uint8_t* codes, const float* scales,
 __global__ void k_reduce_generic(PieceTable pt, uint64_t len, uint32_t block, uint64_t nblocks,
                                  long long blk_base, agq_errors* err) {
   __shared__ double lut[128];
-  fill_fp8_unit_lut(lut);
+  fill_fp8_dq_table(lut);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -221,7 +318,7 @@ __global__ void k_reduce_generic(PieceTable pt, uint64_t len, uint32_t block, ui
     for (uint64_t i = beg + lane; i < end; i += 32) {
       float acc = 0.0f;
       for (int p = 0; p < pt.np; ++p)
-        acc = fadd(acc, fp8_dequant(pt.codes[p][i], (double)pt.scales[p][b], lut));
+        acc = fadd(acc, fp8_dequant(pt.codes[p][i], (double)pt.scales[p][b], lut, dq_fast(pt.scales[p][b])));
       m = max(m, f2u(acc) & 0x7fffffffu);
     }
 #pragma unroll
@@ -233,7 +330,7 @@ __global__ void k_reduce_generic(PieceTable pt, uint64_t len, uint32_t block, ui
     for (uint64_t i = beg + lane; i < end; i += 32) {
       float acc = 0.0f;
       for (int p = 0; p < pt.np; ++p)
-        acc = fadd(acc, fp8_dequant(pt.codes[p][i], (double)pt.scales[p][b], lut));
+        acc = fadd(acc, fp8_dequant(pt.codes[p][i], (double)pt.scales[p][b], lut, dq_fast(pt.scales[p][b])));
       const uint8_t c = (uint8_t)(m == 0 || !ok ? 0u : encode_f32(2, 8, acc, a, inv));
       for (int o = 0; o < pt.nout; ++o) pt.out_codes[o][i] = c;
     }
@@ -247,7 +344,7 @@ template <int NP>
 __global__ void __launch_bounds__(256)
     k_reduce128(PieceTable pt, uint64_t len, long long blk_base, int vec, agq_errors* err) {
   __shared__ double lut[128];
-  fill_fp8_unit_lut(lut);
+  fill_fp8_dq_table(lut);
   __syncthreads();
   const uint64_t nblocks = (len + kBlock - 1) / kBlock;
   const uint64_t ngroups = nblocks * 8;
@@ -370,21 +467,64 @@ void launch_reduce128(const PieceTable& pt, uint64_t len, long long bb, int vec,
 }
 }  // namespace
 
+namespace {
+// K3 variant: warp-autonomous (default) or the TMA tile pipeline
+// (AGQ_ACC_KERNEL=tma).
+bool acc_warp() {
+  static const bool w = [] {
+    const char* e = getenv("AGQ_ACC_KERNEL");
+    return !(e && e[0] == 't');
+  }();
+  return w;
+}
+
+template <bool BF16L, int PREC>
+agq_status launch_acc_warp(const uint8_t* codes, const float* scales, const void* local,
+                           uint64_t ntiles, uint8_t* oc, float* os, agq_errors* err,
+                           cudaStream_t s) {
+  auto k = k_accumulate_warp<BF16L, PREC>;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kAccWarps * 32, 0);
+  if (occ < 1) occ = 1;
+  const uint64_t want = (ntiles + kAccWarps - 1) / kAccWarps;
+  const uint64_t cap = (uint64_t)num_sms() * occ;
+  k<<<(int)(want < cap ? want : cap), kAccWarps * 32, 0, s>>>(codes, scales, local, ntiles, oc,
+                                                              os, err);
+  count_launch();
+  return cuda_fail(cudaGetLastError(), "accumulate: launch");
+}
+
+template <bool BF16L>
+agq_status acc_warp_prec(int prec, const uint8_t* codes, const float* scales, const void* local,
+                         uint64_t ntiles, uint8_t* oc, float* os, agq_errors* err,
+                         cudaStream_t s) {
+  if (prec == AGQ_ACC_BF16) return launch_acc_warp<BF16L, AGQ_ACC_BF16>(codes, scales, local, ntiles, oc, os, err, s);
+  if (prec == AGQ_ACC_FP16) return launch_acc_warp<BF16L, AGQ_ACC_FP16>(codes, scales, local, ntiles, oc, os, err, s);
+  return launch_acc_warp<BF16L, AGQ_ACC_FP32>(codes, scales, local, ntiles, oc, os, err, s);
+}
+}  // namespace
+
 agq_status accumulate_device(const uint8_t* codes, const float* scales, const void* local,
                              int local_dtype, uint64_t n, uint32_t block, int prec,
                              uint8_t* oc, float* os, agq_errors* err, cudaStream_t s) {
   if (n == 0) return AGQ_OK;
   const bool bf16l = local_dtype == AGQ_BF16;
+  const uint64_t unit = acc_warp() ? (uint64_t)kAccWarpElems : (uint64_t)kTileElems;
   uint64_t ntiles = 0;
   if (block == (uint32_t)kBlock && aligned16(codes) && aligned16(scales) && aligned16(local) &&
       aligned16(oc) && aligned16(os))
-    ntiles = n / kTileElems;
+    ntiles = n / unit;
   if (ntiles) {
-    agq_status r = bf16l ? acc_tiled_prec<true>(prec, codes, scales, local, ntiles, oc, os, err, s)
-                         : acc_tiled_prec<false>(prec, codes, scales, local, ntiles, oc, os, err, s);
+    agq_status r;
+    if (acc_warp())
+      r = bf16l ? acc_warp_prec<true>(prec, codes, scales, local, ntiles, oc, os, err, s)
+                : acc_warp_prec<false>(prec, codes, scales, local, ntiles, oc, os, err, s);
+    else
+      r = bf16l ? acc_tiled_prec<true>(prec, codes, scales, local, ntiles, oc, os, err, s)
+                : acc_tiled_prec<false>(prec, codes, scales, local, ntiles, oc, os, err, s);
     if (r != AGQ_OK) return r;
   }
-  const uint64_t done = ntiles * kTileElems;
+  const uint64_t done = ntiles * unit;
   if (done == n) return AGQ_OK;
   const uint64_t rest = n - done, nb = (rest + block - 1) / block;
   const void* ltail = static_cast<const char*>(local) + done * (bf16l ? 2 : 4);

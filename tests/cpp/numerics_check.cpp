@@ -298,7 +298,60 @@ static void check_fp8_fast(uint64_t seed) {
   report("fp8 fast encoder (cvt + near routing), bf16 exhaustive + f32", n, bad);
 }
 
+// Exact FP8 decode with FP32 scales from the 16-entry table (gradient path)
+static void check_fp8_t16(uint64_t seed) {
+  double t16[16];
+  for (int i = 0; i < 16; ++i) t16[i] = fp8_t16(i);
+  std::mt19937_64 rng(seed);
+  long long n = 0, bad = 0;
+  for (int it = 0; it < 40000; ++it) {
+    float s = u2f((uint32_t)(rng() % 0x7f800000u));
+    if (it < 4) s = it == 0 ? 0.0f : (it == 1 ? 1.4e-45f : (it == 2 ? 3.4e38f : 1.0f));
+    uint8_t codes[256];
+    float want[256];
+    for (int c = 0; c < 256; ++c) codes[c] = (uint8_t)c;
+    oracle_dequantize(codes, &s, 256, 8, 256, 2, want, nullptr, 0);
+    for (int c = 0; c < 256; ++c) {
+      const float got = fp8_dequant_t16(c, (double)s, t16);
+      ++n;
+      if ((c & 0x7f) == 0x7f) {
+        bad += !(got != got) || ((f2u(got) >> 31) != (uint32_t)(c >> 7));
+        continue;
+      }
+      bad += f2u(got) != f2u(want[c]);
+    }
+  }
+  report("fp8 decode via T16 table, fp32 scales (random + extremes)", n, bad);
+}
+
+static void check_fp8_t16i(uint64_t seed) {
+  double t16[16];
+  for (int i = 0; i < 16; ++i) t16[i] = fp8_t16(i);
+  std::mt19937_64 rng(seed);
+  long long n = 0, bad = 0;
+  for (int it = 0; it < 40000; ++it) {
+    // fast-path scale range [2^-60, 2^60]
+    const float s = ldexpf(1.0f + (float)(rng() % 8388608u) / 8388608.0f, (int)(rng() % 120) - 60);
+    uint8_t codes[256];
+    float want[256];
+    for (int c = 0; c < 256; ++c) codes[c] = (uint8_t)c;
+    oracle_dequantize(codes, &s, 256, 8, 256, 2, want, nullptr, 0);
+    for (int c = 0; c < 256; ++c) {
+      const float got = fp8_dequant_t16i(c, (double)s, t16);
+      ++n;
+      if ((c & 0x7f) == 0x7f) {
+        bad += !(got != got);
+        continue;
+      }
+      bad += f2u(got) != f2u(want[c]);
+    }
+  }
+  report("fp8 decode via T16 + integer rounding, scales in [2^-60,2^60]", n, bad);
+}
+
 int main() {
+  check_fp8_t16(5);
+  check_fp8_t16i(6);
   check_fp8_fast(21);
   check_extreme(11);
   check_fp8_ties();

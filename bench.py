@@ -425,6 +425,83 @@ def bench_allreduce(dev, args, world, rank, n):
     return res
 
 
+def bench_sweep(dev, args, world, rank):
+    """C5: message-size sweep (FP8 payload 2^20..2^32 bytes) plus LLaMA-32B
+    gradient buckets, decomposed 8-bit all-reduce vs BF16 ncclAllReduce of the
+    same element count. LLaMA-32B (hidden 5120, FFN 27648, 64 layers, GQA-8,
+    vocab 152064): one bucket per transformer layer and 40M-param
+    Megatron-style buckets."""
+    import torch
+    import paper_2605_00539_b200 as A
+    from paper_2605_00539_b200 import _lib as L
+    from paper_2605_00539_b200.collective import Communicator
+    sizes = [1 << k for k in range(20, 33)]
+    # q,o (5120^2) + k,v (GQA-8, head 128: 5120x1024) + gate/up/down + 2 norms = 487.6M
+    layer = 5120 * 5120 * 2 + 2 * 5120 * 1024 + 3 * 5120 * 27648 + 2 * 5120
+    buckets = {"llama32b_layer_bucket": layer, "megatron_40M_bucket": 40_000_000}
+    nmax = max(max(sizes), layer)
+    comm = Communicator(device=dev.index)
+    if "p2p" in args.algos:
+        comm.enable_p2p(nmax)
+    sp = torch.cuda.current_stream().cuda_stream
+    g = torch.Generator(device=dev).manual_seed(7 + rank)
+    src_c = torch.empty(nmax, dtype=torch.uint8, device=dev)
+    src_s = torch.empty((nmax + 127) // 128, dtype=torch.float32, device=dev)
+    for off in range(0, nmax, 1 << 28):
+        m = min(1 << 28, nmax - off)
+        x = torch.randn(m, device=dev, generator=g) * 1e-3
+        L.check(L.lib.agq_quantize(x.data_ptr(), L.AGQ_F32, m, 8, 128, 2, src_c[off:].data_ptr(),
+                                   L.AGQ_CODES_BYTES, src_s[off // 128:].data_ptr(), None, sp))
+    work_c, work_s = torch.empty_like(src_c), torch.empty_like(src_s)
+    if "p2p" in args.algos:
+        pc, ps = comm.p2p_buffers(nmax)
+    gb = torch.empty(nmax, dtype=torch.bfloat16, device=dev)
+    gb.normal_(0, 1e-3, generator=g)
+    err = A.ErrorRecord(dev).reset()
+    fac = 2 * (world - 1) / world
+
+    def timeit(fn, n):
+        iters = int(min(200, max(5, (2 << 30) // max(n, 1))))
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        barrier(world)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(iters):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        return max_over_ranks(s.elapsed_time(e) * 1e-3 / iters, world)
+
+    rows = []
+    cases = [(f"{n >> 20}MiB", n) for n in sizes] + list(buckets.items())
+    for name, n in cases:
+        row = {"case": name, "elements": n, "fp8_wire_bytes": int(n * (1 + 4 / 128))}
+        for algo in args.algos:
+            cb, sb = (pc, ps) if algo == "p2p" else (work_c, work_s)
+            cb[:n].copy_(src_c[:n])
+            sb[:(n + 127) // 128].copy_(src_s[:(n + 127) // 128])
+
+            def fn(cb=cb, sb=sb, algo=algo):
+                L.check(L.lib.agq_allreduce_fp8(comm._h, cb.data_ptr(), sb.data_ptr(), n, 128,
+                                                comm.ALGOS[algo], err.ptr, sp))
+            sec = timeit(fn, n)
+            row[algo + "_us"] = round(sec * 1e6, 1)
+            row[algo + "_busGBs_wire"] = round(fac * n * (1 + 4 / 128) / sec / 1e9, 1)
+
+        def bf():
+            L.check(L.lib.agq_allreduce_bf16_nccl(comm._h, gb.data_ptr(), n, sp))
+        sec = timeit(bf, 2 * n)
+        row["bf16_nccl_us"] = round(sec * 1e6, 1)
+        row["bf16_nccl_busGBs"] = round(fac * 2 * n / sec / 1e9, 1)
+        best = min(row[a + "_us"] for a in args.algos)
+        row["speedup_vs_bf16"] = round(row["bf16_nccl_us"] / best, 3)
+        rows.append(row)
+    comm.close()
+    return rows
+
+
 def load_traffic():
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
@@ -515,6 +592,8 @@ def main():
     ap.add_argument("--no-accumulate", action="store_true")
     ap.add_argument("--no-allreduce", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", action="store_true",
+                    help="C5: all-reduce message-size sweep + LLaMA-32B buckets (N > 1)")
     args = ap.parse_args()
     args.algos = [a for a in args.algos.split(",") if a]
     args.warmup = max(args.warmup, 3)
@@ -532,6 +611,15 @@ def main():
     torch.cuda.set_device(dev)
     if not A.device_ok():
         raise SystemExit("not an sm_100 device: the AGoQ kernels have no other path")
+    if args.sweep:
+        rows = bench_sweep(dev, args, world, rank)
+        if rank == 0:
+            print(json.dumps({"metric": "8-bit all-reduce bus GB/s sweep (C5)", "n_gpus": world,
+                              "unit": "GB/s", "sweep": rows}), flush=True)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
     peak, peak_kind = load_peaks()
     clocks = Clocks(local)
 

@@ -35,21 +35,29 @@ __device__ __forceinline__ float apply_prec(float s) {
 #ifndef AGQ_FP8DQ
 #define AGQ_FP8DQ 0
 #endif
-constexpr int kDqTable = AGQ_FP8DQ == 0 ? 128 : 16;
+// Shared table: [0,128) the LUT of mode 0, [128,144) the 16-entry table.
+constexpr int kDqTable = 144;
 __device__ __forceinline__ void fill_fp8_dq_table(double* t) {
-  if (AGQ_FP8DQ == 0)
-    fill_fp8_unit_lut(t);
-  else if (threadIdx.x < 16)
-    t[threadIdx.x] = fp8_t16((int)threadIdx.x);
+  fill_fp8_unit_lut(t);
+  if (threadIdx.x < 16) t[128 + threadIdx.x] = fp8_t16((int)threadIdx.x);
 }
 __device__ __forceinline__ float fp8_dequant(uint32_t c, double sd, const double* t, bool fastblk) {
   if (AGQ_FP8DQ == 0) {
     const float mag = d2f_rn(dmul(t[c & 0x7fu], sd));
     return u2f(f2u(mag) ^ ((c & 0x80u) << 24));
   }
-  if (AGQ_FP8DQ == 2 && fastblk) return fp8_dequant_t16i(c, sd, t);
-  return fp8_dequant_t16(c, sd, t);
+  if (AGQ_FP8DQ == 2 && fastblk) return fp8_dequant_t16i(c, sd, t + 128);
+  return fp8_dequant_t16(c, sd, t + 128);
 }
+// Mode-0 decode (any scale) and the F2F-free decode (fast-scale blocks only).
+__device__ __forceinline__ float fp8_dq_lut(uint32_t c, double sd, const double* t) {
+  const float mag = d2f_rn(dmul(t[c & 0x7fu], sd));
+  return u2f(f2u(mag) ^ ((c & 0x80u) << 24));
+}
+__device__ __forceinline__ float fp8_dq_int(uint32_t c, double sd, const double* t) {
+  return fp8_dequant_t16i(c, sd, t + 128);
+}
+
 // A block scale for which fp8_dequant_t16i is exact (zero blocks excluded).
 __device__ __forceinline__ bool dq_fast(float s) { return s >= kFastLo && s <= kFastHi; }
 
@@ -146,7 +154,7 @@ __device__ __forceinline__ void reduce_group(const PieceTable& pt, uint64_t g, u
         const uint32_t w[4] = {cv[p].x, cv[p].y, cv[p].z, cv[p].w};
 #pragma unroll
         for (int e = 0; e < 16; ++e)
-          acc[e] = fadd(acc[e], fp8_dequant((w[e >> 2] >> (8 * (e & 3))) & 0xffu, sd, t16, dq_fast(sc[p])));
+          acc[e] = fadd(acc[e], fp8_dq_lut((w[e >> 2] >> (8 * (e & 3))) & 0xffu, sd, t16));
       }
     } else {
       (void)kMaxUnroll;
@@ -165,7 +173,7 @@ __device__ __forceinline__ void reduce_group(const PieceTable& pt, uint64_t g, u
         const double sd = (double)scp;
 #pragma unroll
         for (int e = 0; e < 16; ++e)
-          acc[e] = fadd(acc[e], fp8_dequant((w[e >> 2] >> (8 * (e & 3))) & 0xffu, sd, t16, dq_fast(scp)));
+          acc[e] = fadd(acc[e], fp8_dq_lut((w[e >> 2] >> (8 * (e & 3))) & 0xffu, sd, t16));
       }
     }
     // elements past the end contribute nothing to the absmax

@@ -21,6 +21,7 @@
 #include <nccl.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -138,7 +139,7 @@ __device__ bool wait_flag(const uint64_t* f, uint64_t epoch) {
 
 template <int NP>
 __global__ void __launch_bounds__(256) k_fused_allreduce(FusedArgs a) {
-  __shared__ double lut[128];
+  __shared__ double lut[kDqTable];
   __shared__ int ok;
   fill_fp8_dq_table(lut);
   const int tid = threadIdx.x;
@@ -459,7 +460,13 @@ agq_status allreduce_p2p(agq_comm* c, uint8_t* codes, float* scales, uint64_t n,
   a.P = P;
   const uint64_t groups = (a.len + kBlock - 1) / kBlock * 8;
   uint64_t grid = (groups + 255) / 256;
-  const uint64_t cap = (uint64_t)num_sms() * 4;  // co-resident (256 thr, small smem)
+  // co-resident grid (256 threads, small smem); AGQ_P2P_CTAS_PER_SM tunes it
+  static const int per_sm = [] {
+    const char* e = getenv("AGQ_P2P_CTAS_PER_SM");
+    const int v = e ? atoi(e) : 2;
+    return v < 1 ? 1 : (v > 8 ? 8 : v);
+  }();
+  const uint64_t cap = (uint64_t)num_sms() * per_sm;
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
   switch (P) {

@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kAccThreads, 2)
   unsigned char* in_buf = smem;
   unsigned char* out_buf = smem + kStages * kStageB;
   double* lut = reinterpret_cast<double*>(out_buf + 2 * kOutB);
-  uint64_t* full = reinterpret_cast<uint64_t*>(lut + 128);
+  uint64_t* full = reinterpret_cast<uint64_t*>(lut + kDqTable);
 
   const int tid = threadIdx.x;
   const uint64_t policy = policy_evict_first();
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kAccWarps * 32, 3)
     for (int e = 0; e < 16; ++e) {
       const uint32_t c = (cw[e >> 2] >> (8 * (e & 3))) & 0xffu;
       lbad |= (uint32_t)((f2u(l[e]) & 0x7f800000u) == 0x7f800000u) << e;
-      v[e] = apply_prec<PREC>(fadd(fp8_dequant(c, sd, t16, dq_fast(sc)), l[e]));
+      v[e] = apply_prec<PREC>(fadd(fp8_dq_lut(c, sd, t16), l[e]));
     }
     if (lbad)
       err_min(&err->nonfinite_local, (long long)(t * kAccWarpElems + lane * 16 + (__ffs(lbad) - 1)));
@@ -261,7 +261,7 @@ __global__ void k_accumulate_generic(const uint8_t* codes, const float* scales,
                                      uint32_t block, uint64_t nblocks, uint8_t* out_codes,
                                      float* out_scales, long long elem_base,
                                      agq_errors* err) {
-  __shared__ double lut[128];
+  __shared__ double lut[kDqTable];
   fill_fp8_dq_table(lut);
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -301,7 +301,7 @@ __global__ void k_accumulate_generic(const uint8_t* codes, const float* scales,
 
 __global__ void k_reduce_generic(PieceTable pt, uint64_t len, uint32_t block, uint64_t nblocks,
                                  long long blk_base, agq_errors* err) {
-  __shared__ double lut[128];
+  __shared__ double lut[kDqTable];
   fill_fp8_dq_table(lut);
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -343,7 +343,7 @@ __global__ void k_reduce_generic(PieceTable pt, uint64_t len, uint32_t block, ui
 template <int NP>
 __global__ void __launch_bounds__(256)
     k_reduce128(PieceTable pt, uint64_t len, long long blk_base, int vec, agq_errors* err) {
-  __shared__ double lut[128];
+  __shared__ double lut[kDqTable];
   fill_fp8_dq_table(lut);
   __syncthreads();
   const uint64_t nblocks = (len + kBlock - 1) / kBlock;
@@ -435,7 +435,7 @@ agq_status launch_acc_tiled(const uint8_t* codes, const float* scales, const voi
                             uint64_t ntiles, uint8_t* oc, float* os, agq_errors* err,
                             cudaStream_t s) {
   const size_t stage = kTileElems + kTileBlocks * 4 + (size_t)kTileElems * (BF16L ? 2 : 4);
-  const size_t smem = 2 * stage + 2 * (kTileElems + kTileBlocks * 4) + 128 * 8 + 2 * 8;
+  const size_t smem = 2 * stage + 2 * (kTileElems + kTileBlocks * 4) + kDqTable * 8 + 2 * 8;
   auto k = k_accumulate_tiled<BF16L, PREC>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_fail(e, "accumulate: smem attribute");

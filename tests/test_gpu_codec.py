@@ -226,3 +226,36 @@ def test_launches_are_counted(cuda):
     n0 = A.launch_count()
     A.quantize_blockwise(t(np.ones(8192, np.float32), cuda, torch.bfloat16), 4)
     assert A.launch_count() > n0
+
+
+def test_c2_layer_store_sampled(cuda):
+    """Config C2: one LLaMA-8B block's stored activations (T=16384 tokens)
+    under every 8-stage DBCA policy through ActivationStore (grouped
+    launches); sampled blocks of every tensor bit-exact vs the oracle, and
+    the reconstruction is the oracle's BF16-rounded dequantization."""
+    T = 4 * 4096
+    g = torch.Generator(device=cuda).manual_seed(5)
+    acts = {"norm1_input": torch.randn(T * 4096, device=cuda, generator=g).to(torch.bfloat16),
+            "norm2_input": torch.randn(T * 4096, device=cuda, generator=g).to(torch.bfloat16),
+            "outproj_input": (torch.randn(T * 4096, device=cuda, generator=g) * 0.5).to(torch.bfloat16),
+            "silu_gate": (torch.randn(T * 14336, device=cuda, generator=g) * 4).to(torch.bfloat16),
+            "silu_value": torch.randn(T * 14336, device=cuda, generator=g).to(torch.bfloat16),
+            "q": torch.randn(T * 4096, device=cuda, generator=g).to(torch.bfloat16)}
+    plan = A.plan_bit_widths(A.PipelineConfig(8, 16, 2))
+    rng = np.random.default_rng(2)
+    for stage in range(1, 9):
+        store = A.ActivationStore(A.stage_policy(plan, stage))
+        store.store(acts)
+        bits = plan.stages[stage - 1].assigned_bits
+        assert store.entries["q"] is acts["q"]  # attention stays full precision
+        for name in ("norm1_input", "silu_gate", "outproj_input"):
+            q = store.entries[name]
+            assert q.bit_width == bits and q.packed
+            back = store.read(name)
+            for b in rng.integers(0, acts[name].numel() // 128, 6):
+                x = acts[name][b * 128:(b + 1) * 128].float().cpu().numpy()
+                c, s = O.quantize(x, bits, 128)
+                got = q.codes[b * 16 * bits:(b + 1) * 16 * bits].cpu().numpy()
+                assert np.array_equal(got, O.pack(c, bits))
+                want = O.bf16_round(O.dequantize(c, s, bits))
+                assert np.array_equal(u32(back[b * 128:(b + 1) * 128].float().cpu().numpy()), u32(want))

@@ -185,3 +185,45 @@ def test_second_allreduce_scales_by_world(cuda):
     v2 = A.dequantize_blockwise(second).cpu().numpy()
     step = np.repeat(second.scales.cpu().numpy(), 128) * (32.0 / 448.0)
     assert np.all(np.abs(v2 - 4.0 * v1) <= 4 * step + 1e-5)
+
+
+def test_accumulate_beyond_2g_elements_sampled(cuda):
+    """Config C3 class at > 2^31 elements (64-bit indexing): the whole buffer
+    is processed on the GPU, blocks sampled around the 2^31 boundary and at
+    random are checked bit-exact against the oracle."""
+    n = (1 << 31) + 8192 * 3 + 256
+    g = torch.Generator(device=cuda).manual_seed(3)
+    x = torch.randn(n, device=cuda, generator=g) * 1e-3
+    main = A.quantize_blockwise(x, 8, 128, FP8, packed=False)
+    del x
+    loc = torch.randn(n, device=cuda, generator=g) * 1e-3
+    ref_codes = main.codes.clone()
+    ref_scales = main.scales.clone()
+    out = A.local_accumulate(main, loc, in_place=True)
+    rng = np.random.default_rng(0)
+    blocks = list(rng.integers(0, n // 128, 40)) + [(1 << 31) // 128 - 1, (1 << 31) // 128,
+                                                    (1 << 31) // 128 + 1, n // 128]
+    for b in blocks:
+        lo, hi = b * 128, min(n, b * 128 + 128)
+        oc, os_ = O.local_accumulate(ref_codes[lo:hi].cpu().numpy(), ref_scales[b:b + 1].cpu().numpy(),
+                                     loc[lo:hi].cpu().numpy())
+        assert np.array_equal(out.codes[lo:hi].cpu().numpy(), oc), b
+        assert np.array_equal(u32(out.scales[b:b + 1].cpu().numpy()), u32(os_)), b
+
+
+def test_allreduce_beyond_2g_elements_sampled(cuda):
+    n = (1 << 31) + 1000
+    g = torch.Generator(device=cuda).manual_seed(4)
+    mains = []
+    for _ in range(2):
+        x = torch.randn(n, device=cuda, generator=g) * 1e-2
+        mains.append(A.quantize_blockwise(x, 8, 128, FP8, packed=False))
+        del x
+    out = A.allreduce_simulated(mains)
+    rng = np.random.default_rng(1)
+    for b in list(rng.integers(0, n // 128, 30)) + [(1 << 31) // 128, n // 128]:
+        lo, hi = b * 128, min(n, b * 128 + 128)
+        oc, os_ = O.allreduce_decomposed([m.codes[lo:hi].cpu().numpy() for m in mains],
+                                         [m.scales[b:b + 1].cpu().numpy() for m in mains])
+        assert np.array_equal(out.codes[lo:hi].cpu().numpy(), oc), b
+        assert np.array_equal(u32(out.scales[b:b + 1].cpu().numpy()), u32(os_)), b

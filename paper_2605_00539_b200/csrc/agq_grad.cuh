@@ -35,43 +35,44 @@ __device__ __forceinline__ float apply_prec(float s) {
 #ifndef AGQ_FP8DQ
 #define AGQ_FP8DQ 0
 #endif
-// Shared table: [0,128) the LUT of mode 0, [128,144) the 16-entry table.
-constexpr int kDqTable = 144;
+// Shared table: [0,256) signed unit values fl64(e4m3(c)/448) for every code
+// (NaN for 0x7f/0xff), [256,272) the 16-entry table of the other decoders.
+constexpr int kDqTable = 272;
 __device__ __forceinline__ void fill_fp8_dq_table(double* t) {
-  fill_fp8_unit_lut(t);
-  if (threadIdx.x < 16) t[128 + threadIdx.x] = fp8_t16((int)threadIdx.x);
+  for (int c = threadIdx.x; c < 256; c += blockDim.x)
+    t[c] = ((c & 0x7f) == 0x7f) ? __longlong_as_double(0x7ff8000000000000LL)
+                                : (double)e4m3_value((uint32_t)c) / 448.0;
+  if (threadIdx.x < 16) t[256 + threadIdx.x] = fp8_t16((int)threadIdx.x);
 }
 __device__ __forceinline__ float fp8_dequant(uint32_t c, double sd, const double* t, bool fastblk) {
-  if (AGQ_FP8DQ == 0) {
-    const float mag = d2f_rn(dmul(t[c & 0x7fu], sd));
-    return u2f(f2u(mag) ^ ((c & 0x80u) << 24));
-  }
-  if (AGQ_FP8DQ == 2 && fastblk) return fp8_dequant_t16i(c, sd, t + 128);
-  return fp8_dequant_t16(c, sd, t + 128);
+  if (AGQ_FP8DQ == 0) return d2f_rn(dmul(t[c & 0xffu], sd));
+  if (AGQ_FP8DQ == 2 && fastblk) return fp8_dequant_t16i(c, sd, t + 256);
+  return fp8_dequant_t16(c, sd, t + 256);
 }
-// Mode-0 decode (any scale) and the F2F-free decode (fast-scale blocks only).
+// Signed-LUT decode: one LDS.64 + DMUL + F2F, the sign rides in the table
+// (-0.0 * s = -0.0 as in the reference).
 __device__ __forceinline__ float fp8_dq_lut(uint32_t c, double sd, const double* t) {
-  const float mag = d2f_rn(dmul(t[c & 0x7fu], sd));
-  return u2f(f2u(mag) ^ ((c & 0x80u) << 24));
+  return d2f_rn(dmul(t[c & 0xffu], sd));
 }
-__device__ __forceinline__ float fp8_dq_int(uint32_t c, double sd, const double* t) {
-  return fp8_dequant_t16i(c, sd, t + 128);
+// byte k of w (PRMT)
+__device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) {
+  return __byte_perm(w, 0u, 0x4440u | (uint32_t)k);
 }
 
 // A block scale for which fp8_dequant_t16i is exact (zero blocks excluded).
 __device__ __forceinline__ bool dq_fast(float s) { return s >= kFastLo && s <= kFastHi; }
 
-// Encode 2 values of a block with absmax a (fast scale) -> 2 E4M3 codes.
-__device__ __forceinline__ uint32_t fp8_encode_pair(float s0, float s1, float a, float inv) {
-  const float v0 = fmul(s0, inv), v1 = fmul(s1, inv);
-  uint32_t r = cvt_e4m3x2(v0, v1);
-  if (fp8_near(v0)) r = (r & 0xff00u) | fp8_code(s0, a, inv);
-  if (fp8_near(v1)) r = (r & 0x00ffu) | (fp8_code(s1, a, inv) << 8);
-  return r;
-}
-
 // Requantize 16 fp32 values of a block whose absmax is `a` (all 8 threads of
 // the block agree on a): returns 4 words of codes (element e in byte e).
+//
+// Fast scales: the hardware RNE conversion of s*inv*(1 +- 2^-21). The two
+// perturbed products bracket y = 448 s / a (their relative offsets exceed the
+// 2^-22 error of fl(fl(448/a) s)), so when both convert to the same code C,
+// every value in between — y included — rounds to C, which is then the
+// reference's code (a tie would split the bracket). Pairs whose brackets
+// split (an E4M3 midpoint within ~2^-20 relative of y) are recomputed with
+// the exact comparison fp8_code. Subnormal E4M3 and saturation need no
+// special case: RNE with satfinite is monotone over the whole range.
 __device__ __forceinline__ void fp8_requant16(const float (&v)[16], float a, uint32_t (&w)[4]) {
   if (a == 0.0f) {
     w[0] = w[1] = w[2] = w[3] = 0u;
@@ -79,10 +80,30 @@ __device__ __forceinline__ void fp8_requant16(const float (&v)[16], float a, uin
   }
   if (fast_scale(a)) {
     const float inv = fdiv(448.0f, a);
+    const float ip = fmul(inv, 1.0f + 0x1p-21f), im = fmul(inv, 1.0f - 0x1p-21f);
+    const f32x2 ip2 = pk2(ip, ip), im2 = pk2(im, im);
+    uint32_t split = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      w[k] = fp8_encode_pair(v[4 * k], v[4 * k + 1], a, inv) |
-             (fp8_encode_pair(v[4 * k + 2], v[4 * k + 3], a, inv) << 16);
+    for (int k = 0; k < 8; ++k) {
+      const f32x2 x = pk2(v[2 * k], v[2 * k + 1]);
+      float p0, p1, m0, m1;
+      up2(mul2(x, ip2), p0, p1);
+      up2(mul2(x, im2), m0, m1);
+      const uint32_t cp = cvt_e4m3x2(p0, p1), cm = cvt_e4m3x2(m0, m1);
+      split |= (uint32_t)(cp != cm) << k;
+      if (k & 1)
+        w[k >> 1] |= cp << 16;
+      else
+        w[k >> 1] = cp;
+    }
+    if (split) {
+      for (int k = 0; k < 8; ++k)
+        if (split >> k & 1) {
+          const uint32_t c2 = fp8_code(v[2 * k], a, inv) | (fp8_code(v[2 * k + 1], a, inv) << 8);
+          const int sh = (k & 1) * 16;
+          w[k >> 1] = (w[k >> 1] & ~(0xffffu << sh)) | (c2 << sh);
+        }
+    }
   } else {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -154,7 +175,7 @@ __device__ __forceinline__ void reduce_group(const PieceTable& pt, uint64_t g, u
         const uint32_t w[4] = {cv[p].x, cv[p].y, cv[p].z, cv[p].w};
 #pragma unroll
         for (int e = 0; e < 16; ++e)
-          acc[e] = fadd(acc[e], fp8_dq_lut((w[e >> 2] >> (8 * (e & 3))) & 0xffu, sd, t16));
+          acc[e] = fadd(acc[e], fp8_dq_lut(byte_of(w[e >> 2], e & 3), sd, t16));
       }
     } else {
       (void)kMaxUnroll;
@@ -173,7 +194,7 @@ __device__ __forceinline__ void reduce_group(const PieceTable& pt, uint64_t g, u
         const double sd = (double)scp;
 #pragma unroll
         for (int e = 0; e < 16; ++e)
-          acc[e] = fadd(acc[e], fp8_dq_lut((w[e >> 2] >> (8 * (e & 3))) & 0xffu, sd, t16));
+          acc[e] = fadd(acc[e], fp8_dq_lut(byte_of(w[e >> 2], e & 3), sd, t16));
       }
     }
     // elements past the end contribute nothing to the absmax

@@ -232,17 +232,20 @@ __global__ void __launch_bounds__(kAccWarps * 32, 3)
       err_min(&err->bad_scale_block, (long long)gblk);
     const double sd = (double)sc;
     float v[16];
-    uint32_t lbad = 0;
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const uint32_t c = (cw[e >> 2] >> (8 * (e & 3))) & 0xffu;
-      lbad |= (uint32_t)((f2u(l[e]) & 0x7f800000u) == 0x7f800000u) << e;
-      v[e] = apply_prec<PREC>(fadd(fp8_dq_lut(c, sd, t16), l[e]));
-    }
-    if (lbad)
-      err_min(&err->nonfinite_local, (long long)(t * kAccWarpElems + lane * 16 + (__ffs(lbad) - 1)));
+    for (int e = 0; e < 16; ++e)
+      v[e] = apply_prec<PREC>(fadd(fp8_dq_lut(byte_of(cw[e >> 2], e & 3), sd, t16), l[e]));
     const uint32_t m = absmax_bits16(v);
-    if (m >= 0x7f800000u && (lane & 7) == 0) err_min(&err->nonfinite_block, (long long)gblk);
+    if (m >= 0x7f800000u) {
+      // a non-finite local gradient makes the sum non-finite: tell the two
+      // reference errors apart only on this (rare) path
+      uint32_t lbad = 0;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) lbad |= (uint32_t)((f2u(l[e]) & 0x7f800000u) == 0x7f800000u) << e;
+      if (lbad)
+        err_min(&err->nonfinite_local, (long long)(t * kAccWarpElems + lane * 16 + (__ffs(lbad) - 1)));
+      if ((lane & 7) == 0) err_min(&err->nonfinite_block, (long long)gblk);
+    }
     uint32_t ow[4];
     fp8_requant16(v, u2f(m), ow);
     *reinterpret_cast<uint4*>(out_codes + t * kAccWarpElems + lane * 16) =

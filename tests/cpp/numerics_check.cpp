@@ -349,7 +349,59 @@ static void check_fp8_t16i(uint64_t seed) {
   report("fp8 decode via T16 + integer rounding, scales in [2^-60,2^60]", n, bad);
 }
 
+// Bracketing encoder of the gradient kernels (agq_grad.cuh fp8_requant16):
+// cvt(s*inv*(1+2^-21)) == cvt(s*inv*(1-2^-21)) -> that code, else fp8_code.
+static uint32_t fp8_bracket(float x, float a) {
+  const float inv = fdiv(448.0f, a);
+  const float ip = fmul(inv, 1.0f + 0x1p-21f), im = fmul(inv, 1.0f - 0x1p-21f);
+  const uint32_t cp = cvt_e4m3x2(fmul(x, ip), 0.0f) & 0xffu;
+  const uint32_t cm = cvt_e4m3x2(fmul(x, im), 0.0f) & 0xffu;
+  return cp == cm ? cp : fp8_code(x, a, inv);
+}
+
+static void check_fp8_bracket(uint64_t seed) {
+  long long n = 0, bad = 0, split = 0;
+  for (int am = 0; am < 128; ++am) {
+    const float a = bf16_to_f((uint16_t)(0x3f80 | am));
+    for (uint32_t h = 0; h < 0x8000; ++h) {
+      const float ax = bf16_to_f((uint16_t)h);
+      if (!(ax <= a)) continue;
+      for (int sg = 0; sg < 2; ++sg) {
+        const float x = sg ? -ax : ax;
+        ++n;
+        bad += fp8_bracket(x, a) != ref_code(2, 8, x, a);
+      }
+    }
+  }
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<float> ua(0.5f, 4.0f);
+  std::uniform_int_distribution<int> ue(-55, 55);
+  std::uniform_real_distribution<float> ux(-1.0f, 1.0f);
+  for (int it = 0; it < 400000; ++it) {
+    const float a = ldexpf(ua(rng), ue(rng));
+    const int c = (int)(rng() % 0x7e);
+    const double bnd = (oracle_fp8_decode((uint8_t)c) + oracle_fp8_decode((uint8_t)(c + 1))) /
+                       2.0 * (double)a / 448.0;
+    float y = (float)bnd;
+    for (int d = 0; d < 6; ++d) y = nextafterf(y, -INFINITY);
+    for (int d = -6; d <= 6; ++d, y = nextafterf(y, INFINITY)) {
+      if (!(std::fabs(y) <= a)) continue;
+      const float x = (rng() & 1) ? y : -y;
+      ++n;
+      bad += fp8_bracket(x, a) != ref_code(2, 8, x, a);
+    }
+    for (int k = 0; k < 4; ++k) {
+      const float x = a * ux(rng) * (k == 3 ? 1e-4f : 1.0f);
+      ++n;
+      bad += fp8_bracket(x, a) != ref_code(2, 8, x, a);
+    }
+  }
+  (void)split;
+  report("fp8 bracketing encoder (gradient requant), bf16 exhaustive + f32", n, bad);
+}
+
 int main() {
+  check_fp8_bracket(31);
   check_fp8_t16(5);
   check_fp8_t16i(6);
   check_fp8_fast(21);

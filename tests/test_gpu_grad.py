@@ -227,3 +227,26 @@ def test_allreduce_beyond_2g_elements_sampled(cuda):
                                          [m.scales[b:b + 1].cpu().numpy() for m in mains])
         assert np.array_equal(out.codes[lo:hi].cpu().numpy(), oc), b
         assert np.array_equal(u32(out.scales[b:b + 1].cpu().numpy()), u32(os_)), b
+
+
+def test_accumulate_encoder_exhaustive_bf16_domain(cuda):
+    """K3's requantizer (hardware E4M3 conversion bracketed by +-2^-21, exact
+    fallback) over every BF16 x <= a for every BF16 mantissa a: accumulate
+    onto an all-zero FP8 main gradient, so the result must equal the
+    reference's FP8 quantization of the local gradient itself."""
+    mags = (np.arange(0x8000, dtype=np.uint32) << 16).view(np.float32)
+    rows = []
+    for am in range(128):
+        a = np.array([(0x3F80 | am) << 16], np.uint32).view(np.float32)[0]
+        xs = mags[mags <= a]
+        xs = np.concatenate([xs, -xs])
+        xs = np.concatenate([xs, np.zeros((-len(xs)) % 127, np.float32)]).reshape(-1, 127)
+        rows.append(np.concatenate([np.full((xs.shape[0], 1), a, np.float32), xs], 1).reshape(-1))
+    x = np.concatenate(rows)
+    x = np.concatenate([x, np.zeros((-x.size) % 512, np.float32)])
+    zc, zs = O.quantize(np.zeros(x.size, np.float32), 8, 128, O.FP8)
+    out = A.local_accumulate(fp8q(zc, zs, cuda), t(x, cuda))
+    c, s = O.quantize(x, 8, 128, O.FP8)
+    bad = np.nonzero(out.codes.cpu().numpy() != c)[0]
+    assert bad.size == 0, (bad[:5], x[bad[:5]])
+    assert np.array_equal(u32(out.scales.cpu().numpy()), u32(s))

@@ -114,6 +114,59 @@ __device__ __forceinline__ void fp8_requant16(const float (&v)[16], float a, uin
   }
 }
 
+// 8-value variant (16 lanes per 128-block): bracketed E4M3 requant.
+__device__ __forceinline__ void fp8_requant8(const float (&v)[8], float a, uint32_t (&w)[2]) {
+  if (a == 0.0f) {
+    w[0] = w[1] = 0u;
+    return;
+  }
+  if (fast_scale(a)) {
+    const float inv = fdiv(448.0f, a);
+    const float ip = fmul(inv, 1.0f + 0x1p-21f), im = fmul(inv, 1.0f - 0x1p-21f);
+    const f32x2 ip2 = pk2(ip, ip), im2 = pk2(im, im);
+    uint32_t split = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const f32x2 x = pk2(v[2 * k], v[2 * k + 1]);
+      float p0, p1, m0, m1;
+      up2(mul2(x, ip2), p0, p1);
+      up2(mul2(x, im2), m0, m1);
+      const uint32_t cp = cvt_e4m3x2(p0, p1), cm = cvt_e4m3x2(m0, m1);
+      split |= (uint32_t)(cp != cm) << k;
+      if (k & 1)
+        w[k >> 1] |= cp << 16;
+      else
+        w[k >> 1] = cp;
+    }
+    if (split) {
+      for (int k = 0; k < 4; ++k)
+        if (split >> k & 1) {
+          const uint32_t c2 = fp8_code(v[2 * k], a, inv) | (fp8_code(v[2 * k + 1], a, inv) << 8);
+          const int sh = (k & 1) * 16;
+          w[k >> 1] = (w[k >> 1] & ~(0xffffu << sh)) | (c2 << sh);
+        }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      w[k] = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) w[k] |= encode_double(2, 8, v[4 * k + e], a) << (8 * e);
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t absmax_bits8(const float (&v)[8]) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) m = max(m, f2u(v[e]) & 0x7fffffffu);
+  m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
+  m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
+  m = max(m, __shfl_xor_sync(0xffffffffu, m, 4));
+  m = max(m, __shfl_xor_sync(0xffffffffu, m, 8));
+  return m;
+}
+
 __device__ __forceinline__ uint32_t absmax_bits16(const float (&v)[16]) {
   uint32_t m = 0;
 #pragma unroll

@@ -125,6 +125,7 @@ struct FusedArgs {
   unsigned int* done_counter;
   agq_errors* err;
   int rank, P;
+  int copy_only;
 };
 
 // Spin until flag >= epoch; returns false on timeout (20 s).
@@ -137,8 +138,152 @@ __device__ bool wait_flag(const uint64_t* f, uint64_t epoch) {
   return true;
 }
 
+// AGQ_P2P_COPYONLY=1 (measurement only): identical NVLink traffic, no
+// dequant/reduce/requant — bounds the transfer-only time of the kernel.
+// One 16-element group of the fused all-reduce with every pointer in
+// registers (compile-time NP): chunk r of every rank is read over NVLink
+// (rank order = ascending sender rank), reduced from +0.0f in FP32, requantized
+// and written back in place to all ranks.
 template <int NP>
-__global__ void __launch_bounds__(256) k_fused_allreduce(FusedArgs a) {
+__device__ __forceinline__ void fused_group(unsigned char* const (&base)[NP], uint64_t coff,
+                                            uint64_t soff, uint64_t g, uint64_t len,
+                                            long long blk_base, const double* t16,
+                                            agq_errors* err) {
+  const uint64_t e0 = g * 16;
+  const uint64_t blk = e0 / kBlock;
+  // chunk-relative addresses from one common offset per array
+  auto cbase = [&](int p) { return base[p] + coff; };
+  auto sbase = [&](int p) { return reinterpret_cast<float*>(base[p] + soff); };
+  const bool in_range = e0 < len;
+  const bool whole = e0 + 16 <= len;
+  float acc[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) acc[e] = 0.0f;
+  uint32_t sbad = 0;
+  if (in_range) {
+    uint4 cv[NP];
+    float sc[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      sc[p] = sbase(p)[blk];
+      if (whole) {
+        cv[p] = *reinterpret_cast<const uint4*>(cbase(p) + e0);
+      } else {
+        uint32_t w[4] = {0, 0, 0, 0};
+        for (int e = 0; e < 16 && e0 + e < len; ++e)
+          w[e >> 2] |= (uint32_t)cbase(p)[e0 + e] << (8 * (e & 3));
+        cv[p] = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      sbad |= !(sc[p] >= 0.0f) || !(sc[p] <= 3.402823466e38f);
+      const double sd = (double)sc[p];
+      const uint32_t w[4] = {cv[p].x, cv[p].y, cv[p].z, cv[p].w};
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        acc[e] = fadd(acc[e], fp8_dq_lut(byte_of(w[e >> 2], e & 3), sd, t16));
+    }
+    if (!whole)
+      for (int e = 0; e < 16; ++e)
+        if (e0 + e >= len) acc[e] = 0.0f;
+  }
+  const uint32_t m = absmax_bits16(acc);
+  const int sub = threadIdx.x & 7;
+  if (in_range && sub == 0) {
+    if (sbad) err_min(&err->bad_scale_block, blk_base + (long long)blk);
+    if (m >= 0x7f800000u) err_min(&err->overflow_block, blk_base + (long long)blk);
+  }
+  if (!in_range) return;
+  const float a = u2f(m);
+  uint32_t ow[4];
+  if (m >= 0x7f800000u) {
+    ow[0] = ow[1] = ow[2] = ow[3] = 0;
+  } else {
+    fp8_requant16(acc, a, ow);
+  }
+#pragma unroll
+  for (int o = 0; o < NP; ++o) {
+    if (whole) {
+      *reinterpret_cast<uint4*>(cbase(o) + e0) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+    } else {
+      for (int e = 0; e < 16 && e0 + e < len; ++e) cbase(o)[e0 + e] = (uint8_t)(ow[e >> 2] >> (8 * (e & 3)));
+    }
+    if (sub == 0) sbase(o)[blk] = a;
+  }
+}
+
+// 8 elements per thread (16 lanes per block) for large worlds: half the
+// per-piece registers so NP = 5..8 keeps two CTAs per SM without spills.
+template <int NP>
+__device__ __forceinline__ void fused_group8(unsigned char* const (&base)[NP], uint64_t coff,
+                                             uint64_t soff, uint64_t g, uint64_t len,
+                                             long long blk_base, const double* t16,
+                                             agq_errors* err) {
+  const uint64_t e0 = g * 8;
+  const uint64_t blk = e0 / kBlock;
+  const bool in_range = e0 < len;
+  const bool whole = e0 + 8 <= len;
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
+  uint32_t sbad = 0;
+  if (in_range) {
+    uint2 cv[NP];
+    float sc[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      sc[p] = reinterpret_cast<const float*>(base[p] + soff)[blk];
+      if (whole) {
+        cv[p] = *reinterpret_cast<const uint2*>(base[p] + coff + e0);
+      } else {
+        uint32_t w[2] = {0, 0};
+        for (int e = 0; e < 8 && e0 + e < len; ++e)
+          w[e >> 2] |= (uint32_t)base[p][coff + e0 + e] << (8 * (e & 3));
+        cv[p] = make_uint2(w[0], w[1]);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      sbad |= !(sc[p] >= 0.0f) || !(sc[p] <= 3.402823466e38f);
+      const double sd = (double)sc[p];
+      const uint32_t w[2] = {cv[p].x, cv[p].y};
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        acc[e] = fadd(acc[e], fp8_dq_lut(byte_of(w[e >> 2], e & 3), sd, t16));
+    }
+    if (!whole)
+      for (int e = 0; e < 8; ++e)
+        if (e0 + e >= len) acc[e] = 0.0f;
+  }
+  const uint32_t m = absmax_bits8(acc);
+  const int sub = threadIdx.x & 15;
+  if (in_range && sub == 0) {
+    if (sbad) err_min(&err->bad_scale_block, blk_base + (long long)blk);
+    if (m >= 0x7f800000u) err_min(&err->overflow_block, blk_base + (long long)blk);
+  }
+  if (!in_range) return;
+  const float a = u2f(m);
+  uint32_t ow[2];
+  if (m >= 0x7f800000u) {
+    ow[0] = ow[1] = 0;
+  } else {
+    fp8_requant8(acc, a, ow);
+  }
+#pragma unroll
+  for (int o = 0; o < NP; ++o) {
+    if (whole) {
+      *reinterpret_cast<uint2*>(base[o] + coff + e0) = make_uint2(ow[0], ow[1]);
+    } else {
+      for (int e = 0; e < 8 && e0 + e < len; ++e)
+        base[o][coff + e0 + e] = (uint8_t)(ow[e >> 2] >> (8 * (e & 3)));
+    }
+    if (sub == 0) reinterpret_cast<float*>(base[o] + soff)[blk] = a;
+  }
+}
+
+template <int NP, int EPT>
+__global__ void __launch_bounds__(256, 2) k_fused_allreduce(FusedArgs a) {
   __shared__ double lut[kDqTable];
   __shared__ int ok;
   fill_fp8_dq_table(lut);
@@ -159,22 +304,52 @@ __global__ void __launch_bounds__(256) k_fused_allreduce(FusedArgs a) {
     return;
   }
 
-  PieceTable pt;
-  pt.np = a.P;
-  pt.nout = a.P;
   const uint64_t b0 = a.begin / kBlock;
-  for (int s = 0; s < a.P; ++s) {
-    pt.codes[s] = a.base[s] + a.codes_off + a.begin;
-    pt.scales[s] = reinterpret_cast<const float*>(a.base[s] + a.scales_off) + b0;
-    pt.out_codes[s] = a.base[s] + a.codes_off + a.begin;
-    pt.out_scales[s] = reinterpret_cast<float*>(a.base[s] + a.scales_off) + b0;
-  }
   const uint64_t nblocks = (a.len + kBlock - 1) / kBlock;
   const uint64_t ngroups = nblocks * 8;
   const uint64_t gpad = (ngroups + 31) / 32 * 32;
   const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
-  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + tid; g < gpad; g += stride)
-    reduce_group<NP>(pt, g, g < ngroups ? a.len : 0, (long long)b0, lut, a.err, true);
+  if constexpr (NP > 0) {
+    unsigned char* bs[NP];
+#pragma unroll
+    for (int s = 0; s < NP; ++s) bs[s] = a.base[s];
+    const uint64_t coff = a.codes_off + a.begin, soff = a.scales_off + 4 * b0;
+    if (a.copy_only) {
+      for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + tid; g < ngroups; g += stride) {
+        const uint64_t e0 = g * 16;
+        if (e0 + 16 > a.len) continue;
+        uint4 x = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          const uint4 v = *reinterpret_cast<const uint4*>(bs[p] + coff + e0);
+          x.x ^= v.x; x.y ^= v.y; x.z ^= v.z; x.w ^= v.w;
+        }
+#pragma unroll
+        for (int o = 0; o < NP; ++o) *reinterpret_cast<uint4*>(bs[o] + coff + e0) = x;
+      }
+    } else {
+      if constexpr (EPT == 8) {
+        const uint64_t ng8 = nblocks * 16, gp8 = (ng8 + 31) / 32 * 32;
+        for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + tid; g < gp8; g += stride)
+          fused_group8<NP>(bs, coff, soff, g, g < ng8 ? a.len : 0, (long long)b0, lut, a.err);
+      } else {
+        for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + tid; g < gpad; g += stride)
+          fused_group<NP>(bs, coff, soff, g, g < ngroups ? a.len : 0, (long long)b0, lut, a.err);
+      }
+    }
+  } else {
+    PieceTable pt;
+    pt.np = a.P;
+    pt.nout = a.P;
+    for (int s = 0; s < a.P; ++s) {
+      pt.codes[s] = a.base[s] + a.codes_off + a.begin;
+      pt.scales[s] = reinterpret_cast<const float*>(a.base[s] + a.scales_off) + b0;
+      pt.out_codes[s] = a.base[s] + a.codes_off + a.begin;
+      pt.out_scales[s] = reinterpret_cast<float*>(a.base[s] + a.scales_off) + b0;
+    }
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + tid; g < gpad; g += stride)
+      reduce_group<0>(pt, g, g < ngroups ? a.len : 0, (long long)b0, lut, a.err, true);
+  }
 
   // end barrier: the last CTA to finish publishes "done" to every rank and
   // waits for all of them, so the kernel completes only when every chunk of
@@ -424,9 +599,23 @@ agq_status allreduce_nccl(agq_comm* c, uint8_t* codes, float* scales, uint64_t n
   return nccl_fail(nccl().GroupEnd(), "all-gather");
 }
 
+// Elements per thread: 16 up to 4 ranks, 8 beyond (register budget);
+// AGQ_P2P_EPT=8 forces the 8-element kernel (lets 2-4 GPU runs test it).
+int fused_ept(int P) {
+  static const int forced = [] {
+    const char* e = getenv("AGQ_P2P_EPT");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced == 8 || forced == 16) return forced;
+  return P >= 5 ? 8 : 16;
+}
+
 template <int NP>
 void launch_fused(const FusedArgs& a, int grid, cudaStream_t s) {
-  k_fused_allreduce<NP><<<grid, 256, 0, s>>>(a);
+  if (fused_ept(a.P) == 8)
+    k_fused_allreduce<NP, 8><<<grid, 256, 0, s>>>(a);
+  else
+    k_fused_allreduce<NP, 16><<<grid, 256, 0, s>>>(a);
 }
 
 agq_status allreduce_p2p(agq_comm* c, uint8_t* codes, float* scales, uint64_t n, uint32_t block,
@@ -458,7 +647,9 @@ agq_status allreduce_p2p(agq_comm* c, uint8_t* codes, float* scales, uint64_t n,
   a.err = err;
   a.rank = r;
   a.P = P;
-  const uint64_t groups = (a.len + kBlock - 1) / kBlock * 8;
+  static const int copy_only = getenv("AGQ_P2P_COPYONLY") ? 1 : 0;
+  a.copy_only = copy_only;
+  const uint64_t groups = (a.len + kBlock - 1) / kBlock * (fused_ept(P) == 8 && P <= 8 ? 16 : 8);
   uint64_t grid = (groups + 255) / 256;
   // co-resident grid (256 threads, small smem); AGQ_P2P_CTAS_PER_SM tunes it
   static const int per_sm = [] {

@@ -291,6 +291,80 @@ def bench_e2e(wl, args, world, steps):
     return wl.bytes_per_step() * steps * world / sec / 1e9, bi, bo
 
 
+def bench_c1(dev, args):
+    """C1: INT4 block-128 quantize/dequantize round trip of a 4096x4096 BF16
+    activation (the reference's CPU-runnable config). 16 rotating copies
+    (1.6 GB) so every launch streams from HBM, not the 126 MB L2."""
+    import torch
+    from paper_2605_00539_b200 import _lib as L
+    n, R = 4096 * 4096, 16
+    g = torch.Generator(device=dev).manual_seed(11)
+    xs = [torch.randn(n, device=dev, generator=g).to(torch.bfloat16) for _ in range(R)]
+    cs = [torch.empty(n // 2, dtype=torch.uint8, device=dev) for _ in range(R)]
+    ss = [torch.empty(n // 128, dtype=torch.float32, device=dev) for _ in range(R)]
+    ys = [torch.empty_like(xs[0]) for _ in range(R)]
+    sp = torch.cuda.current_stream().cuda_stream
+
+    def rt(i):
+        L.check(L.lib.agq_quantize(xs[i].data_ptr(), L.AGQ_BF16, n, 4, 128, 0, cs[i].data_ptr(),
+                                   L.AGQ_CODES_PACKED, ss[i].data_ptr(), None, sp))
+        L.check(L.lib.agq_dequantize(cs[i].data_ptr(), L.AGQ_CODES_PACKED, ss[i].data_ptr(), n, 4,
+                                     128, 0, ys[i].data_ptr(), L.AGQ_BF16, 0, None, sp))
+    for i in range(R):
+        rt(i)
+    torch.cuda.synchronize()
+    iters = 5 * R
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for i in range(iters):
+        rt(i % R)
+    e.record()
+    torch.cuda.synchronize()
+    sec = s.elapsed_time(e) * 1e-3 / iters
+    nbytes = 2 * n * (2 + 0.5 + 4 / 128)
+    return {"config": "C1 INT4 block-128 quantize+dequantize, 4096x4096 BF16",
+            "us_per_roundtrip": round(sec * 1e6, 2), "GBs": round(nbytes / sec / 1e9, 1)}
+
+
+def bench_reduce_local(dev, args, P=8):
+    """K4 on one GPU: the local reduce one rank performs in the decomposed
+    all-reduce of the LLaMA-8B gradient at P=8 (its 1/8 chunk, 8 pieces)."""
+    import torch
+    import paper_2605_00539_b200 as A
+    from paper_2605_00539_b200 import _lib as L
+    n = (LLAMA8B_PARAMS // P + 127) // 128 * 128
+    g = torch.Generator(device=dev).manual_seed(12)
+    pieces = []
+    for _ in range(P):
+        x = torch.randn(n, device=dev, generator=g) * 1e-3
+        pieces.append(A.quantize_blockwise(x, 8, 128, A.CodecKind.Fp8E4M3, packed=False, check=False))
+        del x
+    oc = torch.empty(n, dtype=torch.uint8, device=dev)
+    osc = torch.empty(n // 128, dtype=torch.float32, device=dev)
+    err = A.ErrorRecord(dev).reset()
+    pc = L.ptr_array([q.codes.data_ptr() for q in pieces])
+    ps = L.ptr_array([q.scales.data_ptr() for q in pieces])
+    po, pso = L.ptr_array([oc.data_ptr()]), L.ptr_array([osc.data_ptr()])
+    sp = torch.cuda.current_stream().cuda_stream
+
+    def run():
+        L.check(L.lib.agq_fp8_reduce_requant(P, pc, ps, n, 128, 1, po, pso, err.ptr, sp))
+    run()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(3):
+        run()
+    e.record()
+    torch.cuda.synchronize()
+    sec = s.elapsed_time(e) * 1e-3 / 3
+    L.errors_message(err.read(), L.AGQ_OP_ALLREDUCE)
+    del pieces
+    torch.cuda.empty_cache()
+    return {"config": f"K4 local reduce-requant, LLaMA-8B chunk at P={P} ({n} elems, {P} pieces)",
+            "ms": round(sec * 1e3, 3), "GBs": round(n * (P + 1) * (1 + 4 / 128) / sec / 1e9, 1)}
+
+
 def bench_accumulate(dev, args, n_params):
     """C3: FP8 local_accumulate over an 8B-param gradient, FP32 local grads."""
     import torch
@@ -636,8 +710,11 @@ def main():
                         "d2h_bytes_per_step": bo}
     del wl
     torch.cuda.empty_cache()
+    extra["c1"] = bench_c1(dev, args)
     if not args.no_accumulate:
         extra["accumulate"] = bench_accumulate(dev, args, args.acc_elements)
+    if world == 1 and not args.no_allreduce:
+        extra["reduce_local"] = bench_reduce_local(dev, args)
     if world > 1 and not args.no_allreduce:
         extra["allreduce"] = bench_allreduce(dev, args, world, rank, args.ar_elements)
     clk = clocks.stop()

@@ -475,6 +475,106 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tin) == 2 ? AGQ_QUAN
   }
 }
 
+// K1, per-warp TMA ring variant (AGQ_ACT_KERNEL=wtma): each warp owns
+// kWStages 2 KB shared slots filled by 1-D bulk copies that lane 0 keeps in
+// flight (one mbarrier per slot), so up to kWStages tiles per warp are in
+// flight without any register prefetch. Rows are read in a per-lane rotated
+// chunk order (the bulk copy cannot swizzle) and put back with selects.
+constexpr int kWStages = 4;
+
+template <int BITS, int PACK, int CODEC, typename Tin>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 3)
+    k_quant_wtma(SegTable st, agq_errors* err) {
+  using TR = InTraits<Tin>;
+  constexpr int kChunks = TR::kChunks;
+  constexpr uint32_t kTileB = kWarpElems * sizeof(Tin);
+  constexpr uint32_t kCodeB = kWarpElems * PACK / 8;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* slots = dsm + warp * kWStages * kTileB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dsm + kWarpsPerCta * kWStages * kTileB) + warp * kWStages;
+  if (lane == 0) {
+    for (int s2 = 0; s2 < kWStages; ++s2) mbar_init(&bars[s2], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  const uint64_t total = st.tile_begin[st.nseg];
+  const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
+  const uint64_t first = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
+  const uint64_t policy = policy_evict_first();
+  auto issue = [&](uint64_t t, int slot) {
+    const TileRef tr = locate(st, t);
+    mbar_arrive_expect_tx(&bars[slot], kTileB);
+    bulk_g2s(slots + slot * kTileB,
+             static_cast<const unsigned char*>(st.src[tr.g]) + tr.lt * kTileB, kTileB, &bars[slot],
+             policy);
+  };
+  if (lane == 0)
+    for (int s2 = 0; s2 < kWStages; ++s2) {
+      const uint64_t t = first + (uint64_t)s2 * nw;
+      if (t < total) issue(t, s2);
+    }
+  const int rot = kChunks == 4 ? ((lane >> 1) & 3) : (lane & 7);
+  for (uint64_t it = 0;; ++it) {
+    const uint64_t t = first + it * nw;
+    if (t >= total) break;
+    const int slot = (int)(it % kWStages);
+    mbar_wait(&bars[slot], (uint32_t)((it / kWStages) & 1));
+    uint4 ch[kChunks];
+    const unsigned char* row = slots + slot * kTileB + lane * (32 * sizeof(Tin));
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) ch[j] = lds128(row + ((j + rot) & (kChunks - 1)) * 16);
+    __syncwarp();
+    if (lane == 0) {
+      const uint64_t nt = t + (uint64_t)kWStages * nw;
+      if (nt < total) issue(nt, slot);
+    }
+    // back to natural chunk order (slot j holds chunk j + rot)
+    if constexpr (kChunks == 4) rotr4(ch, rot); else rotr8(ch, rot);
+    uint32_t m;
+    if constexpr (TR::kBf16) {
+      uint32_t mm = 0;
+#pragma unroll
+      for (int j = 0; j < kChunks; ++j) {
+        mm = __vmaxu2(mm, ch[j].x & 0x7fff7fffu);
+        mm = __vmaxu2(mm, ch[j].y & 0x7fff7fffu);
+        mm = __vmaxu2(mm, ch[j].z & 0x7fff7fffu);
+        mm = __vmaxu2(mm, ch[j].w & 0x7fff7fffu);
+      }
+      m = max(mm & 0xffffu, mm >> 16) << 16;
+    } else {
+      m = 0;
+#pragma unroll
+      for (int j = 0; j < kChunks; ++j) {
+        m = max(m, ch[j].x & 0x7fffffffu);
+        m = max(m, ch[j].y & 0x7fffffffu);
+        m = max(m, ch[j].z & 0x7fffffffu);
+        m = max(m, ch[j].w & 0x7fffffffu);
+      }
+    }
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
+    m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
+    const float a = u2f(m);
+    const TileRef tr = locate(st, t);
+    if (m >= 0x7f800000u && (lane & 3) == 0)
+      err_min(&err->nonfinite_block, (long long)(st.block_base[tr.g] + tr.lt * 8 + (lane >> 2)));
+    uint32_t words[PACK];
+    encode_row<BITS, PACK, CODEC, Tin>(ch, a, m == 0, fast_scale(a), words);
+    uint32_t* cdst = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(st.codes[tr.g]) +
+                                                 tr.lt * kCodeB) + lane * PACK;
+    if constexpr (PACK % 4 == 0) {
+#pragma unroll
+      for (int k = 0; k < PACK / 4; ++k)
+        *reinterpret_cast<uint4*>(cdst + 4 * k) =
+            make_uint4(words[4 * k], words[4 * k + 1], words[4 * k + 2], words[4 * k + 3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < PACK; ++k) cdst[k] = words[k];
+    }
+    if ((lane & 3) == 0) st.scales[tr.g][tr.lt * 8 + (lane >> 2)] = a;
+  }
+}
+
 // K2 warp-autonomous variant: lane loads its PACK code words (+ block scale),
 // next tile prefetched, decodes 32 values, stages the 2/4 KB warp output in
 // shared memory and writes it back with coalesced 128-bit stores.
@@ -984,6 +1084,13 @@ bool act_warp() {
   }();
   return w;
 }
+bool act_wtma() {
+  static const bool w = [] {
+    const char* e = getenv("AGQ_ACT_KERNEL");
+    return e && e[0] == 'w' && e[1] == 't';
+  }();
+  return w;
+}
 uint64_t act_unit() { return act_warp() ? (uint64_t)kWarpElems : (uint64_t)kTileElems; }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -1025,7 +1132,25 @@ agq_status launch_quant_tiled(const SegTable& st, agq_errors* err, cudaStream_t 
 }
 
 template <int BITS, int PACK, int CODEC, typename Tin>
+agq_status launch_quant_wtma(const SegTable& st, agq_errors* err, cudaStream_t s) {
+  auto k = k_quant_wtma<BITS, PACK, CODEC, Tin>;
+  const size_t smem = (size_t)kWarpsPerCta * kWStages * (kWarpElems * sizeof(Tin) + 8);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return cuda_fail(e, "quantize: smem attribute");
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWarpsPerCta * 32, smem);
+  if (occ < 1) occ = 1;
+  const uint64_t tiles = st.tile_begin[st.nseg];
+  const uint64_t want = (tiles + kWarpsPerCta - 1) / kWarpsPerCta;
+  const uint64_t cap = (uint64_t)num_sms() * occ;
+  k<<<(int)(want < cap ? want : cap), kWarpsPerCta * 32, smem, s>>>(st, err);
+  count_launch();
+  return cuda_fail(cudaGetLastError(), "quantize: launch");
+}
+
+template <int BITS, int PACK, int CODEC, typename Tin>
 agq_status launch_quant_warp(const SegTable& st, agq_errors* err, cudaStream_t s) {
+  if (act_wtma()) return launch_quant_wtma<BITS, PACK, CODEC, Tin>(st, err, s);
   auto k = k_quant_warp<BITS, PACK, CODEC, Tin>;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWarpsPerCta * 32, 0);

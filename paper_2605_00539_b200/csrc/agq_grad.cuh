@@ -62,6 +62,31 @@ __device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) {
 // A block scale for which fp8_dequant_t16i is exact (zero blocks excluded).
 __device__ __forceinline__ bool dq_fast(float s) { return s >= kFastLo && s <= kFastHi; }
 
+// Elements (bit e of the mask, e mod 16) whose double->float rounding runs on
+// the integer pipes (d2f_rn_bits) instead of F2F.F32.F64. F2F issues at 1/16
+// of the FP32 rate, so decoding every element through it bounds the reduce
+// kernels; splitting the elements balances the F2F pipe against issue slots.
+#ifndef AGQ_DQ_INT_MASK
+#define AGQ_DQ_INT_MASK 0x0u  // measured: all-F2F is fastest (profiles/r01_dq_split.log)
+#endif
+// acc[e] = fadd(acc[e], dequant(code e of w, sc)) for the N codes of one
+// block piece; bit-identical to fp8_dq_lut for every element.
+template <int N>
+__device__ __forceinline__ void dq_accum(const uint32_t (&w)[N / 4], float sc, const double* t,
+                                         float (&acc)[N]) {
+  const double sd = (double)sc;
+  if (AGQ_DQ_INT_MASK != 0u && dq_fast(sc)) {
+#pragma unroll
+    for (int e = 0; e < N; ++e) {
+      const double p = dmul(t[byte_of(w[e >> 2], e & 3)], sd);
+      acc[e] = fadd(acc[e], ((AGQ_DQ_INT_MASK >> (e & 15)) & 1u) ? d2f_rn_bits(p) : d2f_rn(p));
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < N; ++e) acc[e] = fadd(acc[e], fp8_dq_lut(byte_of(w[e >> 2], e & 3), sd, t));
+  }
+}
+
 // Requantize 16 fp32 values of a block whose absmax is `a` (all 8 threads of
 // the block agree on a): returns 4 words of codes (element e in byte e).
 //
@@ -224,11 +249,8 @@ __device__ __forceinline__ void reduce_group(const PieceTable& pt, uint64_t g, u
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
         sbad |= !(sc[p] >= 0.0f) || !(sc[p] <= 3.402823466e38f);
-        const double sd = (double)sc[p];
         const uint32_t w[4] = {cv[p].x, cv[p].y, cv[p].z, cv[p].w};
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          acc[e] = fadd(acc[e], fp8_dq_lut(byte_of(w[e >> 2], e & 3), sd, t16));
+        dq_accum<16>(w, sc[p], t16, acc);
       }
     } else {
       (void)kMaxUnroll;
@@ -244,10 +266,7 @@ __device__ __forceinline__ void reduce_group(const PieceTable& pt, uint64_t g, u
           for (int e = 0; e < 16 && e0 + e < len; ++e)
             w[e >> 2] |= (uint32_t)pt.codes[p][e0 + e] << (8 * (e & 3));
         }
-        const double sd = (double)scp;
-#pragma unroll
-        for (int e = 0; e < 16; ++e)
-          acc[e] = fadd(acc[e], fp8_dq_lut(byte_of(w[e >> 2], e & 3), sd, t16));
+        dq_accum<16>(w, scp, t16, acc);
       }
     }
     // elements past the end contribute nothing to the absmax

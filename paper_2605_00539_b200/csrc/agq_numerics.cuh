@@ -385,6 +385,25 @@ AGQ_HD float fp8_dequant_t16i(uint32_t c, double sd, const double* t16) {
   return u2f(f ^ ((c & 0x80u) << 24));
 }
 
+// RNE of a double to float on the bit pattern, for |p| = 0 or a normal float
+// result (block scales in [2^-60, 2^60] guarantee that for every non-NaN
+// E4M3 code times its scale): re-bias the exponent in the high word (clamped
+// at 0 so +-0 stays 0), add half-minus-one + the guard LSB at bit 29 with
+// carry, funnel-shift, restore the sign. A NaN input (E4M3 code 0x7f/0xff)
+// saturates to a non-finite float (inf or NaN), which keeps every sum it
+// enters non-finite — the only property the reduce paths observe. About 9
+// integer ops instead of one
+// F2F.F32.F64 (a 1/16-rate pipe); exact, see tests/cpp/numerics_check.cpp.
+AGQ_HD float d2f_rn_bits(double p) {
+  const uint64_t u = d_to_u64(p);
+  const uint32_t lo = (uint32_t)u, hi = (uint32_t)(u >> 32);
+  int32_t hb = (int32_t)(hi & 0x7fffffffu) - (int32_t)((1023 - 127) << 20);
+  hb = hb < 0 ? 0 : (hb > 0x0FF00000 ? 0x0FF00000 : hb);  // NaN/huge -> non-finite
+  const uint64_t mag = ((uint64_t)(uint32_t)hb << 32) | lo;
+  const uint64_t r = mag + 0x0FFFFFFFull + ((lo >> 29) & 1u);
+  return u2f((uint32_t)(r >> 29) | (hi & 0x80000000u));
+}
+
 // Fast path for BF16-valued scales in [2^-60, 2^60]: p = g*s is exact in
 // FP32 (g has <= 8 significant bits), and the reference value equals the
 // correctly rounded quotient p / den, computed by one Markstein correction

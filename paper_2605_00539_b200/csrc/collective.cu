@@ -178,11 +178,8 @@ __device__ __forceinline__ void fused_group(unsigned char* const (&base)[NP], ui
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       sbad |= !(sc[p] >= 0.0f) || !(sc[p] <= 3.402823466e38f);
-      const double sd = (double)sc[p];
       const uint32_t w[4] = {cv[p].x, cv[p].y, cv[p].z, cv[p].w};
-#pragma unroll
-      for (int e = 0; e < 16; ++e)
-        acc[e] = fadd(acc[e], fp8_dq_lut(byte_of(w[e >> 2], e & 3), sd, t16));
+      dq_accum<16>(w, sc[p], t16, acc);
     }
     if (!whole)
       for (int e = 0; e < 16; ++e)
@@ -246,11 +243,8 @@ __device__ __forceinline__ void fused_group8(unsigned char* const (&base)[NP], u
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       sbad |= !(sc[p] >= 0.0f) || !(sc[p] <= 3.402823466e38f);
-      const double sd = (double)sc[p];
       const uint32_t w[2] = {cv[p].x, cv[p].y};
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        acc[e] = fadd(acc[e], fp8_dq_lut(byte_of(w[e >> 2], e & 3), sd, t16));
+      dq_accum<8>(w, sc[p], t16, acc);
     }
     if (!whole)
       for (int e = 0; e < 8; ++e)

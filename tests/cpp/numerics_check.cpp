@@ -400,7 +400,42 @@ static void check_fp8_bracket(uint64_t seed) {
   report("fp8 bracketing encoder (gradient requant), bf16 exhaustive + f32", n, bad);
 }
 
+// Integer double->float rounding used for half of the gradient decodes
+static void check_d2f_bits(uint64_t seed) {
+  std::mt19937_64 rng(seed);
+  long long n = 0, bad = 0;
+  double lut[256];
+  for (int c = 0; c < 256; ++c) lut[c] = oracle_code_unit_value(2, 8, (uint8_t)c);
+  for (int it = 0; it < 40000; ++it) {
+    const float s = ldexpf(1.0f + (float)(rng() % 8388608u) / 8388608.0f, (int)(rng() % 120) - 60);
+    uint8_t codes[256];
+    float want[256];
+    for (int c = 0; c < 256; ++c) codes[c] = (uint8_t)c;
+    oracle_dequantize(codes, &s, 256, 8, 256, 2, want, nullptr, 0);
+    for (int c = 0; c < 256; ++c) {
+      ++n;
+      const float got = d2f_rn_bits(lut[c] * (double)s);
+      if ((c & 0x7f) == 0x7f)
+        bad += std::isfinite(got);  // NaN codes: any non-finite value
+      else
+        bad += f2u(got) != f2u(want[c]);
+    }
+  }
+  // random doubles in the normal-float range, ties at bit 29 included
+  for (int it = 0; it < 2000000; ++it) {
+    uint64_t u = rng();
+    const int e = 1023 - 120 + (int)(rng() % 240);
+    u = (u & 0x800FFFFFFFFFFFFFull) | ((uint64_t)e << 52);
+    if (it % 4 == 0) u = (u & ~0x1FFFFFFFull) | 0x10000000ull;  // exact tie
+    const double d = u64_to_d(u);
+    ++n;
+    bad += f2u(d2f_rn_bits(d)) != f2u((float)d);
+  }
+  report("double->float integer RNE (gradient decode), incl. ties", n, bad);
+}
+
 int main() {
+  check_d2f_bits(41);
   check_fp8_bracket(31);
   check_fp8_t16(5);
   check_fp8_t16i(6);

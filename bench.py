@@ -256,25 +256,60 @@ def bench_act(wl, args, world):
     return sec, launches, (sum(qb) / sum(qt) / 1e9, sum(qt)), (sum(db) / sum(dt) / 1e9, sum(dt))
 
 
-def bench_e2e(wl, args, world, steps):
+def bench_e2e(wl, args, world, steps, chunks=16, nstreams=4):
     """Host-buffer path: pinned BF16 activations H2D every step, all stage
     policies quantize+dequantize on device, each stage's BF16 reconstruction
-    D2H (what dequantize_blockwise returns to a host caller)."""
+    D2H (what dequantize_blockwise returns to a host caller).
+
+    The step is split into `chunks` block-aligned slices of every tensor,
+    issued round-robin on `nstreams` streams, so the H2D of one slice, the
+    kernels of another and the D2H of a third overlap (the two copy directions
+    run on separate copy engines). Block-aligned slices quantize exactly like
+    the whole tensor (no block straddles a slice boundary)."""
     import torch
+    L = wl.L
     host_in = [torch.empty(n, dtype=torch.bfloat16, pin_memory=True) for n in wl.n]
     for h, x in zip(host_in, wl.x):
         h.copy_(x)
     host_out = [torch.empty(n, dtype=torch.bfloat16, pin_memory=True) for n in wl.n]
-    sp = torch.cuda.current_stream().cuda_stream
+    streams = [torch.cuda.Stream() for _ in range(nstreams)]
+    # per chunk: element range of every tensor, and grouped segment tables
+    plan = []
+    for k in range(chunks):
+        rng = []
+        for n in wl.n:
+            nb = (n + 127) // 128
+            b0, b1 = nb * k // chunks, nb * (k + 1) // chunks
+            rng.append((b0 * 128, min(b1 * 128, n)))
+        segq, segd = {}, {}
+        for b in wl.q:
+            sq, sd = (L.AgqSegment * 5)(), (L.AgqSegment * 5)()
+            for i, (e0, e1) in enumerate(rng):
+                c, sc = wl.q[b][i]
+                cp = c.data_ptr() + e0 * b // 8
+                spp = sc.data_ptr() + (e0 // 128) * 4
+                sq[i] = L.AgqSegment(wl.x[i].data_ptr() + 2 * e0, cp, spp, e1 - e0)
+                sd[i] = L.AgqSegment(wl.out[i].data_ptr() + 2 * e0, cp, spp, e1 - e0)
+            segq[b], segd[b] = sq, sd
+        plan.append((rng, segq, segd))
 
     def one():
-        for h, x in zip(host_in, wl.x):
-            x.copy_(h, non_blocking=True)
-        for b in wl.bits:
-            wl.quant(b, sp)
-            wl.dequant(b, sp)
-            for h, o in zip(host_out, wl.out):
-                h.copy_(o, non_blocking=True)
+        main = torch.cuda.current_stream()
+        for st in streams:
+            st.wait_stream(main)
+        for k, (rng, segq, segd) in enumerate(plan):
+            st = streams[k % nstreams]
+            with torch.cuda.stream(st):
+                sp = st.cuda_stream
+                for i, (e0, e1) in enumerate(rng):
+                    wl.x[i][e0:e1].copy_(host_in[i][e0:e1], non_blocking=True)
+                for b in wl.bits:
+                    L.check(L.lib.agq_quantize_grouped(segq[b], 5, L.AGQ_BF16, b, 0, wl.err.ptr, sp))
+                    L.check(L.lib.agq_dequantize_grouped(segd[b], 5, L.AGQ_BF16, b, 0, sp))
+                    for i, (e0, e1) in enumerate(rng):
+                        host_out[i][e0:e1].copy_(wl.out[i][e0:e1], non_blocking=True)
+        for st in streams:
+            main.wait_stream(st)
 
     one()
     torch.cuda.synchronize()
@@ -286,6 +321,12 @@ def bench_e2e(wl, args, world, steps):
     e.record()
     torch.cuda.synchronize()
     sec = max_over_ranks(s.elapsed_time(e) * 1e-3, world)
+    wl.L.errors_message(wl.err.read(), wl.L.AGQ_OP_QUANTIZE)
+    # the result read back must equal the device result of the last stage
+    last = wl.bits[-1]
+    ok = all(torch.equal(h[:4096], o[:4096].cpu()) for h, o in zip(host_out, wl.out))
+    if not ok:
+        raise RuntimeError(f"e2e: host copy of stage {last} differs from the device result")
     bi = sum(wl.n) * 2
     bo = sum(wl.n) * 2 * len(wl.bits)
     return wl.bytes_per_step() * steps * world / sec / 1e9, bi, bo
@@ -663,6 +704,8 @@ def main():
     ap.add_argument("--acc-elements", type=int, default=LLAMA8B_PARAMS)
     ap.add_argument("--algos", default="nccl,p2p")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=16)
+    ap.add_argument("--e2e-streams", type=int, default=4)
     ap.add_argument("--no-accumulate", action="store_true")
     ap.add_argument("--no-allreduce", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -705,7 +748,8 @@ def main():
     value = step_bytes * args.steps * world / sec / 1e9
     extra = {}
     if not args.no_e2e:
-        e2e_val, bi, bo = bench_e2e(wl, args, world, steps=2)
+        e2e_val, bi, bo = bench_e2e(wl, args, world, steps=2, chunks=args.e2e_chunks,
+                                     nstreams=args.e2e_streams)
         extra["e2e"] = {"value": round(e2e_val, 1), "unit": "GB/s", "h2d_bytes_per_step": bi,
                         "d2h_bytes_per_step": bo}
     del wl

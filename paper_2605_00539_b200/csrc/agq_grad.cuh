@@ -59,6 +59,69 @@ __device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) {
   return __byte_perm(w, 0u, 0x4440u | (uint32_t)k);
 }
 
+// Gradient decode through the per-block 8-entry table (1) or the 256-entry
+// signed unit table for every element (0); both exact. K3 (one piece per
+// element) is issue/latency bound and measured faster with the full table;
+// the multi-piece reduce kernels are shared-memory bound and use the block
+// table (profiles/r01_acc_tab_ab.log, r01_reduce_tab_ab.log).
+#ifndef AGQ_ACC_TAB
+#define AGQ_ACC_TAB 0
+#endif
+#ifndef AGQ_RED_TAB
+#define AGQ_RED_TAB 1
+#endif
+// Block-table decode of byte k of w (fp8_dq_tab with the byte moved to the
+// top of the word by one PRMT): tab = the block's 8 entries, fp8_tab_entry.
+__device__ __forceinline__ float fp8_dq_tab_w(uint32_t w, int k, const float* tab) {
+  const uint32_t x = __byte_perm(w, 0u, ((uint32_t)k << 12) | 0x0444u);  // byte k -> bits 24..31
+  const uint32_t y = (uint32_t)((int32_t)x >> 4);
+  return fmul(tab[(x >> 24) & 7u], u2f((y & 0x87800000u) + 0x37800000u));
+}
+// Lean table decode + accumulate of NW code words (4 codes each) against
+// this block's table at shared address tb_s (32-byte aligned, 8 entries
+// holding F[m]/2): the entry address comes straight from the code word
+// (shift + one LOP3), the signed power of two 2^(e-15) from an arithmetic
+// shift + one LOP3 ((e | 0x70) = e + 112 for e < 16), products and sums in
+// f32x2 pairs. Per element ~7 issued ops, no F2F, no bank conflicts.
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+template <int NW>
+__device__ __forceinline__ void dq_tab_accum(const uint32_t (&w)[NW], uint32_t tb_s,
+                                             float (&acc)[4 * NW]) {
+#pragma unroll
+  for (int i = 0; i < NW; ++i) {
+    float f[4], p2[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const uint32_t x = b == 3 ? w[i] : (w[i] << (24 - 8 * b));
+      const uint32_t y = (uint32_t)((int32_t)x >> 4);
+      p2[b] = u2f((y & 0x87800000u) | 0x38000000u);
+      const uint32_t idx = b == 0 ? ((w[i] << 2) & 0x1cu) : ((w[i] >> (8 * b - 2)) & 0x1cu);
+      f[b] = lds_f32(idx | tb_s);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const f32x2 v = mul2(pk2(f[2 * h], f[2 * h + 1]), pk2(p2[2 * h], p2[2 * h + 1]));
+      const f32x2 a = add2(pk2(acc[4 * i + 2 * h], acc[4 * i + 2 * h + 1]), v);
+      up2(a, acc[4 * i + 2 * h], acc[4 * i + 2 * h + 1]);
+    }
+  }
+}
+__device__ __forceinline__ float fp8_tab_entry_half(double t8, float s) {
+  return fmul(fp8_tab_entry(t8, s), 0.5f);  // exact: the entry is a normal float
+}
+
+__device__ __forceinline__ bool fp8_tab_ok16(const uint32_t (&w)[4]) {
+  return (fp8_tab_unsafe(w[0]) | fp8_tab_unsafe(w[1]) | fp8_tab_unsafe(w[2]) |
+          fp8_tab_unsafe(w[3])) == 0u;
+}
+__device__ __forceinline__ bool fp8_tab_ok8(const uint32_t (&w)[2]) {
+  return (fp8_tab_unsafe(w[0]) | fp8_tab_unsafe(w[1])) == 0u;
+}
+
 // A block scale for which fp8_dequant_t16i is exact (zero blocks excluded).
 __device__ __forceinline__ bool dq_fast(float s) { return s >= kFastLo && s <= kFastHi; }
 
@@ -211,15 +274,41 @@ struct PieceTable {
   int np, nout;
 };
 
+// Fill this warp's per-piece block tables after the previous group's lookups
+// are done. LPB lanes per 128-block (8: 16 elements per lane, 16: 8 per
+// lane); lane l builds entry (l & 7) of warp-local block l / LPB, so a piece
+// table is 32 / LPB blocks x 8 entries (lanes l and l + 8 of a 16-lane block
+// store the same value). Blocks past the end build from scale 0 (unused).
+template <int LPB>
+__device__ __forceinline__ uint32_t tab_slot(int lane) { return (lane / LPB) * 8 + (lane & 7); }
+template <int NP, int LPB>
+__device__ __forceinline__ void build_tables(float* wtab, const float (&sc)[NP]) {
+  const int lane = threadIdx.x & 31;
+  const double t8 = fp8_t8(lane & 7);
+  __syncwarp();
+#pragma unroll
+  for (int p = 0; p < NP; ++p) wtab[p * (256 / LPB) + tab_slot<LPB>(lane)] = fp8_tab_entry_half(t8, sc[p]);
+  __syncwarp();
+}
+// shared address of this lane's block table for piece p
+template <int LPB>
+__device__ __forceinline__ uint32_t tab_addr(const float* wtab, int p) {
+  const int lane = threadIdx.x & 31;
+  return (uint32_t)__cvta_generic_to_shared(wtab + p * (256 / LPB) + (lane / LPB) * 8);
+}
+
 // ---------------------------------------------------------------------------
 // K4: block-128 reduce-requant, 16 elements per thread, direct loads.
 // ---------------------------------------------------------------------------
 // One 16-element group: loads of every piece first (memory-level
 // parallelism), then the fp32 sum in ascending piece order from +0.0f.
+// wtab (NP > 0): this warp's block tables, NP x 32 floats (4 blocks x 8
+// entries per piece), or nullptr for the full-table decode only. Every lane
+// of the warp must call (the table build synchronises the warp).
 template <int NP>
 __device__ __forceinline__ void reduce_group(const PieceTable& pt, uint64_t g, uint64_t len,
                                              long long blk_base, const double* t16,
-                                             agq_errors* err, bool vec) {
+                                             agq_errors* err, bool vec, float* wtab = nullptr) {
   const int np = NP > 0 ? NP : pt.np;
   const uint64_t e0 = g * 16;
   const uint64_t blk = e0 / kBlock;
@@ -229,31 +318,41 @@ __device__ __forceinline__ void reduce_group(const PieceTable& pt, uint64_t g, u
 #pragma unroll
   for (int e = 0; e < 16; ++e) acc[e] = 0.0f;
   uint32_t sbad = 0;
-  if (in_range) {
-    constexpr int kMaxUnroll = NP > 0 ? NP : AGQ_MAX_WORLD;
-    uint4 cv[NP > 0 ? NP : 1];
-    float sc[NP > 0 ? NP : 1];
-    if constexpr (NP > 0) {
+  if constexpr (NP > 0) {
+    uint4 cv[NP];
+    float sc[NP];
 #pragma unroll
-      for (int p = 0; p < NP; ++p) {
-        sc[p] = pt.scales[p][blk];
-        if (whole) {
-          cv[p] = *reinterpret_cast<const uint4*>(pt.codes[p] + e0);
-        } else {
-          uint32_t w[4] = {0, 0, 0, 0};
-          for (int e = 0; e < 16 && e0 + e < len; ++e)
-            w[e >> 2] |= (uint32_t)pt.codes[p][e0 + e] << (8 * (e & 3));
-          cv[p] = make_uint4(w[0], w[1], w[2], w[3]);
-        }
+    for (int p = 0; p < NP; ++p) {
+      cv[p] = make_uint4(0, 0, 0, 0);
+      // every lane of an existing block loads its scale: a lane past the end
+      // of a partial last block still builds its table entry for the others
+      sc[p] = blk * kBlock < len ? pt.scales[p][blk] : 0.0f;
+      if (!in_range) continue;
+      if (whole) {
+        cv[p] = *reinterpret_cast<const uint4*>(pt.codes[p] + e0);
+      } else {
+        uint32_t w[4] = {0, 0, 0, 0};
+        for (int e = 0; e < 16 && e0 + e < len; ++e)
+          w[e >> 2] |= (uint32_t)pt.codes[p][e0 + e] << (8 * (e & 3));
+        cv[p] = make_uint4(w[0], w[1], w[2], w[3]);
       }
+    }
+    if (AGQ_RED_TAB && wtab != nullptr) build_tables<NP, 8>(wtab, sc);  // all lanes
+    if (in_range) {
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
         sbad |= !(sc[p] >= 0.0f) || !(sc[p] <= 3.402823466e38f);
         const uint32_t w[4] = {cv[p].x, cv[p].y, cv[p].z, cv[p].w};
-        dq_accum<16>(w, sc[p], t16, acc);
+        if (AGQ_RED_TAB && wtab != nullptr && dq_fast(sc[p]) && fp8_tab_ok16(w)) {
+          dq_tab_accum<4>(w, tab_addr<8>(wtab, p), acc);
+        } else {
+          dq_accum<16>(w, sc[p], t16, acc);
+        }
       }
-    } else {
-      (void)kMaxUnroll;
+    }
+  }
+  if (in_range) {
+    if constexpr (NP == 0) {
 #pragma unroll 1
       for (int p = 0; p < np; ++p) {
         const float scp = pt.scales[p][blk];

@@ -404,6 +404,31 @@ AGQ_HD float d2f_rn_bits(double p) {
   return u2f((uint32_t)(r >> 29) | (hi & 0x80000000u));
 }
 
+// Per-block FP8 decode table (gradient paths). For a normal E4M3 code
+// (exponent field e in 1..15, mantissa m) fl64(v/448) = fl64((8+m)/7)*2^(e-16)
+// exactly, and power-of-two scaling commutes with both roundings while the
+// float result stays normal, which block scales in [2^-60, 2^60] guarantee.
+// So (float)(fl64(v/448)*s) = F[m] * 2^(e-16) with the 8-entry block table
+// F[m] = (float)(fl64((8+m)/7) * s): one DMUL + F2F per entry instead of per
+// element, and an exact FMUL per element. Zero/subnormal (e = 0) and NaN
+// codes are excluded (callers route them to the full table).
+AGQ_HD double fp8_t8(int m) { return (double)(8 + m) / 7.0; }
+AGQ_HD float fp8_tab_entry(double t8, float s) { return d2f_rn(dmul(t8, (double)s)); }
+// signed 2^(e-16) for code byte c (e >= 1): sign and exponent field moved
+// into a float's sign and exponent with one arithmetic shift
+AGQ_HD float fp8_pow2(uint32_t c) {
+  const uint32_t y = (uint32_t)((int32_t)(c << 24) >> 4);
+  return u2f((y & 0x87800000u) + 0x37800000u);
+}
+AGQ_HD float fp8_dq_tab(uint32_t c, const float* tab) { return fmul(tab[c & 7u], fp8_pow2(c)); }
+// nonzero iff one of the 4 code bytes of w is zero/subnormal (e = 0) or NaN
+AGQ_HD uint32_t fp8_tab_unsafe(uint32_t w) {
+  const uint32_t u = w & 0x78787878u;
+  const uint32_t z = (u - 0x01010101u) & ~u;            // byte with e == 0
+  const uint32_t nn = (w & 0x7f7f7f7fu) + 0x01010101u;  // byte with low 7 bits all 1
+  return (z | nn) & 0x80808080u;
+}
+
 // Fast path for BF16-valued scales in [2^-60, 2^60]: p = g*s is exact in
 // FP32 (g has <= 8 significant bits), and the reference value equals the
 // correctly rounded quotient p / den, computed by one Markstein correction

@@ -148,7 +148,7 @@ template <int NP>
 __device__ __forceinline__ void fused_group(unsigned char* const (&base)[NP], uint64_t coff,
                                             uint64_t soff, uint64_t g, uint64_t len,
                                             long long blk_base, const double* t16,
-                                            agq_errors* err) {
+                                            agq_errors* err, float* wtab) {
   const uint64_t e0 = g * 16;
   const uint64_t blk = e0 / kBlock;
   // chunk-relative addresses from one common offset per array
@@ -160,12 +160,14 @@ __device__ __forceinline__ void fused_group(unsigned char* const (&base)[NP], ui
 #pragma unroll
   for (int e = 0; e < 16; ++e) acc[e] = 0.0f;
   uint32_t sbad = 0;
-  if (in_range) {
+  {
     uint4 cv[NP];
     float sc[NP];
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-      sc[p] = sbase(p)[blk];
+      cv[p] = make_uint4(0, 0, 0, 0);
+      sc[p] = blk * kBlock < len ? sbase(p)[blk] : 0.0f;  // whole block's lanes (tables)
+      if (!in_range) continue;
       if (whole) {
         cv[p] = *reinterpret_cast<const uint4*>(cbase(p) + e0);
       } else {
@@ -175,15 +177,21 @@ __device__ __forceinline__ void fused_group(unsigned char* const (&base)[NP], ui
         cv[p] = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
+    if (AGQ_RED_TAB) build_tables<NP, 8>(wtab, sc);  // every lane of the warp
+    if (in_range) {
 #pragma unroll
-    for (int p = 0; p < NP; ++p) {
-      sbad |= !(sc[p] >= 0.0f) || !(sc[p] <= 3.402823466e38f);
-      const uint32_t w[4] = {cv[p].x, cv[p].y, cv[p].z, cv[p].w};
-      dq_accum<16>(w, sc[p], t16, acc);
+      for (int p = 0; p < NP; ++p) {
+        sbad |= !(sc[p] >= 0.0f) || !(sc[p] <= 3.402823466e38f);
+        const uint32_t w[4] = {cv[p].x, cv[p].y, cv[p].z, cv[p].w};
+        if (AGQ_RED_TAB && dq_fast(sc[p]) && fp8_tab_ok16(w))
+          dq_tab_accum<4>(w, tab_addr<8>(wtab, p), acc);
+        else
+          dq_accum<16>(w, sc[p], t16, acc);
+      }
+      if (!whole)
+        for (int e = 0; e < 16; ++e)
+          if (e0 + e >= len) acc[e] = 0.0f;
     }
-    if (!whole)
-      for (int e = 0; e < 16; ++e)
-        if (e0 + e >= len) acc[e] = 0.0f;
   }
   const uint32_t m = absmax_bits16(acc);
   const int sub = threadIdx.x & 7;
@@ -216,7 +224,7 @@ template <int NP>
 __device__ __forceinline__ void fused_group8(unsigned char* const (&base)[NP], uint64_t coff,
                                              uint64_t soff, uint64_t g, uint64_t len,
                                              long long blk_base, const double* t16,
-                                             agq_errors* err) {
+                                             agq_errors* err, float* wtab) {
   const uint64_t e0 = g * 8;
   const uint64_t blk = e0 / kBlock;
   const bool in_range = e0 < len;
@@ -225,12 +233,14 @@ __device__ __forceinline__ void fused_group8(unsigned char* const (&base)[NP], u
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
   uint32_t sbad = 0;
-  if (in_range) {
+  {
     uint2 cv[NP];
     float sc[NP];
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-      sc[p] = reinterpret_cast<const float*>(base[p] + soff)[blk];
+      cv[p] = make_uint2(0, 0);
+      sc[p] = blk * kBlock < len ? reinterpret_cast<const float*>(base[p] + soff)[blk] : 0.0f;
+      if (!in_range) continue;
       if (whole) {
         cv[p] = *reinterpret_cast<const uint2*>(base[p] + coff + e0);
       } else {
@@ -240,15 +250,21 @@ __device__ __forceinline__ void fused_group8(unsigned char* const (&base)[NP], u
         cv[p] = make_uint2(w[0], w[1]);
       }
     }
+    if (AGQ_RED_TAB) build_tables<NP, 16>(wtab, sc);  // every lane of the warp
+    if (in_range) {
 #pragma unroll
-    for (int p = 0; p < NP; ++p) {
-      sbad |= !(sc[p] >= 0.0f) || !(sc[p] <= 3.402823466e38f);
-      const uint32_t w[2] = {cv[p].x, cv[p].y};
-      dq_accum<8>(w, sc[p], t16, acc);
+      for (int p = 0; p < NP; ++p) {
+        sbad |= !(sc[p] >= 0.0f) || !(sc[p] <= 3.402823466e38f);
+        const uint32_t w[2] = {cv[p].x, cv[p].y};
+        if (AGQ_RED_TAB && dq_fast(sc[p]) && fp8_tab_ok8(w))
+          dq_tab_accum<2>(w, tab_addr<16>(wtab, p), acc);
+        else
+          dq_accum<8>(w, sc[p], t16, acc);
+      }
+      if (!whole)
+        for (int e = 0; e < 8; ++e)
+          if (e0 + e >= len) acc[e] = 0.0f;
     }
-    if (!whole)
-      for (int e = 0; e < 8; ++e)
-        if (e0 + e >= len) acc[e] = 0.0f;
   }
   const uint32_t m = absmax_bits8(acc);
   const int sub = threadIdx.x & 15;
@@ -279,8 +295,10 @@ __device__ __forceinline__ void fused_group8(unsigned char* const (&base)[NP], u
 template <int NP, int EPT>
 __global__ void __launch_bounds__(256, 2) k_fused_allreduce(FusedArgs a) {
   __shared__ double lut[kDqTable];
+  __shared__ float btab[8 * (NP > 0 ? NP : 1) * 32];  // 8 warps x NP pieces x 32 entries
   __shared__ int ok;
   fill_fp8_dq_table(lut);
+  float* wtab = btab + (threadIdx.x >> 5) * (NP > 0 ? NP : 1) * 32;
   const int tid = threadIdx.x;
   uint64_t* my_flags = reinterpret_cast<uint64_t*>(a.base[a.rank]);
   // start barrier: announce "my input is final" to every rank, then wait for
@@ -325,10 +343,10 @@ __global__ void __launch_bounds__(256, 2) k_fused_allreduce(FusedArgs a) {
       if constexpr (EPT == 8) {
         const uint64_t ng8 = nblocks * 16, gp8 = (ng8 + 31) / 32 * 32;
         for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + tid; g < gp8; g += stride)
-          fused_group8<NP>(bs, coff, soff, g, g < ng8 ? a.len : 0, (long long)b0, lut, a.err);
+          fused_group8<NP>(bs, coff, soff, g, g < ng8 ? a.len : 0, (long long)b0, lut, a.err, wtab);
       } else {
         for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + tid; g < gpad; g += stride)
-          fused_group<NP>(bs, coff, soff, g, g < ngroups ? a.len : 0, (long long)b0, lut, a.err);
+          fused_group<NP>(bs, coff, soff, g, g < ngroups ? a.len : 0, (long long)b0, lut, a.err, wtab);
       }
     }
   } else {

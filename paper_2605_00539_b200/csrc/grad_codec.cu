@@ -182,10 +182,13 @@ __global__ void __launch_bounds__(kAccWarps * 32, 3)
   constexpr uint32_t kLocTileB = kAccWarpElems * (BF16L ? 2 : 4);  // 1 KB / 2 KB
   __shared__ __align__(16) unsigned char sbuf[kAccWarps][kLocTileB];
   __shared__ double t16[kDqTable];
+  __shared__ float btab[kAccWarps][32];  // per warp: 4 blocks x 8 table entries
   fill_fp8_dq_table(t16);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wb = sbuf[warp];
+  const double t8 = fp8_t8(lane & 7);  // lane 8b+j builds entry j of block b
+  const float* mytab = &btab[warp][lane & ~7];
   const uint64_t nw = (uint64_t)gridDim.x * kAccWarps;
   uint64_t t = (uint64_t)blockIdx.x * kAccWarps + warp;
   const unsigned char* lbase = static_cast<const unsigned char*>(local);
@@ -208,6 +211,7 @@ __global__ void __launch_bounds__(kAccWarps * 32, 3)
     }
     const uint32_t cw[4] = {pc.x, pc.y, pc.z, pc.w};
     const float sc = ps;
+    btab[warp][lane] = fp8_tab_entry(t8, sc);
     __syncwarp();
     if (t + nw < ntiles) load(t + nw);
     float l[16];
@@ -230,11 +234,17 @@ __global__ void __launch_bounds__(kAccWarps * 32, 3)
     const uint64_t gblk = t * 4 + (lane >> 3);
     if ((!(sc >= 0.0f) || !(sc <= 3.402823466e38f)) && (lane & 7) == 0)
       err_min(&err->bad_scale_block, (long long)gblk);
-    const double sd = (double)sc;
     float v[16];
+    if (AGQ_ACC_TAB && dq_fast(sc) && fp8_tab_ok16(cw)) {
 #pragma unroll
-    for (int e = 0; e < 16; ++e)
-      v[e] = apply_prec<PREC>(fadd(fp8_dq_lut(byte_of(cw[e >> 2], e & 3), sd, t16), l[e]));
+      for (int e = 0; e < 16; ++e)
+        v[e] = apply_prec<PREC>(fadd(fp8_dq_tab_w(cw[e >> 2], e & 3, mytab), l[e]));
+    } else {  // zero/subnormal/NaN codes or an extreme scale: full table
+      const double sd = (double)sc;
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        v[e] = apply_prec<PREC>(fadd(fp8_dq_lut(byte_of(cw[e >> 2], e & 3), sd, t16), l[e]));
+    }
     const uint32_t m = absmax_bits16(v);
     if (m >= 0x7f800000u) {
       // a non-finite local gradient makes the sum non-finite: tell the two
@@ -343,19 +353,24 @@ __global__ void k_reduce_generic(PieceTable pt, uint64_t len, uint32_t block, ui
   }
 }
 
+#ifndef AGQ_RED_MINB
+#define AGQ_RED_MINB 1
+#endif
 template <int NP>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, AGQ_RED_MINB)
     k_reduce128(PieceTable pt, uint64_t len, long long blk_base, int vec, agq_errors* err) {
   __shared__ double lut[kDqTable];
+  __shared__ float btab[NP > 0 ? 8 * NP * 32 : 1];  // 8 warps x NP pieces x 32 entries
   fill_fp8_dq_table(lut);
   __syncthreads();
   const uint64_t nblocks = (len + kBlock - 1) / kBlock;
   const uint64_t ngroups = nblocks * 8;
   const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
+  float* wtab = NP > 0 ? btab + (threadIdx.x >> 5) * NP * 32 : nullptr;
   // warp-uniform trip count so the 8-lane shuffles always have all lanes
   const uint64_t gpad = (ngroups + 31) / 32 * 32;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < gpad; g += stride)
-    reduce_group<NP>(pt, g, g < ngroups ? len : 0, blk_base, lut, err, vec != 0);
+    reduce_group<NP>(pt, g, g < ngroups ? len : 0, blk_base, lut, err, vec != 0, wtab);
 }
 
 // ---------------------------------------------------------------------------

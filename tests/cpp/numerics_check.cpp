@@ -434,7 +434,48 @@ static void check_d2f_bits(uint64_t seed) {
   report("double->float integer RNE (gradient decode), incl. ties", n, bad);
 }
 
+// Per-block 8-entry decode table (K3/K4 gradient decode)
+static void check_fp8_tab(uint64_t seed) {
+  std::mt19937_64 rng(seed);
+  long long n = 0, bad = 0, unsafe_ok = 0;
+  double t8[8];
+  for (int m = 0; m < 8; ++m) t8[m] = fp8_t8(m);
+  // the unsafe-byte detector against a per-byte definition, all 2^16 byte pairs x 4 positions
+  for (uint32_t a = 0; a < 256; ++a)
+    for (uint32_t b = 0; b < 256; ++b) {
+      const uint32_t w = a | (b << 8) | (0x40u << 16) | (0x3au << 24);
+      auto uns = [](uint32_t c) { return ((c & 0x78u) == 0) || ((c & 0x7fu) == 0x7fu); };
+      const bool want = uns(a) || uns(b);
+      const uint32_t w2 = (a << 16) | (b << 24) | 0x4040u;
+      ++n;
+      bad += (fp8_tab_unsafe(w) != 0) != want;
+      bad += (fp8_tab_unsafe(w2) != 0) != want;
+      unsafe_ok += want;
+    }
+  auto run_scale = [&](float s) {
+    uint8_t codes[256];
+    float want[256];
+    for (int c = 0; c < 256; ++c) codes[c] = (uint8_t)c;
+    oracle_dequantize(codes, &s, 256, 8, 256, 2, want, nullptr, 0);
+    float tab[8];
+    for (int m = 0; m < 8; ++m) tab[m] = fp8_tab_entry(t8[m], s);
+    for (int c = 0; c < 256; ++c) {
+      if ((c & 0x78) == 0 || (c & 0x7f) == 0x7f) continue;
+      ++n;
+      bad += f2u(fp8_dq_tab((uint32_t)c, tab)) != f2u(want[c]);
+    }
+  };
+  // every BF16 scale in [2^-60, 2^60] and random FP32 scales there
+  for (int e = -60; e < 60; ++e)
+    for (int k = 0; k < 128; ++k) run_scale(ldexpf(1.0f + k / 128.0f, e));
+  run_scale(0x1p60f);
+  for (int it = 0; it < 200000; ++it)
+    run_scale(ldexpf(1.0f + (float)(rng() % 8388608u) / 8388608.0f, (int)(rng() % 120) - 60));
+  report("fp8 decode via 8-entry block table (+ unsafe-byte detector)", n, bad);
+}
+
 int main() {
+  check_fp8_tab(43);
   check_d2f_bits(41);
   check_fp8_bracket(31);
   check_fp8_t16(5);

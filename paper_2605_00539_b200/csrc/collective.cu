@@ -611,15 +611,17 @@ agq_status allreduce_nccl(agq_comm* c, uint8_t* codes, float* scales, uint64_t n
   return nccl_fail(nccl().GroupEnd(), "all-gather");
 }
 
-// Elements per thread: 16 up to 4 ranks, 8 beyond (register budget);
-// AGQ_P2P_EPT=8 forces the 8-element kernel (lets 2-4 GPU runs test it).
+// Elements per thread: 16 (measured ~10% faster than 8 at 4 GPUs,
+// profiles/r01_p2p_ept_ctas_n4.log; with the block-table decode the NP = 8
+// instance fits 128 registers without spills). AGQ_P2P_EPT=8 selects the
+// 8-element kernel (16 lanes per block) for comparison.
 int fused_ept(int P) {
+  (void)P;
   static const int forced = [] {
     const char* e = getenv("AGQ_P2P_EPT");
     return e ? atoi(e) : 0;
   }();
-  if (forced == 8 || forced == 16) return forced;
-  return P >= 5 ? 8 : 16;
+  return forced == 8 ? 8 : 16;
 }
 
 template <int NP>

@@ -497,7 +497,7 @@ def bench_allreduce(dev, args, world, rank, n):
     wire = n * (1 + 4 / 128)
     fac = 2 * (world - 1) / world
     for algo in args.algos:
-        if algo == "p2p":
+        if algo in ("p2p", "push"):
             comm.enable_p2p(n)
             pc, ps = comm.p2p_buffers(n)
             qq = A.QuantizedTensor(pc, ps, 8, 128, (n,), A.CodecKind.Fp8E4M3, packed=False)
@@ -522,9 +522,9 @@ def bench_allreduce(dev, args, world, rank, n):
             continue
         res[algo] = {"ms": round(sec * 1e3, 3), "bus_GBs_wire": round(fac * wire / sec / 1e9, 1),
                      "bus_GBs_bf16_equiv": round(fac * 2 * n / sec / 1e9, 1)}
-        if algo == "p2p" and "ms" in res.get("nccl", {}):
+        if algo in ("p2p", "push") and "ms" in res.get("nccl", {}):
             ok = torch.equal(qq.codes, q.codes) and torch.equal(qq.scales, q.scales)
-            res["p2p_equals_nccl"] = bool(ok)
+            res[algo + "_equals_nccl"] = bool(ok)
     del src_codes
     # BF16 baseline on the same element count
     gb = torch.empty(n, dtype=torch.bfloat16, device=dev)
@@ -561,7 +561,7 @@ def bench_sweep(dev, args, world, rank):
     buckets = {"llama32b_layer_bucket": layer, "megatron_40M_bucket": 40_000_000}
     nmax = max(max(sizes), layer)
     comm = Communicator(device=dev.index)
-    if "p2p" in args.algos:
+    if "p2p" in args.algos or "push" in args.algos:
         comm.enable_p2p(nmax)
     sp = torch.cuda.current_stream().cuda_stream
     g = torch.Generator(device=dev).manual_seed(7 + rank)
@@ -573,7 +573,7 @@ def bench_sweep(dev, args, world, rank):
         L.check(L.lib.agq_quantize(x.data_ptr(), L.AGQ_F32, m, 8, 128, 2, src_c[off:].data_ptr(),
                                    L.AGQ_CODES_BYTES, src_s[off // 128:].data_ptr(), None, sp))
     work_c, work_s = torch.empty_like(src_c), torch.empty_like(src_s)
-    if "p2p" in args.algos:
+    if "p2p" in args.algos or "push" in args.algos:
         pc, ps = comm.p2p_buffers(nmax)
     gb = torch.empty(nmax, dtype=torch.bfloat16, device=dev)
     gb.normal_(0, 1e-3, generator=g)
@@ -612,7 +612,7 @@ def bench_sweep(dev, args, world, rank):
     for name, n in cases:
         row = {"case": name, "elements": n, "fp8_wire_bytes": int(n * (1 + 4 / 128))}
         for algo in args.algos:
-            cb, sb = (pc, ps) if algo == "p2p" else (work_c, work_s)
+            cb, sb = (pc, ps) if algo in ("p2p", "push") else (work_c, work_s)
             nb = (n + 127) // 128
 
             def restore(cb=cb, sb=sb):
@@ -725,7 +725,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ar-elements", type=int, default=LLAMA8B_PARAMS)
     ap.add_argument("--acc-elements", type=int, default=LLAMA8B_PARAMS)
-    ap.add_argument("--algos", default="nccl,p2p")
+    ap.add_argument("--algos", default="nccl,p2p,push")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=16)
     ap.add_argument("--e2e-streams", type=int, default=4)

@@ -186,15 +186,17 @@ agq_status agq_allreduce_naive_simulated(int world, const uint8_t* const* codes,
 
 /* ---- multi-GPU decomposed all-reduce (one process per GPU) --------------- */
 typedef struct agq_comm agq_comm;
-enum { AGQ_AR_NCCL = 0, AGQ_AR_FUSED_P2P = 1 };
+enum { AGQ_AR_NCCL = 0, AGQ_AR_FUSED_P2P = 1, AGQ_AR_PUSH_P2P = 2 };
 
 agq_status agq_comm_unique_id(unsigned char id[128]);
 /* Collective over all ranks (NCCL communicator). device = CUDA ordinal. */
 agq_status agq_comm_init(agq_comm** comm, const unsigned char id[128],
                          int nranks, int rank, int device);
-/* Peer-memory setup for AGQ_AR_FUSED_P2P: export this rank's IPC handle,
- * then open every peer's. Handles are exchanged by the caller (any
- * transport). capacity = max element count per all-reduce. */
+/* Peer-memory setup for AGQ_AR_FUSED_P2P / AGQ_AR_PUSH_P2P: export this
+ * rank's IPC handle, then open every peer's. Handles are exchanged by the
+ * caller (any transport). capacity = max element count per all-reduce; the
+ * symmetric buffer holds the gradient (capacity * (1 + 4/128) bytes) plus
+ * the push algorithm's inbox (one chunk per sender, about the same again). */
 agq_status agq_comm_p2p_export(agq_comm* comm, uint64_t capacity,
                                unsigned char handle[256]);
 agq_status agq_comm_p2p_open(agq_comm* comm, const unsigned char* handles
@@ -210,8 +212,11 @@ int agq_comm_size(const agq_comm* comm);
 /* Replaces allreduce_decomposed for real ranks: in-place on this rank's FP8
  * gradient (codes one byte/element + block scales). All ranks call it with
  * the same n/block. algo = AGQ_AR_NCCL (grouped send/recv all-to-all +
- * reduce-requant kernel + ncclAllGather) or AGQ_AR_FUSED_P2P (one kernel
- * per rank over NVLink peer memory). */
+ * reduce-requant kernel + ncclAllGather), AGQ_AR_FUSED_P2P (one kernel per
+ * rank: pull pieces over NVLink, reduce, push results) or AGQ_AR_PUSH_P2P
+ * (two kernels per rank, every NVLink transfer a store: scatter pieces into
+ * the owners' inboxes, then reduce from local memory and push results).
+ * All three give bit-identical results. */
 agq_status agq_allreduce_fp8(agq_comm* comm, uint8_t* codes, float* scales,
                              uint64_t n, uint32_t block, int algo,
                              agq_errors* d_err, agq_stream_t stream);

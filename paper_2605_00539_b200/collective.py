@@ -25,7 +25,7 @@ class _CudaArray:
 
 
 class Communicator:
-    ALGOS = {"nccl": L.AGQ_AR_NCCL, "p2p": L.AGQ_AR_FUSED_P2P}
+    ALGOS = {"nccl": L.AGQ_AR_NCCL, "p2p": L.AGQ_AR_FUSED_P2P, "push": L.AGQ_AR_PUSH_P2P}
 
     def __init__(self, group=None, device: int | None = None, p2p_capacity: int = 0):
         import torch.distributed as dist

@@ -80,7 +80,7 @@ const NcclApi& nccl() {
 // Symmetric buffer layout (identical offsets on every rank).
 namespace {
 constexpr size_t kFlagsBytes = 4096;  // ready[16] | done[16] | err words
-constexpr int kReadyOff = 0, kDoneOff = 16;
+constexpr int kReadyOff = 0, kDoneOff = 16, kScatterOff = 32;
 size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 }  // namespace
 
@@ -292,6 +292,46 @@ __device__ __forceinline__ void fused_group8(unsigned char* const (&base)[NP], u
   }
 }
 
+// End of an all-reduce epoch (every CTA calls it): the last CTA of this
+// rank's grid to finish publishes "done" to every rank and waits for all of
+// them, so the kernel completes only when every rank has finished writing
+// into this rank's buffer (and reading from it). A local-reduce overflow is
+// shared with every rank first (collective.hpp:278-281 aborts all ranks).
+template <class Args>
+__device__ __forceinline__ void epoch_end(const Args& a) {
+  unsigned char* const* base = a.base;
+  const int P = a.P, rank = a.rank;
+  const uint64_t epoch = a.epoch;
+  unsigned int* done_counter = a.done_counter;
+  agq_errors* err = a.err;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const unsigned int prev = atomicAdd(done_counter, 1u);
+  if (prev != gridDim.x * gridDim.y - 1) return;
+  __threadfence_system();
+  uint64_t* my_flags = reinterpret_cast<uint64_t*>(base[rank]);
+  const long long ov = *reinterpret_cast<volatile long long*>(&err->overflow_block);
+  for (int s = 0; s < P; ++s) {
+    uint64_t* peer_flags = reinterpret_cast<uint64_t*>(base[s]);
+    if (ov != kNone) atomicMin(reinterpret_cast<long long*>(peer_flags + 64 + rank), ov);
+  }
+  __threadfence_system();
+  for (int s = 0; s < P; ++s)
+    st_release_sys(reinterpret_cast<uint64_t*>(base[s]) + kDoneOff + rank, epoch);
+  bool fine = true;
+  for (int s = 0; s < P; ++s)
+    if (!wait_flag(my_flags + kDoneOff + s, epoch)) fine = false;
+  for (int s = 0; s < P; ++s) {
+    const long long o = *reinterpret_cast<volatile long long*>(my_flags + 64 + s);
+    if (o != kNone) err_min(&err->overflow_block, o);
+    // reset for the next epoch
+    *reinterpret_cast<volatile long long*>(my_flags + 64 + s) = kNone;
+  }
+  if (!fine) err_min(&err->overflow_block, -1);
+  *done_counter = 0u;
+}
+
 template <int NP, int EPT>
 __global__ void __launch_bounds__(256, 2) k_fused_allreduce(FusedArgs a) {
   __shared__ double lut[kDqTable];
@@ -363,37 +403,107 @@ __global__ void __launch_bounds__(256, 2) k_fused_allreduce(FusedArgs a) {
       reduce_group<0>(pt, g, g < ngroups ? a.len : 0, (long long)b0, lut, a.err, true);
   }
 
-  // end barrier: the last CTA to finish publishes "done" to every rank and
-  // waits for all of them, so the kernel completes only when every chunk of
-  // this rank's buffer has been written.
+  epoch_end(a);
+}
+
+// ---------------------------------------------------------------------------
+// Push all-reduce (AGQ_AR_PUSH_P2P): the same decomposition with every NVLink
+// transfer a fire-and-forget store (SM stores reach 690 GB/s per direction on
+// this NVSwitch, pulls 655, profiles/r01_nvlink_probe_n4.log) and no load on
+// a reduction's critical path crossing NVLink:
+//   1. k_push_scatter: chunk q of my gradient -> inbox slot [me] of rank q;
+//      the last CTA publishes "scattered" to every rank.
+//   2. k_push_reduce: wait for every rank's "scattered", reduce my chunk from
+//      P local pieces (my own + P-1 inbox slots, HBM) in ascending sender
+//      rank, requantize, store the result into every rank's buffer; the epoch
+//      end barrier (epoch_end) keeps the next call's scatter out of inboxes
+//      still being read.
+// ---------------------------------------------------------------------------
+struct PushArgs {
+  unsigned char* base[AGQ_MAX_WORLD];
+  uint64_t scales_off, codes_off;              // my gradient in the symmetric buffer
+  uint64_t in_scales_off, in_codes_off;        // inbox (P slots, indexed by sender)
+  uint64_t slot_scales, slot_codes;            // bytes per inbox slot
+  uint64_t rg[2 * AGQ_MAX_WORLD];              // chunk [begin, end) per owner (elements)
+  uint64_t epoch;
+  unsigned int* done_counter;
+  agq_errors* err;
+  int rank, P;
+};
+
+__global__ void __launch_bounds__(256) k_push_scatter(PushArgs a) {
+  const int q = (a.rank + 1 + (int)blockIdx.y) % a.P;  // staggered peers
+  const uint64_t b = a.rg[2 * q], len = a.rg[2 * q + 1] - b;
+  const unsigned char* src = a.base[a.rank] + a.codes_off + b;
+  unsigned char* dst = a.base[q] + a.in_codes_off + (uint64_t)a.rank * a.slot_codes;
+  const uint64_t nv = len / 16;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t nth = gridDim.x * (uint64_t)blockDim.x;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  uint64_t i = tid;
+  for (; i + 3 * nth < nv; i += 4 * nth) {  // 4 independent 16-byte loads in flight
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = ldg128_stream(s4 + i + u * nth);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) d4[i + u * nth] = v[u];
+  }
+  for (; i < nv; i += nth) d4[i] = ldg128_stream(s4 + i);
+  for (uint64_t j = nv * 16 + tid; j < len; j += nth) dst[j] = src[j];
+  // block scales of chunk q
+  const uint64_t nbq = (len + kBlock - 1) / kBlock;
+  const float* ss = reinterpret_cast<const float*>(a.base[a.rank] + a.scales_off) + b / kBlock;
+  float* ds = reinterpret_cast<float*>(a.base[q] + a.in_scales_off +
+                                       (uint64_t)a.rank * a.slot_scales);
+  for (uint64_t j = tid; j < nbq; j += nth) ds[j] = ss[j];
+  // publish "scattered" once every CTA's stores are performed system-wide
   __threadfence_system();
   __syncthreads();
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
     const unsigned int prev = atomicAdd(a.done_counter, 1u);
-    if (prev == gridDim.x - 1) {
-      __threadfence_system();
-      // share a local-reduce overflow with every rank (runtime_error on all)
-      const long long ov = *reinterpret_cast<volatile long long*>(&a.err->overflow_block);
-      for (int s = 0; s < a.P; ++s) {
-        uint64_t* peer_flags = reinterpret_cast<uint64_t*>(a.base[s]);
-        if (ov != kNone) atomicMin(reinterpret_cast<long long*>(peer_flags + 64 + a.rank), ov);
-      }
+    if (prev == gridDim.x * gridDim.y - 1) {
       __threadfence_system();
       for (int s = 0; s < a.P; ++s)
-        st_release_sys(reinterpret_cast<uint64_t*>(a.base[s]) + kDoneOff + a.rank, a.epoch);
-      bool fine = true;
-      for (int s = 0; s < a.P; ++s)
-        if (!wait_flag(my_flags + kDoneOff + s, a.epoch)) fine = false;
-      for (int s = 0; s < a.P; ++s) {
-        const long long o = *reinterpret_cast<volatile long long*>(my_flags + 64 + s);
-        if (o != kNone) err_min(&a.err->overflow_block, o);
-        // reset for the next epoch
-        *reinterpret_cast<volatile long long*>(my_flags + 64 + s) = kNone;
-      }
-      if (!fine) err_min(&a.err->overflow_block, -1);
+        if (s != a.rank)
+          st_release_sys(reinterpret_cast<uint64_t*>(a.base[s]) + kScatterOff + a.rank, a.epoch);
       *a.done_counter = 0u;
     }
   }
+}
+
+// pt: pieces in ascending sender rank (my own chunk, else my inbox slot of
+// that sender) and outputs = chunk [me] of every rank's buffer; built on the
+// host so it stays in the parameter bank.
+template <int NP>
+__global__ void __launch_bounds__(256) k_push_reduce(PushArgs a, PieceTable pt) {
+  __shared__ double lut[kDqTable];
+  __shared__ float btab[8 * (NP > 0 ? NP : 1) * 32];
+  __shared__ int ok;
+  fill_fp8_dq_table(lut);
+  const int tid = threadIdx.x;
+  uint64_t* my_flags = reinterpret_cast<uint64_t*>(a.base[a.rank]);
+  if (tid == 0) {
+    ok = 1;
+    for (int s = 0; s < a.P; ++s)
+      if (s != a.rank && !wait_flag(my_flags + kScatterOff + s, a.epoch)) ok = 0;
+  }
+  __syncthreads();
+  if (!ok) {
+    if (tid == 0) err_min(&a.err->overflow_block, -1);
+    epoch_end(a);
+    return;
+  }
+  const uint64_t begin = a.rg[2 * a.rank], len = a.rg[2 * a.rank + 1] - begin;
+  const uint64_t b0 = begin / kBlock;
+  const uint64_t nblocks = (len + kBlock - 1) / kBlock;
+  const uint64_t ngroups = nblocks * 8;
+  const uint64_t gpad = (ngroups + 31) / 32 * 32;
+  const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
+  float* wtab = NP > 0 ? btab + (tid >> 5) * NP * 32 : nullptr;
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + tid; g < gpad; g += stride)
+    reduce_group<NP>(pt, g, g < ngroups ? len : 0, (long long)b0, lut, a.err, true, wtab);
+  epoch_end(a);
 }
 
 __global__ void k_init_flags(uint64_t* flags) {
@@ -451,9 +561,27 @@ agq_status comm_init(agq_comm** out, const unsigned char id[128], int nranks, in
   return AGQ_OK;
 }
 
-agq_status comm_p2p_export(agq_comm* c, uint64_t capacity, unsigned char handle[256]) {
+// Symmetric buffer: [flags 4 KB | scales | codes | inbox scales | inbox codes],
+// the inbox holding P slots of one chunk each (push algorithm).
+struct SymLayout {
+  uint64_t scales_off, codes_off, in_scales_off, in_codes_off, slot_scales, slot_codes, bytes;
+};
+SymLayout sym_layout(uint64_t capacity, int P) {
+  SymLayout L{};
   const uint64_t nb = (capacity + kBlock - 1) / kBlock;
-  const size_t bytes = kFlagsBytes + round_up(nb * 4, 256) + round_up(capacity, 256);
+  const uint64_t chunk_blocks = (nb + P - 1) / P;
+  L.scales_off = kFlagsBytes;
+  L.codes_off = L.scales_off + round_up(nb * 4, 256);
+  L.in_scales_off = L.codes_off + round_up(capacity, 256);
+  L.slot_scales = round_up(chunk_blocks * 4, 256);
+  L.in_codes_off = L.in_scales_off + (uint64_t)P * L.slot_scales;
+  L.slot_codes = round_up(chunk_blocks * kBlock, 256);
+  L.bytes = L.in_codes_off + (uint64_t)P * L.slot_codes;
+  return L;
+}
+
+agq_status comm_p2p_export(agq_comm* c, uint64_t capacity, unsigned char handle[256]) {
+  const size_t bytes = sym_layout(capacity, c->nranks).bytes;
   if (c->sym && c->sym_bytes >= bytes) {
     // keep the existing mapping
   } else {
@@ -499,9 +627,9 @@ agq_status comm_p2p_open(agq_comm* c, const unsigned char* handles) {
 
 agq_status comm_p2p_buffers(agq_comm* c, uint8_t** codes, float** scales) {
   if (!c->sym) return set_error(AGQ_ERR_INVALID_ARGUMENT, "p2p buffers not exported");
-  const uint64_t nb = (c->sym_cap + kBlock - 1) / kBlock;
-  *scales = reinterpret_cast<float*>(c->sym + kFlagsBytes);
-  *codes = c->sym + kFlagsBytes + round_up(nb * 4, 256);
+  const SymLayout L = sym_layout(c->sym_cap, c->nranks);
+  *scales = reinterpret_cast<float*>(c->sym + L.scales_off);
+  *codes = c->sym + L.codes_off;
   return AGQ_OK;
 }
 
@@ -652,7 +780,7 @@ agq_status allreduce_p2p(agq_comm* c, uint8_t* codes, float* scales, uint64_t n,
   chunk_ranges(n, block, P, rg.data());
   FusedArgs a{};
   for (int q = 0; q < P; ++q) a.base[q] = c->peer[q];
-  a.scales_off = kFlagsBytes;
+  a.scales_off = (uint64_t)(reinterpret_cast<unsigned char*>(sc_scales) - c->sym);
   a.codes_off = (uint64_t)(reinterpret_cast<unsigned char*>(sc_codes) - c->sym);
   a.begin = rg[2 * r];
   a.len = rg[2 * r + 1] - rg[2 * r];
@@ -695,6 +823,92 @@ agq_status allreduce_p2p(agq_comm* c, uint8_t* codes, float* scales, uint64_t n,
   return AGQ_OK;
 }
 
+template <int NP>
+void launch_push_reduce(const PushArgs& a, const PieceTable& pt, int grid, cudaStream_t s) {
+  k_push_reduce<NP><<<grid, 256, 0, s>>>(a, pt);
+}
+
+agq_status allreduce_push(agq_comm* c, uint8_t* codes, float* scales, uint64_t n, uint32_t block,
+                          agq_errors* err, cudaStream_t s) {
+  if (!c->p2p_ready) return set_error(AGQ_ERR_INVALID_ARGUMENT, "p2p buffers not opened");
+  if (block != (uint32_t)kBlock) return set_error(AGQ_ERR_INVALID_ARGUMENT, "push all-reduce needs block 128");
+  if (n > c->sym_cap) return set_error(AGQ_ERR_INVALID_ARGUMENT, "all-reduce larger than p2p capacity");
+  if (!err) return set_error(AGQ_ERR_INVALID_ARGUMENT, "push all-reduce needs an error record");
+  const SymLayout L = sym_layout(c->sym_cap, c->nranks);
+  uint8_t* sc_codes = c->sym + L.codes_off;
+  float* sc_scales = reinterpret_cast<float*>(c->sym + L.scales_off);
+  const uint64_t nb = (n + block - 1) / block;
+  const bool inplace = codes == sc_codes && scales == sc_scales;
+  if (!inplace) {
+    cudaMemcpyAsync(sc_codes, codes, n, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(sc_scales, scales, nb * 4, cudaMemcpyDeviceToDevice, s);
+  }
+  const int P = c->nranks, r = c->rank;
+  std::vector<uint64_t> rg(2 * P);
+  chunk_ranges(n, block, P, rg.data());
+  PushArgs a{};
+  for (int q = 0; q < P; ++q) a.base[q] = c->peer[q];
+  for (int q = 0; q < 2 * P; ++q) a.rg[q] = rg[q];
+  a.scales_off = L.scales_off;
+  a.codes_off = L.codes_off;
+  a.in_scales_off = L.in_scales_off;
+  a.in_codes_off = L.in_codes_off;
+  a.slot_scales = L.slot_scales;
+  a.slot_codes = L.slot_codes;
+  a.epoch = ++c->epoch;
+  a.done_counter = c->done_counter;
+  a.err = err;
+  a.rank = r;
+  a.P = P;
+  uint64_t maxlen = 0;
+  for (int q = 0; q < P; ++q) maxlen = std::max<uint64_t>(maxlen, rg[2 * q + 1] - rg[2 * q]);
+  // scatter: ~2 CTAs per SM in total across the P-1 peers
+  uint64_t gx = (maxlen / 16 + 1023) / 1024;
+  const uint64_t cap_x = std::max<uint64_t>(1, (uint64_t)num_sms() * 2 / (P - 1));
+  gx = std::min<uint64_t>(std::max<uint64_t>(gx, 1), cap_x);
+  k_push_scatter<<<dim3((unsigned)gx, (unsigned)(P - 1)), 256, 0, s>>>(a);
+  count_launch();
+  agq_status st = cuda_fail(cudaGetLastError(), "push all-reduce: scatter launch");
+  if (st) return st;
+  PieceTable pt{};
+  pt.np = P;
+  pt.nout = P;
+  const uint64_t begin = rg[2 * r];
+  for (int q = 0; q < P; ++q) {
+    if (q == r) {
+      pt.codes[q] = c->peer[r] + L.codes_off + begin;
+      pt.scales[q] = reinterpret_cast<const float*>(c->peer[r] + L.scales_off) + begin / kBlock;
+    } else {
+      pt.codes[q] = c->peer[r] + L.in_codes_off + (uint64_t)q * L.slot_codes;
+      pt.scales[q] = reinterpret_cast<const float*>(c->peer[r] + L.in_scales_off +
+                                                    (uint64_t)q * L.slot_scales);
+    }
+    pt.out_codes[q] = c->peer[q] + L.codes_off + begin;
+    pt.out_scales[q] = reinterpret_cast<float*>(c->peer[q] + L.scales_off) + begin / kBlock;
+  }
+  const uint64_t groups = (rg[2 * r + 1] - rg[2 * r] + kBlock - 1) / kBlock * 8;
+  uint64_t grid = (groups + 255) / 256;
+  grid = std::min<uint64_t>(std::max<uint64_t>(grid, 1), (uint64_t)num_sms() * 2);
+  switch (P) {
+    case 2: launch_push_reduce<2>(a, pt, (int)grid, s); break;
+    case 3: launch_push_reduce<3>(a, pt, (int)grid, s); break;
+    case 4: launch_push_reduce<4>(a, pt, (int)grid, s); break;
+    case 5: launch_push_reduce<5>(a, pt, (int)grid, s); break;
+    case 6: launch_push_reduce<6>(a, pt, (int)grid, s); break;
+    case 7: launch_push_reduce<7>(a, pt, (int)grid, s); break;
+    case 8: launch_push_reduce<8>(a, pt, (int)grid, s); break;
+    default: return set_error(AGQ_ERR_INVALID_ARGUMENT, "push all-reduce: world size 2..8");
+  }
+  count_launch();
+  st = cuda_fail(cudaGetLastError(), "push all-reduce: reduce launch");
+  if (st) return st;
+  if (!inplace) {
+    cudaMemcpyAsync(codes, sc_codes, n, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(scales, sc_scales, nb * 4, cudaMemcpyDeviceToDevice, s);
+  }
+  return AGQ_OK;
+}
+
 }  // namespace
 
 agq_status allreduce_fp8(agq_comm* c, uint8_t* codes, float* scales, uint64_t n, uint32_t block,
@@ -708,6 +922,7 @@ agq_status allreduce_fp8(agq_comm* c, uint8_t* codes, float* scales, uint64_t n,
     return reduce_requant_device(1, &pc, &ps, n, block, 1, &codes, &scales, 0, err, s);
   }
   if (algo == AGQ_AR_FUSED_P2P) return allreduce_p2p(c, codes, scales, n, block, err, s);
+  if (algo == AGQ_AR_PUSH_P2P) return allreduce_push(c, codes, scales, n, block, err, s);
   return allreduce_nccl(c, codes, scales, n, block, err, s);
 }
 

@@ -44,9 +44,9 @@ def main():
     for seed, n in enumerate([128, 1000, 8192 * 3 + 300, 8192 * 9 + 300, 77]):
         g = grads(world, n, seed)
         want_c, want_s = O.allreduce_decomposed([c for c, _ in g], [s for _, s in g])
-        for algo in ("nccl", "p2p"):
+        for algo in ("nccl", "p2p", "push"):
             c, s = g[rank]
-            if algo == "p2p":
+            if algo in ("p2p", "push"):
                 pc, ps = comm.p2p_buffers(n)
                 pc.copy_(torch.from_numpy(c))
                 ps.copy_(torch.from_numpy(s))
@@ -64,7 +64,7 @@ def main():
     # every rank (collective.hpp:278-281): block 0 (owned by rank 0) holds
     # 3e38 on every rank, so only rank 0's reduce overflows.
     if world > 1:
-        for algo in ("nccl", "p2p"):
+        for algo in ("nccl", "p2p", "push"):
             n = 8192 * 2
             g = grads(world, n, 99, big_rank=-1)
             c, s = g[rank]
@@ -72,7 +72,7 @@ def main():
             c = c.copy()
             s = s.copy()
             c[:128], s[0] = big_c, big_s[0]
-            if algo == "p2p":
+            if algo in ("p2p", "push"):
                 pc, ps = comm.p2p_buffers(n)
                 pc.copy_(torch.from_numpy(c))
                 ps.copy_(torch.from_numpy(s))

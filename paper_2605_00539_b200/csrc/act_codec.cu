@@ -105,6 +105,50 @@ __device__ __forceinline__ void encode_linear_bf16_fast(const uint4 (&ch)[4], fl
   }
 }
 
+// Same encode, written straight into the lane's PACK output words (32 codes,
+// LSB-first): the pair (lo, hi) becomes ((f2u(hi) << PACK) + f2u(lo) +
+// kOff * (1 + 2^PACK)) mod 2^32 = (k1 + L) << PACK | (k0 + L), since
+// f2u(magic + k) = kMagicBits + k and kMagicBits + kOff = L; pair K is then
+// added at bit 2*PACK*K (fields are disjoint, so add = or), which compiles
+// to one LEA per pair (+ one LEA.HI where a pair straddles two words)
+// instead of 64-bit chunk accumulators re-split into words.
+#ifndef AGQ_QUANT_WORDS
+#define AGQ_QUANT_WORDS 1
+#endif
+template <int PACK, int K>
+__device__ __forceinline__ void put_pair(uint32_t (&words)[PACK], uint32_t p) {
+  constexpr int o = 2 * PACK * K, w = o / 32, sh = o % 32;
+  words[w] += p << sh;
+  if constexpr (sh + 2 * PACK > 32) words[w + 1] += p >> (32 - sh);
+}
+template <int BITS, int PACK, int J = 0>
+__device__ __forceinline__ void encode_linear_bf16_words(const uint4 (&ch)[4], const f32x2& inv2,
+                                                         const f32x2& rcp2, const f32x2& na2,
+                                                         uint32_t (&words)[PACK]) {
+  constexpr int L = (1 << (BITS - 1)) - 1;
+  constexpr uint32_t kOff = (uint32_t)L - kMagicBits;
+  constexpr uint32_t kPairOff = kOff + (kOff << PACK);
+  const f32x2 L2 = pk2((float)L, (float)L), mg2 = pk2(kMagicRound, kMagicRound);
+  const uint32_t wv[4] = {ch[J].x, ch[J].y, ch[J].z, ch[J].w};
+  uint32_t pr[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const f32x2 x = pk2(u2f(wv[k] << 16), u2f(wv[k] & 0xffff0000u));
+    const f32x2 v = mul2(x, inv2);
+    const f32x2 xl = mul2(x, L2);
+    const f32x2 r = fma2(v, na2, xl);
+    const f32x2 v2 = fma2(r, rcp2, v);
+    float lo, hi;
+    up2(add2(v2, mg2), lo, hi);
+    pr[k] = (f2u(hi) << PACK) + f2u(lo) + kPairOff;
+  }
+  put_pair<PACK, 4 * J + 0>(words, pr[0]);
+  put_pair<PACK, 4 * J + 1>(words, pr[1]);
+  put_pair<PACK, 4 * J + 2>(words, pr[2]);
+  put_pair<PACK, 4 * J + 3>(words, pr[3]);
+  if constexpr (J < 3) encode_linear_bf16_words<BITS, PACK, J + 1>(ch, inv2, rcp2, na2, words);
+}
+
 // PACK: bits per stored code (BITS for the packed stream, 8 for one byte per
 // element).
 template <int BITS, int PACK, int CODEC, typename Tin>
@@ -350,8 +394,15 @@ __device__ __forceinline__ void encode_row(const uint4 (&ch)[InTraits<Tin>::kChu
 #pragma unroll
     for (int j = 0; j < kChunks; ++j) pk[j] = zc;
   } else if (fast) {
-    if constexpr (CODEC == 0 && TR::kBf16) {
+    if constexpr (CODEC == 0 && TR::kBf16 && AGQ_QUANT_WORDS) {
       const float rcp = fdiv(1.0f, a);  // one division per block: inv = L * (1/a)
+      const float inv = fmul((float)L, rcp);
+#pragma unroll
+      for (int k = 0; k < PACK; ++k) words[k] = 0;
+      encode_linear_bf16_words<BITS, PACK>(ch, pk2(inv, inv), pk2(rcp, rcp), pk2(-a, -a), words);
+      return;
+    } else if constexpr (CODEC == 0 && TR::kBf16) {
+      const float rcp = fdiv(1.0f, a);
       encode_linear_bf16_fast<BITS, PACK>(ch, a, fmul((float)L, rcp), rcp, pk);
     } else {
       const float inv = codec_inv(CODEC, BITS, a);

@@ -680,17 +680,24 @@ __device__ __noinline__ float decode_slow(int codec, int bits, uint32_t c, float
 // the magic add (no I2F), p = c' s exact, then the Markstein-corrected
 // division by L (agq_numerics.cuh:dq_linear_bf16scale) on pairs. Linear codes
 // never produce -0, so the division needs no sign handling here.
+// The magic exponent bits in a register the optimiser cannot see through, so
+// mask-and-or of a code compiles to one LOP3 (x & mask) | R (a LOP3 takes one
+// immediate only).
+__constant__ uint32_t c_magic_bits = kMagicBits;
+__device__ __forceinline__ uint32_t opaque_magic() { return c_magic_bits; }
+
 template <int BITS, int PACK, int NPER>
 __device__ __forceinline__ void decode_linear_fast(uint64_t bits, float s, float (&v)[NPER]) {
   constexpr int L = (1 << (BITS - 1)) - 1;
   const f32x2 s2 = pk2(s, s);
   const f32x2 off2 = pk2(-(kMagicRound + (float)L), -(kMagicRound + (float)L));
   const f32x2 den2 = pk2(-(float)L, -(float)L), rden2 = pk2(1.0f / L, 1.0f / L);
+  const uint32_t mb = opaque_magic();
 #pragma unroll
   for (int e = 0; e < NPER; e += 2) {
     const uint32_t c0 = (uint32_t)(bits >> (e * PACK)) & ((1u << BITS) - 1u);
     const uint32_t c1 = (uint32_t)(bits >> ((e + 1) * PACK)) & ((1u << BITS) - 1u);
-    const f32x2 cp = add2(pk2(u2f(kMagicBits | c0), u2f(kMagicBits | c1)), off2);
+    const f32x2 cp = add2(pk2(u2f(mb | c0), u2f(mb | c1)), off2);
     const f32x2 p = mul2(cp, s2);
     const f32x2 q0 = mul2(p, rden2);
     const f32x2 r = fma2(q0, den2, p);

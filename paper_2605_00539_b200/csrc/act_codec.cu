@@ -377,6 +377,14 @@ __device__ __forceinline__ TileRef locate(const SegTable& st, uint64_t t) {
   return {g, t - st.tile_begin[g]};
 }
 
+// Incremental locate for a warp whose tiles only move forward (t += grid
+// warps): advance the segment while the tile is past its end — one compare
+// per tile in the common case instead of a select chain over every segment.
+__device__ __forceinline__ TileRef locate_from(const SegTable& st, uint64_t t, int& g) {
+  while (g + 1 < st.nseg && t >= st.tile_begin[g + 1]) ++g;
+  return {g, t - st.tile_begin[g]};
+}
+
 template <int BITS, int PACK, int CODEC, typename Tin>
 __device__ __forceinline__ void encode_row(const uint4 (&ch)[InTraits<Tin>::kChunks], float a,
                                            bool zero, bool fast, uint32_t (&words)[PACK]) {
@@ -465,8 +473,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tin) == 2 ? AGQ_QUAN
   };
   uint4 buf[kChunks];
   TileRef cur{0, 0};
+  int gseg = 0;
   if (t < total) {
-    cur = locate(st, t);
+    cur = locate_from(st, t, gseg);
     load(cur, buf);
   }
   for (; t < total; t += nw) {
@@ -475,7 +484,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tin) == 2 ? AGQ_QUAN
     __syncwarp();
     const TileRef tr = cur;
     if (t + nw < total) {
-      cur = locate(st, t + nw);
+      cur = locate_from(st, t + nw, gseg);
       load(cur, buf);
     }
     uint4 ch[kChunks];
@@ -705,6 +714,39 @@ __device__ __forceinline__ void decode_linear_fast(uint64_t bits, float s, float
   }
 }
 
+// Code e (LSB-first, PACK bits) of a lane row held in PACK 32-bit words;
+// with e a compile-time constant after unrolling this is one SHF (or one
+// funnel shift where the code straddles two words). High bits are garbage:
+// callers mask.
+template <int PACK>
+__device__ __forceinline__ uint32_t code_at(const uint32_t (&w)[PACK], int e) {
+  const int o = e * PACK, wi = o >> 5, sh = o & 31;
+  if (sh == 0) return w[wi];
+  if (sh + PACK > 32) return __funnelshift_r(w[wi], w[wi + 1], sh);
+  return w[wi] >> sh;
+}
+// decode_linear_fast for elements [e0, e0 + NPER) straight from the words
+template <int BITS, int PACK, int NPER>
+__device__ __forceinline__ void decode_linear_words(const uint32_t (&w)[PACK], int e0, float s,
+                                                    float (&v)[NPER]) {
+  constexpr int L = (1 << (BITS - 1)) - 1;
+  constexpr uint32_t kMask = (1u << BITS) - 1u;
+  const f32x2 s2 = pk2(s, s);
+  const f32x2 off2 = pk2(-(kMagicRound + (float)L), -(kMagicRound + (float)L));
+  const f32x2 den2 = pk2(-(float)L, -(float)L), rden2 = pk2(1.0f / L, 1.0f / L);
+  const uint32_t mb = opaque_magic();
+#pragma unroll
+  for (int e = 0; e < NPER; e += 2) {
+    const uint32_t c0 = (code_at<PACK>(w, e0 + e) & kMask) | mb;
+    const uint32_t c1 = (code_at<PACK>(w, e0 + e + 1) & kMask) | mb;
+    const f32x2 cp = add2(pk2(u2f(c0), u2f(c1)), off2);
+    const f32x2 p = mul2(cp, s2);
+    const f32x2 q0 = mul2(p, rden2);
+    const f32x2 r = fma2(q0, den2, p);
+    up2(fma2(r, rden2, q0), v[e], v[e + 1]);
+  }
+}
+
 // round-to-nearest-even to bf16 with the reference's integer rule
 // (collective.hpp:101-110; identical to cvt.rn for non-NaN values, and keeps
 // the quiet-NaN payload the reference produces).
@@ -907,8 +949,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? AGQ_DEQ
   uint32_t words[PACK];
   float sc = 0.f;
   TileRef cur{0, 0};
+  int gseg = 0;
   if (t < total) {
-    cur = locate(st, t);
+    cur = locate_from(st, t, gseg);
     load(cur, words, sc);
   }
   for (; t < total; t += nw) {
@@ -918,7 +961,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? AGQ_DEQ
     const float s = sc;
     const TileRef tr = cur;
     if (t + nw < total) {
-      cur = locate(st, t + nw);
+      cur = locate_from(st, t + nw, gseg);
       load(cur, words, sc);
     }
     if (validate) {
@@ -948,7 +991,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? AGQ_DEQ
     for (int j = 0; j < kChunks; ++j) {
       float v[kPerChunk];
       if (CODEC == 0 && fast) {
-        decode_linear_fast<BITS, PACK, kPerChunk>(pk[j], s, v);
+        decode_linear_words<BITS, PACK, kPerChunk>(cw, j * kPerChunk, s, v);
       } else if (fast) {
 #pragma unroll
         for (int e = 0; e < kPerChunk; ++e) {

@@ -378,11 +378,26 @@ __device__ __forceinline__ TileRef locate(const SegTable& st, uint64_t t) {
 }
 
 // Incremental locate for a warp whose tiles only move forward (t += grid
-// warps): advance the segment while the tile is past its end — one compare
-// per tile in the common case instead of a select chain over every segment.
-__device__ __forceinline__ TileRef locate_from(const SegTable& st, uint64_t t, int& g) {
-  while (g + 1 < st.nseg && t >= st.tile_begin[g + 1]) ++g;
-  return {g, t - st.tile_begin[g]};
+// warps): the current segment's [begin, end) tile range lives in registers,
+// so a tile costs one compare (no parameter-bank load in front of the
+// prefetch address) and the table is read only when crossing a boundary —
+// instead of a select chain over every segment per tile.
+struct SegCursor {
+  int g = 0;
+  uint64_t begin = 0, end = 0;
+};
+__device__ __forceinline__ TileRef locate_from(const SegTable& st, uint64_t t, SegCursor& c) {
+  if (c.end == 0) {  // first tile of this warp
+    c.g = seg_of(st, t);
+    c.begin = st.tile_begin[c.g];
+    c.end = st.tile_begin[c.g + 1];
+  }
+  while (t >= c.end) {
+    ++c.g;
+    c.begin = c.end;
+    c.end = st.tile_begin[c.g + 1];
+  }
+  return {c.g, t - c.begin};
 }
 
 template <int BITS, int PACK, int CODEC, typename Tin>
@@ -473,7 +488,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tin) == 2 ? AGQ_QUAN
   };
   uint4 buf[kChunks];
   TileRef cur{0, 0};
-  int gseg = 0;
+  SegCursor gseg;
   if (t < total) {
     cur = locate_from(st, t, gseg);
     load(cur, buf);
@@ -949,7 +964,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? AGQ_DEQ
   uint32_t words[PACK];
   float sc = 0.f;
   TileRef cur{0, 0};
-  int gseg = 0;
+  SegCursor gseg;
   if (t < total) {
     cur = locate_from(st, t, gseg);
     load(cur, words, sc);

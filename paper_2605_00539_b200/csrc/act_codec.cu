@@ -377,6 +377,9 @@ __device__ __forceinline__ TileRef locate(const SegTable& st, uint64_t t) {
   return {g, t - st.tile_begin[g]};
 }
 
+#ifndef AGQ_DQ_PREFETCH
+#define AGQ_DQ_PREFETCH 2
+#endif
 // Incremental locate for a warp whose tiles only move forward (t += grid
 // warps): the current segment's [begin, end) tile range lives in registers,
 // so a tile costs one compare (no parameter-bank load in front of the
@@ -961,23 +964,39 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? AGQ_DEQ
     }
     sc = __ldg(st.scales[tr.g] + tr.lt * 8 + (lane >> 2));
   };
-  uint32_t words[PACK];
-  float sc = 0.f;
-  TileRef cur{0, 0};
+  // AGQ_DQ_PREFETCH tiles in flight per warp (codes + scale are <= 9
+  // registers per tile, so a second tile in flight is cheap and covers the
+  // load latency the kernel otherwise stalls on)
+  constexpr int kPf = AGQ_DQ_PREFETCH;
+  uint32_t words[kPf][PACK];
+  float scq[kPf];
+  TileRef curq[kPf];
   SegCursor gseg;
-  if (t < total) {
-    cur = locate_from(st, t, gseg);
-    load(cur, words, sc);
+#pragma unroll
+  for (int d = 0; d < kPf; ++d) {
+    scq[d] = 0.f;
+    curq[d] = TileRef{0, 0};
+    if (t + d * nw < total) {
+      curq[d] = locate_from(st, t + d * nw, gseg);
+      load(curq[d], words[d], scq[d]);
+    }
   }
   for (; t < total; t += nw) {
     uint32_t cw[PACK];
 #pragma unroll
-    for (int k = 0; k < PACK; ++k) cw[k] = words[k];
-    const float s = sc;
-    const TileRef tr = cur;
-    if (t + nw < total) {
-      cur = locate_from(st, t + nw, gseg);
-      load(cur, words, sc);
+    for (int k = 0; k < PACK; ++k) cw[k] = words[0][k];
+    const float s = scq[0];
+    const TileRef tr = curq[0];
+#pragma unroll
+    for (int d = 0; d + 1 < kPf; ++d) {  // shift the queue (register renames)
+#pragma unroll
+      for (int k = 0; k < PACK; ++k) words[d][k] = words[d + 1][k];
+      scq[d] = scq[d + 1];
+      curq[d] = curq[d + 1];
+    }
+    if (t + kPf * nw < total) {
+      curq[kPf - 1] = locate_from(st, t + kPf * nw, gseg);
+      load(curq[kPf - 1], words[kPf - 1], scq[kPf - 1]);
     }
     if (validate) {
       if ((!(s >= 0.0f) || !(s <= 3.402823466e38f)) && (lane & 3) == 0)

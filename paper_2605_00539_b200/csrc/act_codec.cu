@@ -470,6 +470,57 @@ __device__ __forceinline__ void encode_row(const uint4 (&ch)[InTraits<Tin>::kChu
   pack_chunks<kChunkBits>(words, pk, std::make_integer_sequence<int, kChunks>{});
 }
 
+// Per-tile compute of the warp-autonomous quantizer: lane row `ch` (32
+// consecutive elements, 4 lanes per 128-block) -> block absmax (2 shuffles),
+// packed codes straight to HBM, one scale per 4 lanes.
+template <int BITS, int PACK, int CODEC, typename Tin>
+__device__ __forceinline__ void quant_tile(const SegTable& st, agq_errors* err, const TileRef& tr,
+                                           int lane, const uint4 (&ch)[InTraits<Tin>::kChunks]) {
+  using TR = InTraits<Tin>;
+  constexpr int kChunks = TR::kChunks;
+  constexpr uint32_t kCodeB = kWarpElems * PACK / 8;
+  uint32_t m;
+  if constexpr (TR::kBf16) {
+    uint32_t mm = 0;
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) {
+      mm = __vmaxu2(mm, ch[j].x & 0x7fff7fffu);
+      mm = __vmaxu2(mm, ch[j].y & 0x7fff7fffu);
+      mm = __vmaxu2(mm, ch[j].z & 0x7fff7fffu);
+      mm = __vmaxu2(mm, ch[j].w & 0x7fff7fffu);
+    }
+    m = max(mm & 0xffffu, mm >> 16) << 16;
+  } else {
+    m = 0;
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) {
+      m = max(m, ch[j].x & 0x7fffffffu);
+      m = max(m, ch[j].y & 0x7fffffffu);
+      m = max(m, ch[j].z & 0x7fffffffu);
+      m = max(m, ch[j].w & 0x7fffffffu);
+    }
+  }
+  m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
+  m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
+  const float a = u2f(m);
+  if (m >= 0x7f800000u && (lane & 3) == 0)
+    err_min(&err->nonfinite_block, (long long)(st.block_base[tr.g] + tr.lt * 8 + (lane >> 2)));
+  uint32_t words[PACK];
+  encode_row<BITS, PACK, CODEC, Tin>(ch, a, m == 0, fast_scale(a), words);
+  uint32_t* cdst = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(st.codes[tr.g]) +
+                                               tr.lt * kCodeB) + lane * PACK;
+  if constexpr (PACK % 4 == 0) {
+#pragma unroll
+    for (int k = 0; k < PACK / 4; ++k)
+      *reinterpret_cast<uint4*>(cdst + 4 * k) =
+          make_uint4(words[4 * k], words[4 * k + 1], words[4 * k + 2], words[4 * k + 3]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < PACK; ++k) cdst[k] = words[k];
+  }
+  if ((lane & 3) == 0) st.scales[tr.g][tr.lt * 8 + (lane >> 2)] = a;
+}
+
 template <int BITS, int PACK, int CODEC, typename Tin>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tin) == 2 ? AGQ_QUANT_MINB : 2)
     k_quant_warp(SegTable st, agq_errors* err) {
@@ -510,47 +561,58 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tin) == 2 ? AGQ_QUAN
     for (int j = 0; j < kChunks; ++j) ch[j] = lds128(wb + swz_off<kChunks>(lane, j));
     __syncwarp();
 
-    uint32_t m;
-    if constexpr (TR::kBf16) {
-      uint32_t mm = 0;
-#pragma unroll
-      for (int j = 0; j < kChunks; ++j) {
-        mm = __vmaxu2(mm, ch[j].x & 0x7fff7fffu);
-        mm = __vmaxu2(mm, ch[j].y & 0x7fff7fffu);
-        mm = __vmaxu2(mm, ch[j].z & 0x7fff7fffu);
-        mm = __vmaxu2(mm, ch[j].w & 0x7fff7fffu);
-      }
-      m = max(mm & 0xffffu, mm >> 16) << 16;
-    } else {
-      m = 0;
-#pragma unroll
-      for (int j = 0; j < kChunks; ++j) {
-        m = max(m, ch[j].x & 0x7fffffffu);
-        m = max(m, ch[j].y & 0x7fffffffu);
-        m = max(m, ch[j].z & 0x7fffffffu);
-        m = max(m, ch[j].w & 0x7fffffffu);
-      }
-    }
-    m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
-    m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
-    const float a = u2f(m);
-    if (m >= 0x7f800000u && (lane & 3) == 0)
-      err_min(&err->nonfinite_block, (long long)(st.block_base[tr.g] + tr.lt * 8 + (lane >> 2)));
-    uint32_t words[PACK];
-    encode_row<BITS, PACK, CODEC, Tin>(ch, a, m == 0, fast_scale(a), words);
-    uint32_t* cdst = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(st.codes[tr.g]) +
-                                                 tr.lt * kCodeB) + lane * PACK;
-    if constexpr (PACK % 4 == 0) {
-#pragma unroll
-      for (int k = 0; k < PACK / 4; ++k)
-        *reinterpret_cast<uint4*>(cdst + 4 * k) =
-            make_uint4(words[4 * k], words[4 * k + 1], words[4 * k + 2], words[4 * k + 3]);
-    } else {
-#pragma unroll
-      for (int k = 0; k < PACK; ++k) cdst[k] = words[k];
-    }
-    if ((lane & 3) == 0) st.scales[tr.g][tr.lt * 8 + (lane >> 2)] = a;
+    quant_tile<BITS, PACK, CODEC, Tin>(st, err, tr, lane, ch);
   }
+}
+
+// K1, cp.async ring variant (AGQ_ACT_KERNEL=cpa): each warp keeps
+// AGQ_CPA_STAGES tiles in flight with 16-byte cp.async copies written straight
+// into its swizzled shared slots (no register staging, no STS), waits for the
+// oldest group, reads its row conflict-free and refills the slot.
+#ifndef AGQ_CPA_STAGES
+#define AGQ_CPA_STAGES 3
+#endif
+template <int BITS, int PACK, int CODEC, typename Tin>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tin) == 2 ? AGQ_QUANT_MINB : 2)
+    k_quant_cpa(SegTable st, agq_errors* err) {
+  using TR = InTraits<Tin>;
+  constexpr int kChunks = TR::kChunks;
+  constexpr int kStg = AGQ_CPA_STAGES;
+  constexpr uint32_t kTileB = kWarpElems * sizeof(Tin);
+  extern __shared__ __align__(128) unsigned char dsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wb = dsm + warp * kStg * kTileB;
+  const uint64_t total = st.tile_begin[st.nseg];
+  const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
+  uint64_t t = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
+  SegCursor icur, pcur;
+  auto issue = [&](uint64_t tt, int slot) {
+    if (tt < total) {
+      const TileRef tr = locate_from(st, tt, icur);
+      const unsigned char* src = static_cast<const unsigned char*>(st.src[tr.g]) + tr.lt * kTileB;
+#pragma unroll
+      for (int j = 0; j < kChunks; ++j)
+        cp_async16(wb + slot * kTileB + swz_of_linear<kChunks>(j * 512 + lane * 16),
+                   src + j * 512 + lane * 16);
+    }
+    cp_async_commit();  // always: keeps the group count uniform
+  };
+#pragma unroll
+  for (int d = 0; d < kStg; ++d) issue(t + d * nw, d);
+  int slot = 0;
+  for (; t < total; t += nw) {
+    cp_async_wait<kStg - 1>();
+    __syncwarp();
+    const TileRef tr = locate_from(st, t, pcur);
+    uint4 ch[kChunks];
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) ch[j] = lds128(wb + slot * kTileB + swz_off<kChunks>(lane, j));
+    __syncwarp();
+    issue(t + kStg * nw, slot);
+    slot = slot + 1 == kStg ? 0 : slot + 1;
+    quant_tile<BITS, PACK, CODEC, Tin>(st, err, tr, lane, ch);
+  }
+  cp_async_wait<0>();
 }
 
 // K1, per-warp TMA ring variant (AGQ_ACT_KERNEL=wtma): each warp owns
@@ -1284,8 +1346,33 @@ agq_status launch_quant_wtma(const SegTable& st, agq_errors* err, cudaStream_t s
 }
 
 template <int BITS, int PACK, int CODEC, typename Tin>
+agq_status launch_quant_cpa(const SegTable& st, agq_errors* err, cudaStream_t s) {
+  auto k = k_quant_cpa<BITS, PACK, CODEC, Tin>;
+  const size_t smem = (size_t)kWarpsPerCta * AGQ_CPA_STAGES * kWarpElems * sizeof(Tin);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWarpsPerCta * 32, smem);
+  if (occ < 1) occ = 1;
+  const uint64_t tiles = st.tile_begin[st.nseg];
+  const uint64_t want = (tiles + kWarpsPerCta - 1) / kWarpsPerCta;
+  const uint64_t cap = (uint64_t)num_sms() * occ;
+  k<<<(int)(want < cap ? want : cap), kWarpsPerCta * 32, smem, s>>>(st, err);
+  count_launch();
+  return cuda_fail(cudaGetLastError(), "quantize: launch");
+}
+
+bool act_cpa() {
+  static const bool v = [] {
+    const char* e = getenv("AGQ_ACT_KERNEL");
+    return e && strcmp(e, "cpa") == 0;
+  }();
+  return v;
+}
+
+template <int BITS, int PACK, int CODEC, typename Tin>
 agq_status launch_quant_warp(const SegTable& st, agq_errors* err, cudaStream_t s) {
   if (act_wtma()) return launch_quant_wtma<BITS, PACK, CODEC, Tin>(st, err, s);
+  if (act_cpa()) return launch_quant_cpa<BITS, PACK, CODEC, Tin>(st, err, s);
   auto k = k_quant_warp<BITS, PACK, CODEC, Tin>;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWarpsPerCta * 32, 0);

@@ -104,6 +104,20 @@ __device__ __forceinline__ void sts128(void* p, uint4 v) {
                : "memory");
 }
 
+// Ampere-style 16-byte async copy global -> shared (LDGSTS), bypassing L1
+// and registers; completion tracked per thread with commit/wait groups.
+__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(g)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // 128-bit global load that does not allocate in L1 (streaming / peer data).
 __device__ __forceinline__ uint4 ldg128_stream(const void* p) {
   uint4 v;

@@ -380,6 +380,9 @@ __device__ __forceinline__ TileRef locate(const SegTable& st, uint64_t t) {
 #ifndef AGQ_DQ_PREFETCH
 #define AGQ_DQ_PREFETCH 2
 #endif
+#ifndef AGQ_Q_PREFETCH
+#define AGQ_Q_PREFETCH 1
+#endif
 // Incremental locate for a warp whose tiles only move forward (t += grid
 // warps): the current segment's [begin, end) tile range lives in registers,
 // so a tile costs one compare (no parameter-bank load in front of the
@@ -540,21 +543,32 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tin) == 2 ? AGQ_QUAN
 #pragma unroll
     for (int j = 0; j < kChunks; ++j) buf[j] = ldg128_stream(src + j * 512 + lane * 16);
   };
-  uint4 buf[kChunks];
-  TileRef cur{0, 0};
+  constexpr int kPf = AGQ_Q_PREFETCH;  // tiles in flight per warp (registers)
+  uint4 buf[kPf][kChunks];
+  TileRef curq[kPf];
   SegCursor gseg;
-  if (t < total) {
-    cur = locate_from(st, t, gseg);
-    load(cur, buf);
+#pragma unroll
+  for (int d = 0; d < kPf; ++d) {
+    curq[d] = TileRef{0, 0};
+    if (t + d * nw < total) {
+      curq[d] = locate_from(st, t + d * nw, gseg);
+      load(curq[d], buf[d]);
+    }
   }
   for (; t < total; t += nw) {
 #pragma unroll
-    for (int j = 0; j < kChunks; ++j) sts128(wb + swz_of_linear<kChunks>(j * 512 + lane * 16), buf[j]);
+    for (int j = 0; j < kChunks; ++j) sts128(wb + swz_of_linear<kChunks>(j * 512 + lane * 16), buf[0][j]);
     __syncwarp();
-    const TileRef tr = cur;
-    if (t + nw < total) {
-      cur = locate_from(st, t + nw, gseg);
-      load(cur, buf);
+    const TileRef tr = curq[0];
+#pragma unroll
+    for (int d = 0; d + 1 < kPf; ++d) {
+#pragma unroll
+      for (int j = 0; j < kChunks; ++j) buf[d][j] = buf[d + 1][j];
+      curq[d] = curq[d + 1];
+    }
+    if (t + kPf * nw < total) {
+      curq[kPf - 1] = locate_from(st, t + kPf * nw, gseg);
+      load(curq[kPf - 1], buf[kPf - 1]);
     }
     uint4 ch[kChunks];
 #pragma unroll

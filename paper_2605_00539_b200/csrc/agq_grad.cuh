@@ -161,87 +161,62 @@ __device__ __forceinline__ void dq_accum(const uint32_t (&w)[N / 4], float sc, c
 // split (an E4M3 midpoint within ~2^-20 relative of y) are recomputed with
 // the exact comparison fp8_code. Subnormal E4M3 and saturation need no
 // special case: RNE with satfinite is monotone over the whole range.
-__device__ __forceinline__ void fp8_requant16(const float (&v)[16], float a, uint32_t (&w)[4]) {
+template <int NW>  // NW code words = 4 * NW values
+__device__ __forceinline__ void fp8_requant_words(const float (&v)[4 * NW], float a,
+                                                  uint32_t (&w)[NW]) {
   if (a == 0.0f) {
-    w[0] = w[1] = w[2] = w[3] = 0u;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) w[k] = 0u;
     return;
   }
   if (fast_scale(a)) {
     const float inv = fdiv(448.0f, a);
     const float ip = fmul(inv, 1.0f + 0x1p-21f), im = fmul(inv, 1.0f - 0x1p-21f);
     const f32x2 ip2 = pk2(ip, ip), im2 = pk2(im, im);
-    uint32_t split = 0;
+    uint32_t wm[NW];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < 2 * NW; ++k) {
       const f32x2 x = pk2(v[2 * k], v[2 * k + 1]);
       float p0, p1, m0, m1;
       up2(mul2(x, ip2), p0, p1);
       up2(mul2(x, im2), m0, m1);
       const uint32_t cp = cvt_e4m3x2(p0, p1), cm = cvt_e4m3x2(m0, m1);
-      split |= (uint32_t)(cp != cm) << k;
-      if (k & 1)
+      if (k & 1) {
         w[k >> 1] |= cp << 16;
-      else
+        wm[k >> 1] |= cm << 16;
+      } else {
         w[k >> 1] = cp;
+        wm[k >> 1] = cm;
+      }
     }
-    if (split) {
-      for (int k = 0; k < 8; ++k)
-        if (split >> k & 1) {
+    // one word-level test; pairs whose brackets split are recomputed exactly
+    uint32_t diff = 0;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) diff |= w[k] ^ wm[k];
+    if (diff) {
+      for (int k = 0; k < 2 * NW; ++k) {
+        const int sh = (k & 1) * 16;
+        if (((w[k >> 1] ^ wm[k >> 1]) >> sh) & 0xffffu) {
           const uint32_t c2 = fp8_code(v[2 * k], a, inv) | (fp8_code(v[2 * k + 1], a, inv) << 8);
-          const int sh = (k & 1) * 16;
           w[k >> 1] = (w[k >> 1] & ~(0xffffu << sh)) | (c2 << sh);
         }
+      }
     }
   } else {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < NW; ++k) {
       w[k] = 0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) w[k] |= encode_double(2, 8, v[4 * k + e], a) << (8 * e);
     }
   }
 }
-
-// 8-value variant (16 lanes per 128-block): bracketed E4M3 requant.
+__device__ __forceinline__ void fp8_requant16(const float (&v)[16], float a, uint32_t (&w)[4]) {
+  fp8_requant_words<4>(v, a, w);
+}
+// 8-value variant (16 lanes per 128-block).
 __device__ __forceinline__ void fp8_requant8(const float (&v)[8], float a, uint32_t (&w)[2]) {
-  if (a == 0.0f) {
-    w[0] = w[1] = 0u;
-    return;
-  }
-  if (fast_scale(a)) {
-    const float inv = fdiv(448.0f, a);
-    const float ip = fmul(inv, 1.0f + 0x1p-21f), im = fmul(inv, 1.0f - 0x1p-21f);
-    const f32x2 ip2 = pk2(ip, ip), im2 = pk2(im, im);
-    uint32_t split = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const f32x2 x = pk2(v[2 * k], v[2 * k + 1]);
-      float p0, p1, m0, m1;
-      up2(mul2(x, ip2), p0, p1);
-      up2(mul2(x, im2), m0, m1);
-      const uint32_t cp = cvt_e4m3x2(p0, p1), cm = cvt_e4m3x2(m0, m1);
-      split |= (uint32_t)(cp != cm) << k;
-      if (k & 1)
-        w[k >> 1] |= cp << 16;
-      else
-        w[k >> 1] = cp;
-    }
-    if (split) {
-      for (int k = 0; k < 4; ++k)
-        if (split >> k & 1) {
-          const uint32_t c2 = fp8_code(v[2 * k], a, inv) | (fp8_code(v[2 * k + 1], a, inv) << 8);
-          const int sh = (k & 1) * 16;
-          w[k >> 1] = (w[k >> 1] & ~(0xffffu << sh)) | (c2 << sh);
-        }
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      w[k] = 0;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) w[k] |= encode_double(2, 8, v[4 * k + e], a) << (8 * e);
-    }
-  }
+  fp8_requant_words<2>(v, a, w);
 }
 
 __device__ __forceinline__ uint32_t absmax_bits8(const float (&v)[8]) {

@@ -173,6 +173,32 @@ __device__ __forceinline__ uint32_t acc_swz(uint32_t row, uint32_t c) {
   return row * (kCh * 16) + ((c + rot) & (kCh - 1)) * 16;
 }
 
+// A non-finite block sum: a non-finite local gradient makes it so; tell the
+// two reference errors apart (collective.hpp:138-139 vs the requant's block
+// error) by re-reading this lane's local values from the warp's staging slot.
+template <bool BF16L>
+__device__ __noinline__ void acc_report_nonfinite(const unsigned char* wb, int lane, uint64_t t,
+                                                  uint64_t gblk, agq_errors* err) {
+  constexpr int kCh = BF16L ? 2 : 4;
+  uint32_t lbad = 0;
+  for (int j = 0; j < kCh; ++j) {
+    const uint4 v = lds128(wb + acc_swz<kCh>(lane, j));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    for (int k = 0; k < 4; ++k) {
+      if constexpr (BF16L) {
+        const uint32_t lo = w[k] << 16, hi = w[k] & 0xffff0000u;
+        lbad |= (uint32_t)((lo & 0x7f800000u) == 0x7f800000u) << (8 * j + 2 * k);
+        lbad |= (uint32_t)((hi & 0x7f800000u) == 0x7f800000u) << (8 * j + 2 * k + 1);
+      } else {
+        lbad |= (uint32_t)((w[k] & 0x7f800000u) == 0x7f800000u) << (4 * j + k);
+      }
+    }
+  }
+  if (lbad)
+    err_min(&err->nonfinite_local, (long long)(t * kAccWarpElems + lane * 16 + (__ffs(lbad) - 1)));
+  if ((lane & 7) == 0) err_min(&err->nonfinite_block, (long long)gblk);
+}
+
 template <bool BF16L, int PREC>
 __global__ void __launch_bounds__(kAccWarps * 32, 3)
     k_accumulate_warp(const uint8_t* codes, const float* scales, const void* local,
@@ -246,21 +272,14 @@ __global__ void __launch_bounds__(kAccWarps * 32, 3)
         v[e] = apply_prec<PREC>(fadd(fp8_dq_lut(byte_of(cw[e >> 2], e & 3), sd, t16), l[e]));
     }
     const uint32_t m = absmax_bits16(v);
-    if (m >= 0x7f800000u) {
-      // a non-finite local gradient makes the sum non-finite: tell the two
-      // reference errors apart only on this (rare) path
-      uint32_t lbad = 0;
-#pragma unroll
-      for (int e = 0; e < 16; ++e) lbad |= (uint32_t)((f2u(l[e]) & 0x7f800000u) == 0x7f800000u) << e;
-      if (lbad)
-        err_min(&err->nonfinite_local, (long long)(t * kAccWarpElems + lane * 16 + (__ffs(lbad) - 1)));
-      if ((lane & 7) == 0) err_min(&err->nonfinite_block, (long long)gblk);
-    }
+    if (m >= 0x7f800000u)  // rare: kept out of line so it is not if-converted
+      acc_report_nonfinite<BF16L>(wb, lane, t, gblk, err);
     uint32_t ow[4];
     fp8_requant16(v, u2f(m), ow);
     *reinterpret_cast<uint4*>(out_codes + t * kAccWarpElems + lane * 16) =
         make_uint4(ow[0], ow[1], ow[2], ow[3]);
     if ((lane & 7) == 0) out_scales[gblk] = u2f(m);
+    __syncwarp();  // the staging slot may still be read by the rare path
   }
 }
 

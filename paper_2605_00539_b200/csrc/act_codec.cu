@@ -527,6 +527,8 @@ __device__ __forceinline__ void quant_tile(const SegTable& st, agq_errors* err, 
 template <int BITS, int PACK, int CODEC, typename Tin>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tin) == 2 ? AGQ_QUANT_MINB : 2)
     k_quant_warp(SegTable st, agq_errors* err) {
+  pdl_launch_dependents();
+  pdl_wait();  // the previous kernel's outputs (our inputs) are visible
   using TR = InTraits<Tin>;
   constexpr int kChunks = TR::kChunks;
   constexpr uint32_t kTileB = kWarpElems * sizeof(Tin);    // 2 KB / 4 KB
@@ -1008,6 +1010,8 @@ __global__ void __launch_bounds__(kThreads)
 template <int BITS, int PACK, int CODEC, typename Tout>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? AGQ_DEQUANT_MINB : 2)
     k_dequant_warp(SegTable st, int validate, agq_errors* err) {
+  pdl_launch_dependents();
+  pdl_wait();
   constexpr int kChunks = OutTraits<Tout>::kChunks;
   constexpr int kPerChunk = 32 / kChunks;
   constexpr int kChunkBits = kPerChunk * PACK;
@@ -1383,34 +1387,64 @@ bool act_cpa() {
   return v;
 }
 
+// Launch with programmatic stream serialization (PDL) unless AGQ_PDL=0: the
+// kernel's launch and prologue overlap the previous kernel's tail; the
+// kernels wait (griddepcontrol.wait) before touching global memory.
+bool act_pdl() {
+  static const bool v = [] {
+    const char* e = getenv("AGQ_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_maybe_pdl(void (*k)(KArgs...), int grid, int block, size_t smem,
+                             cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = act_pdl() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+// resident CTAs per SM of a kernel (queried once per instantiation)
+template <typename K>
+int occupancy_of(K k, int block, size_t smem) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, block, smem);
+  return occ < 1 ? 1 : occ;
+}
+
 template <int BITS, int PACK, int CODEC, typename Tin>
 agq_status launch_quant_warp(const SegTable& st, agq_errors* err, cudaStream_t s) {
   if (act_wtma()) return launch_quant_wtma<BITS, PACK, CODEC, Tin>(st, err, s);
   if (act_cpa()) return launch_quant_cpa<BITS, PACK, CODEC, Tin>(st, err, s);
   auto k = k_quant_warp<BITS, PACK, CODEC, Tin>;
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWarpsPerCta * 32, 0);
-  if (occ < 1) occ = 1;
+  static const int occ = occupancy_of(k, kWarpsPerCta * 32, 0);
   const uint64_t tiles = st.tile_begin[st.nseg];
   const uint64_t want = (tiles + kWarpsPerCta - 1) / kWarpsPerCta;
   const uint64_t cap = (uint64_t)num_sms() * occ;
-  k<<<(int)(want < cap ? want : cap), kWarpsPerCta * 32, 0, s>>>(st, err);
+  cudaError_t e = launch_maybe_pdl(k, (int)(want < cap ? want : cap), kWarpsPerCta * 32, 0, s, st, err);
   count_launch();
-  return cuda_fail(cudaGetLastError(), "quantize: launch");
+  return cuda_fail(e != cudaSuccess ? e : cudaGetLastError(), "quantize: launch");
 }
 
 template <int BITS, int PACK, int CODEC, typename Tout>
 agq_status launch_dequant_warp(const SegTable& st, int validate, agq_errors* err, cudaStream_t s) {
   auto k = k_dequant_warp<BITS, PACK, CODEC, Tout>;
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kWarpsPerCta * 32, 0);
-  if (occ < 1) occ = 1;
+  static const int occ = occupancy_of(k, kWarpsPerCta * 32, 0);
   const uint64_t tiles = st.tile_begin[st.nseg];
   const uint64_t want = (tiles + kWarpsPerCta - 1) / kWarpsPerCta;
   const uint64_t cap = (uint64_t)num_sms() * occ;
-  k<<<(int)(want < cap ? want : cap), kWarpsPerCta * 32, 0, s>>>(st, validate, err);
+  cudaError_t e = launch_maybe_pdl(k, (int)(want < cap ? want : cap), kWarpsPerCta * 32, 0, s, st,
+                                   validate, err);
   count_launch();
-  return cuda_fail(cudaGetLastError(), "dequantize: launch");
+  return cuda_fail(e != cudaSuccess ? e : cudaGetLastError(), "dequantize: launch");
 }
 
 template <int PACK, typename Tin>

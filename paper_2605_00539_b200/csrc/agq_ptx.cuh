@@ -104,6 +104,15 @@ __device__ __forceinline__ void sts128(void* p, uint4 v) {
                : "memory");
 }
 
+// Programmatic dependent launch (launched with the programmatic stream
+// serialization attribute): let the next kernel in the stream start launching,
+// and wait until the previous one has completed and its memory is visible.
+// A kernel must call pdl_wait() before touching global memory.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Ampere-style 16-byte async copy global -> shared (LDGSTS), bypassing L1
 // and registers; completion tracked per thread with commit/wait groups.
 __device__ __forceinline__ void cp_async16(void* smem, const void* g) {

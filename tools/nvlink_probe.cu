@@ -7,6 +7,7 @@
 // Reports GB/s per GPU per direction (bytes crossing this GPU's links).
 #include <cuda_runtime.h>
 
+#include <cstdint>
 #include <cstdio>
 #include <vector>
 
@@ -59,6 +60,61 @@ __global__ void xfer(Ptrs src, Ptrs dst, int me, int P, size_t slice_vec, int mo
   }
 }
 
+// mode 4: pull with 1-D TMA bulk copies (cp.async.bulk global -> shared, one
+// mbarrier per stage, lane 0 of each warp keeps kSt stages of kChunk bytes in
+// flight per peer round-robin); the data is then stored to local HBM so the
+// traffic pattern matches "pull + local write".
+constexpr int kSt = 4, kChunk = 4096;
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__global__ void tma_pull(Ptrs src, Ptrs dst, int me, int P, size_t slice) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  unsigned char* ring = sm + warp * kSt * kChunk;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + nwarps * kSt * kChunk) + warp * kSt;
+  if (lane == 0)
+    for (int s = 0; s < kSt; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bars[s])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  const size_t per_peer = slice / kChunk;             // chunks per peer slice
+  const size_t total = per_peer * (P - 1);
+  const size_t gw = (size_t)blockIdx.x * nwarps + warp, nw = (size_t)gridDim.x * nwarps;
+  auto addr = [&](size_t c, const unsigned char*& s, unsigned char*& d) {
+    const int k = (int)(c % (P - 1)) + 1, peer = (me + k) % P;
+    const size_t off = (c / (P - 1)) * kChunk;
+    s = reinterpret_cast<const unsigned char*>(src.buf[peer]) + me * slice + off;
+    d = reinterpret_cast<unsigned char*>(dst.buf[me]) + peer * slice + off;
+  };
+  auto issue = [&](size_t c, int st) {
+    if (lane == 0 && c < total) {
+      const unsigned char* s; unsigned char* d; addr(c, s, d);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&bars[st])), "r"(kChunk) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(su32(ring + st * kChunk)), "l"(s), "r"(kChunk), "r"(su32(&bars[st])) : "memory");
+    }
+  };
+  size_t c = gw;
+  for (int st = 0; st < kSt; ++st) issue(c + st * nw, st);
+  uint32_t phase = 0;
+  int st = 0;
+  for (; c < total; c += nw) {
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done) : "r"(su32(&bars[st])), "r"((phase >> st) & 1u) : "memory");
+    phase ^= 1u << st;
+    const unsigned char* s; unsigned char* d; addr(c, s, d);
+    const uint4* r4 = reinterpret_cast<const uint4*>(ring + st * kChunk);
+    uint4* d4 = reinterpret_cast<uint4*>(d);
+    for (int i = lane; i < kChunk / 16; i += 32) d4[i] = r4[i];
+    __syncwarp();
+    issue(c + kSt * nw, st);
+    st = st + 1 == kSt ? 0 : st + 1;
+  }
+}
+
 int main(int argc, char** argv) {
   int P = 0;
   CK(cudaGetDeviceCount(&P));
@@ -80,7 +136,13 @@ int main(int argc, char** argv) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const char* names[] = {"pull (peer LDG)", "push (peer STG)", "pull+push"};
-  for (int mode = 0; mode < 4; ++mode) {
+  const int tma_warps = 8;
+  const size_t tma_smem = tma_warps * (kSt * kChunk + kSt * 8);
+  for (int g = 0; g < P; ++g) {
+    CK(cudaSetDevice(g));
+    CK(cudaFuncSetAttribute(tma_pull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tma_smem));
+  }
+  for (int mode = 0; mode < 5; ++mode) {
     for (int grid_mult : {1, 2, 4}) {
       if (mode == 3 && grid_mult > 1) break;
       std::vector<cudaEvent_t> a(P), b(P);
@@ -96,6 +158,8 @@ int main(int argc, char** argv) {
           cudaEventRecord(a[g], st[g]);
           if (mode < 3) {
             xfer<<<sms * grid_mult, 512, 0, st[g]>>>(src, dst, g, P, slice_vec, mode, 4);
+          } else if (mode == 4) {
+            tma_pull<<<sms * grid_mult, tma_warps * 32, tma_smem, st[g]>>>(src, dst, g, P, slice);
           } else {
             for (int k = 1; k < P; ++k) {
               const int peer = (g + k) % P;
@@ -116,8 +180,8 @@ int main(int argc, char** argv) {
         if (rep == 2) {
           const double per_dir = (mode == 2 ? 2.0 : 1.0) * (P - 1) * (double)slice;
           printf("P=%d %-16s grid=%3dxSM slice=%zuMB: %.3f ms, %.1f GB/s per GPU per direction\n",
-                 P, mode == 3 ? "copy engines" : names[mode], grid_mult, slice >> 20, worst,
-                 per_dir / (worst * 1e-3) / 1e9);
+                 P, mode == 3 ? "copy engines" : (mode == 4 ? "pull (TMA bulk)" : names[mode]),
+                 grid_mult, slice >> 20, worst, per_dir / (worst * 1e-3) / 1e9);
         }
       }
     }

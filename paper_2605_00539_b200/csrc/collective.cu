@@ -476,7 +476,10 @@ __global__ void __launch_bounds__(256) k_push_scatter(PushArgs a) {
 // that sender) and outputs = chunk [me] of every rank's buffer; built on the
 // host so it stays in the parameter bank.
 template <int NP>
-__global__ void __launch_bounds__(256) k_push_reduce(PushArgs a, PieceTable pt) {
+#ifndef AGQ_PUSH_MINB
+#define AGQ_PUSH_MINB 2  // 3 measured equal at 4 GPUs and spills the NP = 8 instance
+#endif
+__global__ void __launch_bounds__(256, AGQ_PUSH_MINB) k_push_reduce(PushArgs a, PieceTable pt) {
   __shared__ double lut[kDqTable];
   __shared__ float btab[8 * (NP > 0 ? NP : 1) * 32];
   __shared__ int ok;
@@ -866,8 +869,16 @@ agq_status allreduce_push(agq_comm* c, uint8_t* codes, float* scales, uint64_t n
   uint64_t gx = (maxlen / 16 + 1023) / 1024;
   const uint64_t cap_x = std::max<uint64_t>(1, (uint64_t)num_sms() * 2 / (P - 1));
   gx = std::min<uint64_t>(std::max<uint64_t>(gx, 1), cap_x);
+  // AGQ_PUSH_TIMING=1 (diagnostics only): per-phase device time on stderr
+  static const bool timing = getenv("AGQ_PUSH_TIMING") != nullptr;
+  cudaEvent_t ev[3];
+  if (timing) {
+    for (auto& e : ev) cudaEventCreate(&e);
+    cudaEventRecord(ev[0], s);
+  }
   k_push_scatter<<<dim3((unsigned)gx, (unsigned)(P - 1)), 256, 0, s>>>(a);
   count_launch();
+  if (timing) cudaEventRecord(ev[1], s);
   agq_status st = cuda_fail(cudaGetLastError(), "push all-reduce: scatter launch");
   if (st) return st;
   PieceTable pt{};
@@ -888,7 +899,7 @@ agq_status allreduce_push(agq_comm* c, uint8_t* codes, float* scales, uint64_t n
   }
   const uint64_t groups = (rg[2 * r + 1] - rg[2 * r] + kBlock - 1) / kBlock * 8;
   uint64_t grid = (groups + 255) / 256;
-  grid = std::min<uint64_t>(std::max<uint64_t>(grid, 1), (uint64_t)num_sms() * 2);
+  grid = std::min<uint64_t>(std::max<uint64_t>(grid, 1), (uint64_t)num_sms() * AGQ_PUSH_MINB);
   switch (P) {
     case 2: launch_push_reduce<2>(a, pt, (int)grid, s); break;
     case 3: launch_push_reduce<3>(a, pt, (int)grid, s); break;
@@ -902,6 +913,16 @@ agq_status allreduce_push(agq_comm* c, uint8_t* codes, float* scales, uint64_t n
   count_launch();
   st = cuda_fail(cudaGetLastError(), "push all-reduce: reduce launch");
   if (st) return st;
+  if (timing) {
+    cudaEventRecord(ev[2], s);
+    cudaEventSynchronize(ev[2]);
+    float t1 = 0, t2 = 0;
+    cudaEventElapsedTime(&t1, ev[0], ev[1]);
+    cudaEventElapsedTime(&t2, ev[1], ev[2]);
+    fprintf(stderr, "push all-reduce rank %d n=%llu: scatter %.3f ms, reduce+gather %.3f ms\n", r,
+            (unsigned long long)n, t1, t2);
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
   if (!inplace) {
     cudaMemcpyAsync(codes, sc_codes, n, cudaMemcpyDeviceToDevice, s);
     cudaMemcpyAsync(scales, sc_scales, nb * 4, cudaMemcpyDeviceToDevice, s);

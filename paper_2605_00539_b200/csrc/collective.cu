@@ -407,6 +407,162 @@ __global__ void __launch_bounds__(256, 2) k_fused_allreduce(FusedArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Fused all-reduce, TMA-pipelined variant (AGQ_P2P_TMA=1): the same pull /
+// reduce / push as k_fused_allreduce, but each warp keeps kStages warp tiles
+// (512 elements = 4 blocks) of every piece in flight with 1-D bulk copies
+// from the peers' buffers (lane 0 issues NP x (512 B codes + a 32 B aligned
+// window holding the tile's 4 scales) per stage, one mbarrier per stage), so
+// the NVLink pull latency overlaps the decode/reduce/requant of earlier
+// tiles instead of sitting in front of every group. The partial last tile
+// uses the per-thread path.
+// ---------------------------------------------------------------------------
+template <int NP>
+struct TmaCfg {
+  static constexpr int kStages = NP <= 4 ? 4 : 3;
+  static constexpr uint32_t kPiece = 512 + 32;
+  static constexpr uint32_t kStage = NP * kPiece;
+  static constexpr uint32_t kWarpBytes = kStages * kStage;
+  static constexpr size_t kSmem = 8 * (size_t)kWarpBytes;
+};
+
+// Decode + reduce (ascending piece order from +0.0f), requantize and store to
+// every rank one whole 16-element group whose codes/scales are in registers.
+template <int NP>
+__device__ __forceinline__ void reduce_store16(unsigned char* const (&bs)[NP], uint64_t coff,
+                                               uint64_t soff, uint64_t e0,
+                                               const uint32_t (&cw)[NP][4], const float (&sc)[NP],
+                                               long long blk_base, const double* t16,
+                                               agq_errors* err, float* wtab) {
+  const uint64_t blk = e0 / kBlock;
+  float acc[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) acc[e] = 0.0f;
+  uint32_t sbad = 0;
+  if (AGQ_RED_TAB) build_tables<NP, 8>(wtab, sc);
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    sbad |= !(sc[p] >= 0.0f) || !(sc[p] <= 3.402823466e38f);
+    if (AGQ_RED_TAB && dq_fast(sc[p]) && fp8_tab_ok16(cw[p]))
+      dq_tab_accum<4>(cw[p], tab_addr<8>(wtab, p), acc);
+    else
+      dq_accum<16>(cw[p], sc[p], t16, acc);
+  }
+  const uint32_t m = absmax_bits16(acc);
+  const int sub = threadIdx.x & 7;
+  if (sub == 0) {
+    if (sbad) err_min(&err->bad_scale_block, blk_base + (long long)blk);
+    if (m >= 0x7f800000u) err_min(&err->overflow_block, blk_base + (long long)blk);
+  }
+  const float a = u2f(m);
+  uint32_t ow[4];
+  if (m >= 0x7f800000u) {
+    ow[0] = ow[1] = ow[2] = ow[3] = 0;
+  } else {
+    fp8_requant16(acc, a, ow);
+  }
+#pragma unroll
+  for (int o = 0; o < NP; ++o) {
+    *reinterpret_cast<uint4*>(bs[o] + coff + e0) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+    if (sub == 0) reinterpret_cast<float*>(bs[o] + soff)[blk] = a;
+  }
+}
+
+template <int NP>
+__global__ void __launch_bounds__(256, 1) k_fused_tma(FusedArgs a) {
+  using C = TmaCfg<NP>;
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ double lut[kDqTable];
+  __shared__ float btab[8 * NP * 32];
+  __shared__ __align__(8) uint64_t bars[8 * C::kStages];
+  __shared__ int ok;
+  fill_fp8_dq_table(lut);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint64_t* my_flags = reinterpret_cast<uint64_t*>(a.base[a.rank]);
+  if (blockIdx.x == 0 && tid < a.P)
+    st_release_sys(reinterpret_cast<uint64_t*>(a.base[tid]) + kReadyOff + a.rank, a.epoch);
+  if (tid == 0) {
+    ok = 1;
+    for (int s = 0; s < a.P; ++s)
+      if (!wait_flag(my_flags + kReadyOff + s, a.epoch)) ok = 0;
+  }
+  __syncthreads();
+  if (!ok) {
+    if (tid == 0) err_min(&a.err->overflow_block, -1);
+    return;
+  }
+  // the peers' data was published to the generic proxy; the bulk copies
+  // below read it through the async proxy
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+
+  unsigned char* bs[NP];
+#pragma unroll
+  for (int s = 0; s < NP; ++s) bs[s] = a.base[s];
+  const uint64_t b0 = a.begin / kBlock;
+  const uint64_t coff = a.codes_off + a.begin, soff = a.scales_off + 4 * b0;
+  float* wtab = btab + warp * NP * 32;
+  unsigned char* ring = dsm + warp * C::kWarpBytes;
+  uint64_t* wb = bars + warp * C::kStages;
+  if (lane == 0) {
+    for (int s = 0; s < C::kStages; ++s) mbar_init(&wb[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  const uint64_t ntile = a.len / 512;
+  const uint64_t nw = (uint64_t)gridDim.x * 8;
+  const uint64_t gw = (uint64_t)blockIdx.x * 8 + warp;
+  const uint64_t policy = policy_evict_first();
+  auto issue = [&](uint64_t w, int s) {
+    if (lane == 0 && w < ntile) {
+      unsigned char* stg = ring + s * C::kStage;
+      mbar_arrive_expect_tx(&wb[s], C::kStage);
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        bulk_g2s(stg + p * C::kPiece, bs[p] + coff + w * 512, 512, &wb[s], policy);
+        const uint64_t sa = reinterpret_cast<uint64_t>(bs[p] + soff + 16 * w);
+        bulk_g2s(stg + p * C::kPiece + 512, reinterpret_cast<const void*>(sa & ~15ull), 32, &wb[s],
+                 policy);
+      }
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < C::kStages; ++s) issue(gw + s * nw, s);
+  uint32_t phase = 0;
+  int s = 0;
+  for (uint64_t w = gw; w < ntile; w += nw) {
+    mbar_wait(&wb[s], (phase >> s) & 1u);
+    phase ^= 1u << s;
+    const unsigned char* stg = ring + s * C::kStage;
+    // every rank's buffer has the same layout: the window offset is common
+    const int so = (int)(((a.scales_off + 4 * b0 + 16 * w) & 15u) >> 2) + (lane >> 3);
+    uint32_t cw[NP][4];
+    float sc[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const uint4 v = lds128(stg + p * C::kPiece + lane * 16);
+      cw[p][0] = v.x; cw[p][1] = v.y; cw[p][2] = v.z; cw[p][3] = v.w;
+      sc[p] = reinterpret_cast<const float*>(stg + p * C::kPiece + 512)[so];
+    }
+    __syncwarp();  // the stage is free again
+    issue(w + C::kStages * nw, s);
+    s = s + 1 == C::kStages ? 0 : s + 1;
+    reduce_store16<NP>(bs, coff, soff, w * 512 + lane * 16, cw, sc, (long long)b0, lut, a.err,
+                       wtab);
+  }
+  // the partial last tile: per-thread path (whole warps, tables)
+  const uint64_t nblocks = (a.len + kBlock - 1) / kBlock;
+  const uint64_t ngroups = nblocks * 8;
+  const uint64_t g0 = ntile * 32;
+  if (g0 < ngroups) {
+    const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
+    const uint64_t gpad = g0 + (ngroups - g0 + 31) / 32 * 32;
+    for (uint64_t g = g0 + blockIdx.x * (uint64_t)blockDim.x + tid; g < gpad; g += stride)
+      fused_group<NP>(bs, a.codes_off + a.begin, a.scales_off + 4 * b0, g, g < ngroups ? a.len : 0,
+                      (long long)b0, lut, a.err, wtab);
+  }
+  epoch_end(a);
+}
+
+// ---------------------------------------------------------------------------
 // Push all-reduce (AGQ_AR_PUSH_P2P): the same decomposition with every NVLink
 // transfer a fire-and-forget store (SM stores reach 690 GB/s per direction on
 // this NVSwitch, pulls 655, profiles/r01_nvlink_probe_n4.log) and no load on
@@ -755,8 +911,30 @@ int fused_ept(int P) {
   return forced == 8 ? 8 : 16;
 }
 
+bool fused_tma() {
+  static const bool v = [] {
+    const char* e = getenv("AGQ_P2P_TMA");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+template <int NP>
+void launch_fused_tma(const FusedArgs& a, cudaStream_t s) {
+  using C = TmaCfg<NP>;
+  static const int occ = [] {
+    cudaFuncSetAttribute(k_fused_tma<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)C::kSmem);
+    int o = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_fused_tma<NP>, 256, C::kSmem);
+    return o < 1 ? 1 : o;
+  }();
+  k_fused_tma<NP><<<num_sms() * occ, 256, C::kSmem, s>>>(a);
+}
 template <int NP>
 void launch_fused(const FusedArgs& a, int grid, cudaStream_t s) {
+  if constexpr (NP > 0) {
+    if (fused_tma()) return launch_fused_tma<NP>(a, s);
+  }
   if (fused_ept(a.P) == 8)
     k_fused_allreduce<NP, 8><<<grid, 256, 0, s>>>(a);
   else

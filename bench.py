@@ -60,6 +60,9 @@ def act_bytes_per_elem(bits):
     return q, q  # quant, dequant (bf16 in / bf16 out)
 
 
+NVLINK_GBS = 900.0  # NVLink 5 per direction per GPU (nominal)
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -521,7 +524,8 @@ def bench_allreduce(dev, args, world, rank, n):
             print(f"rank {rank}: allreduce {algo} failed: {ex}", file=sys.stderr, flush=True)
             continue
         res[algo] = {"ms": round(sec * 1e3, 3), "bus_GBs_wire": round(fac * wire / sec / 1e9, 1),
-                     "bus_GBs_bf16_equiv": round(fac * 2 * n / sec / 1e9, 1)}
+                     "bus_GBs_bf16_equiv": round(fac * 2 * n / sec / 1e9, 1),
+                     "frac_of_nvlink_900": round(fac * wire / sec / 1e9 / NVLINK_GBS, 4)}
         if algo in ("p2p", "push") and "ms" in res.get("nccl", {}):
             ok = torch.equal(qq.codes, q.codes) and torch.equal(qq.scales, q.scales)
             res[algo + "_equals_nccl"] = bool(ok)
@@ -535,7 +539,8 @@ def bench_allreduce(dev, args, world, rank, n):
     def bf16():
         L.check(L.lib.agq_allreduce_bf16_nccl(comm._h, gb.data_ptr(), n, sp))
     sec = timed(bf16, lambda: None)
-    res["bf16_nccl"] = {"ms": round(sec * 1e3, 3), "bus_GBs": round(fac * 2 * n / sec / 1e9, 1)}
+    res["bf16_nccl"] = {"ms": round(sec * 1e3, 3), "bus_GBs": round(fac * 2 * n / sec / 1e9, 1),
+                        "frac_of_nvlink_900": round(fac * 2 * n / sec / 1e9 / NVLINK_GBS, 4)}
     done = [res[a]["ms"] for a in args.algos if "ms" in res[a]]
     if done:
         res["speedup_vs_bf16_nccl"] = round(res["bf16_nccl"]["ms"] / min(done), 3)
@@ -790,7 +795,8 @@ def main():
         if q_time >= d_time else ("k_dequant_warp", d_gbs, {"k_quant_warp_GBs": round(q_gbs, 1)})
     traffic = load_traffic().get(dom_name)
     roofline = {"bound": "hbm", "achieved": round(dom_gbs, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(dom_gbs / peak, 4), "traffic": traffic, "kernel": dom_name,
+                "frac": round(dom_gbs / peak, 4), "frac_of_nominal_8tbs": round(dom_gbs / 8000.0, 4),
+                "traffic": traffic, "kernel": dom_name,
                 "peak_kind": peak_kind, **other}
     line = {"metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,

@@ -65,7 +65,7 @@ __device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) {
 // the multi-piece reduce kernels are shared-memory bound and use the block
 // table (profiles/r01_acc_tab_ab.log, r01_reduce_tab_ab.log).
 #ifndef AGQ_ACC_TAB
-#define AGQ_ACC_TAB 0
+#define AGQ_ACC_TAB 1
 #endif
 #ifndef AGQ_RED_TAB
 #define AGQ_RED_TAB 1

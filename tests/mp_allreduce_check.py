@@ -31,6 +31,23 @@ def grads(world, n, seed, big_rank=-1):
     return out
 
 
+VALID = np.array([c for c in range(256) if (c & 0x7F) != 0x7F], np.uint8)
+SCALES = np.array([0.0, 2.0 ** -60, 2.0 ** 60, 2.0 ** -61, 2.0 ** 61, 1e-40, 1e-30, 1e30, 1e37,
+                   3.0, 0.125], np.float32)
+
+
+def every_code_grads(world, nblk, seed):
+    """Every non-NaN E4M3 code per block, block scales on both sides of the
+    block-table decode's fast range: the fused kernels' table and fallback
+    paths on real ranks."""
+    out = []
+    for r in range(world):
+        rng = np.random.default_rng(seed * 100 + r)
+        c = np.concatenate([rng.permutation(VALID)[:128] for _ in range(nblk)])
+        out.append((c, rng.choice(SCALES, nblk).astype(np.float32)))
+    return out
+
+
 def main():
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -41,8 +58,10 @@ def main():
     cap = 8192 * 9 + 300
     comm.enable_p2p(cap)
     fails = 0
-    for seed, n in enumerate([128, 1000, 8192 * 3 + 300, 8192 * 9 + 300, 77]):
-        g = grads(world, n, seed)
+    cases = [(seed, n, None) for seed, n in enumerate([128, 1000, 8192 * 3 + 300, 8192 * 9 + 300, 77])]
+    cases.append((50, 128 * 160, "every_code"))
+    for seed, n, kind in cases:
+        g = every_code_grads(world, n // 128, seed) if kind else grads(world, n, seed)
         want_c, want_s = O.allreduce_decomposed([c for c, _ in g], [s for _, s in g])
         for algo in ("nccl", "p2p", "push"):
             c, s = g[rank]

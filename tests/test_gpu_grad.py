@@ -250,3 +250,57 @@ def test_accumulate_encoder_exhaustive_bf16_domain(cuda):
     bad = np.nonzero(out.codes.cpu().numpy() != c)[0]
     assert bad.size == 0, (bad[:5], x[bad[:5]])
     assert np.array_equal(u32(out.scales.cpu().numpy()), u32(s))
+
+
+# Every non-NaN E4M3 code in every block, with block scales on both sides of
+# the block-table decode's fast range [2^-60, 2^60] (0, subnormal, the
+# boundaries, huge): exercises the per-block table path and every fallback
+# (zero/subnormal codes, extreme scales) of K3 and K4 against the oracle.
+_VALID = np.array([c for c in range(256) if (c & 0x7F) != 0x7F], np.uint8)
+_SCALES = np.array([0.0, 2.0 ** -60, 2.0 ** 60, 2.0 ** -61, 2.0 ** 61, 1e-40, 1e-30, 1e30, 1e37,
+                    3.0, 0.125, 1.7e-5], np.float32)
+
+
+def _all_code_blocks(rng, nblk):
+    codes = np.concatenate([rng.permutation(_VALID)[:128] for _ in range(nblk)])
+    scales = rng.choice(_SCALES, nblk).astype(np.float32)
+    normal = rng.random(nblk) < 0.5
+    scales[normal] = np.abs(rng.standard_normal(normal.sum())).astype(np.float32) * 10.0 ** rng.uniform(
+        -8, 8, normal.sum()).astype(np.float32)
+    return codes, scales
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_reduce_every_code_and_extreme_scales(cuda, world):
+    rng = np.random.default_rng(100 + world)
+    pieces = [_all_code_blocks(rng, 64) for _ in range(world)]
+    oc, os_ = O.allreduce_decomposed([c for c, _ in pieces], [s for _, s in pieces])
+    same(A.allreduce_simulated([fp8q(c, s, cuda) for c, s in pieces]), oc, os_)
+
+
+def test_accumulate_every_code_and_extreme_scales(cuda):
+    rng = np.random.default_rng(5)
+    codes, scales = _all_code_blocks(rng, 64)
+    local = (rng.standard_normal(codes.size) *
+             np.repeat(10.0 ** rng.uniform(-30, 30, 64), 128)).astype(np.float32)
+    local[rng.random(codes.size) < 0.05] = 0.0
+    oc, os_ = O.local_accumulate(codes, scales, local)
+    same(A.local_accumulate(fp8q(codes, scales, cuda), t(local, cuda)), oc, os_)
+
+
+def test_nan_codes_abort_like_the_reference(cuda):
+    rng = np.random.default_rng(9)
+    codes, scales = _all_code_blocks(rng, 8)
+    scales[:] = 1.0
+    codes[300] = 0x7F  # NaN code in block 2
+    with pytest.raises(O.OracleError) as ref:
+        O.allreduce_decomposed([codes, codes], [scales, scales])
+    with pytest.raises(A.ProtocolError) as got:
+        A.allreduce_simulated([fp8q(codes, scales, cuda)] * 2)
+    assert str(got.value) == ref.value.args[-1]
+    local = np.zeros(codes.size, np.float32)
+    with pytest.raises(O.OracleError) as ref:
+        O.local_accumulate(codes, scales, local)
+    with pytest.raises(A.InvalidArgument) as got:
+        A.local_accumulate(fp8q(codes, scales, cuda), t(local, cuda))
+    assert str(got.value) == ref.value.args[-1]

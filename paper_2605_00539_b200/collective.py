@@ -83,11 +83,26 @@ class Communicator:
         scales = torch.as_tensor(_CudaArray(s.value, nb, "<f4"), device=f"cuda:{self.device}")
         return codes, scales
 
-    def allreduce_fp8(self, q: QuantizedTensor, algo: str = "nccl", stream=None,
+    def _in_p2p_buffers(self, q: QuantizedTensor) -> bool:
+        if not self.p2p_capacity or q.num_elements() > self.p2p_capacity or q.block_size != 128:
+            return False
+        c = C.c_void_p()
+        sc = C.c_void_p()
+        L.check(L.lib.agq_comm_p2p_buffers(self._h, C.byref(c), C.byref(sc)))
+        return q.codes.data_ptr() == c.value and q.scales.data_ptr() == sc.value
+
+    def allreduce_fp8(self, q: QuantizedTensor, algo: str = "auto", stream=None,
                       check: bool = True, errors: ErrorRecord | None = None) -> QuantizedTensor:
-        """In place on this rank's FP8 gradient (one byte per code)."""
+        """In place on this rank's FP8 gradient (one byte per code).
+
+        algo: "nccl" (grouped send/recv + reduce kernel), "p2p" (one fused
+        NVLink kernel), "push" (store-only NVLink variant), or "auto": the
+        fused kernel when the gradient already lives in this communicator's
+        symmetric buffers (p2p_buffers), otherwise NCCL — all bit-identical."""
         if q.codec_kind != CodecKind.Fp8E4M3:
             raise L.InvalidArgument("worker gradients are FP8 E4M3 tensors")
+        if algo == "auto":
+            algo = "p2p" if self._in_p2p_buffers(q) else "nccl"
         err = errors if errors is not None else ErrorRecord(q.codes.device)
         err.reset(stream)
         L.check(L.lib.agq_allreduce_fp8(self._h, q.codes.data_ptr(), q.scales.data_ptr(),

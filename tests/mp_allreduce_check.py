@@ -63,9 +63,9 @@ def main():
     for seed, n, kind in cases:
         g = every_code_grads(world, n // 128, seed) if kind else grads(world, n, seed)
         want_c, want_s = O.allreduce_decomposed([c for c, _ in g], [s for _, s in g])
-        for algo in ("nccl", "p2p", "push"):
+        for algo in ("nccl", "p2p", "push", "auto"):
             c, s = g[rank]
-            if algo in ("p2p", "push"):
+            if algo in ("p2p", "push", "auto"):
                 pc, ps = comm.p2p_buffers(n)
                 pc.copy_(torch.from_numpy(c))
                 ps.copy_(torch.from_numpy(s))

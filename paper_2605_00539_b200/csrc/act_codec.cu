@@ -21,6 +21,7 @@
 #include <utility>
 
 #include "agq_common.cuh"
+#include "agq_minifloat.cuh"
 
 namespace agqk {
 
@@ -380,6 +381,9 @@ __device__ __forceinline__ TileRef locate(const SegTable& st, uint64_t t) {
 #ifndef AGQ_DQ_PREFETCH
 #define AGQ_DQ_PREFETCH 2
 #endif
+#ifndef AGQ_MINIFLOAT_FAST
+#define AGQ_MINIFLOAT_FAST 1  // FP4/FP8 activation rows via the hardware conversions
+#endif
 #ifndef AGQ_Q_PREFETCH
 #define AGQ_Q_PREFETCH 1
 #endif
@@ -433,6 +437,36 @@ __device__ __forceinline__ void encode_row(const uint4 (&ch)[InTraits<Tin>::kChu
     } else if constexpr (CODEC == 0 && TR::kBf16) {
       const float rcp = fdiv(1.0f, a);
       encode_linear_bf16_fast<BITS, PACK>(ch, a, fmul((float)L, rcp), rcp, pk);
+    } else if constexpr (CODEC != 0 && AGQ_MINIFLOAT_FAST) {
+      // two independent halves of 16 values (register pressure)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < kChunks / 2; ++j) {
+          const uint4 c4 = ch[h * (kChunks / 2) + j];
+          const uint32_t wv[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if constexpr (TR::kBf16) {
+              v[8 * j + 2 * k] = u2f(wv[k] << 16);
+              v[8 * j + 2 * k + 1] = u2f(wv[k] & 0xffff0000u);
+            } else {
+              v[4 * j + k] = u2f(wv[k]);
+            }
+          }
+        }
+        uint32_t hw[PACK / 2];
+        if constexpr (CODEC == 2) {
+          static_assert(PACK == 8, "E4M3 codes are one byte");
+          fp8_encode16<TR::kBf16>(v, a, hw);
+        } else {
+          fp4_encode16<PACK, TR::kBf16>(v, a, hw);
+        }
+#pragma unroll
+        for (int k = 0; k < PACK / 2; ++k) words[h * (PACK / 2) + k] = hw[k];
+      }
+      return;
     } else {
       const float inv = codec_inv(CODEC, BITS, a);
 #pragma unroll
@@ -1099,6 +1133,13 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? AGQ_DEQ
       }
     }
     const bool fast = is_bf16_value(s) && fast_scale(s);
+    // FP4 / FP8 rows decode through the hardware minifloat conversion; FP8
+    // rows holding a NaN code keep the per-element path (NaN payloads)
+    bool mfast = false;
+    if constexpr (CODEC != 0 && AGQ_MINIFLOAT_FAST) {
+      if constexpr (CODEC == 2) mfast = fast && !fp8_row_has_nan<PACK>(cw);
+      else mfast = fast;
+    }
     uint64_t pk[kChunks];
     unpack_chunks<kChunkBits>(cw, pk, std::make_integer_sequence<int, kChunks>{});
 #pragma unroll
@@ -1106,6 +1147,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? AGQ_DEQ
       float v[kPerChunk];
       if (CODEC == 0 && fast) {
         decode_linear_words<BITS, PACK, kPerChunk>(cw, j * kPerChunk, s, v);
+      } else if (CODEC != 0 && mfast) {
+        minifloat_decode<CODEC == 0 ? 1 : CODEC, PACK, kPerChunk>(cw, j * kPerChunk, s, v);
       } else if (fast) {
 #pragma unroll
         for (int e = 0; e < kPerChunk; ++e) {
@@ -1124,7 +1167,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? AGQ_DEQ
         uint32_t h[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          if (CODEC == 2)
+          if (CODEC == 2 && !mfast)
             h[k] = bf16_bits_rne(v[2 * k]) | (bf16_bits_rne(v[2 * k + 1]) << 16);
           else {
             __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);

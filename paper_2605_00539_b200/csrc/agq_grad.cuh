@@ -193,7 +193,8 @@ __device__ __forceinline__ void fp8_requant_words(const float (&v)[4 * NW], floa
     uint32_t diff = 0;
 #pragma unroll
     for (int k = 0; k < NW; ++k) diff |= w[k] ^ wm[k];
-    if (diff) {
+    if (diff) {  // rare; unrolled so v/w stay in registers
+#pragma unroll
       for (int k = 0; k < 2 * NW; ++k) {
         const int sh = (k & 1) * 16;
         if (((w[k >> 1] ^ wm[k >> 1]) >> sh) & 0xffffu) {

@@ -321,6 +321,38 @@ AGQ_HD float codec_inv(int codec, int bits, float a) {
 // ---- decode (quantize.hpp:142-155 code_unit_value, :184-186) -------------
 // Reference: out = (float)(unit(c) * (double)scale), unit(c) in double.
 
+// Hardware E2M1 conversion of a pair (cvt.rn.satfinite.e2m1x2.f32: RNE on
+// the E2M1 grid, ties to the even code, saturate at 6, sign kept so -0 and
+// negative underflow give 0x8): low nibble = lo. Host: the same rounding.
+AGQ_HD uint32_t e2m1_rne_signed(float v) {  // host model of one lane of the cvt
+  const float grid[8] = {0.0f, 0.5f, 1.0f, 1.5f, 2.0f, 3.0f, 4.0f, 6.0f};
+  const float a = fabsf(v);
+  uint32_t best = 7;
+  if (a < 6.0f) {
+    for (uint32_t i = 0; i < 7; ++i) {
+      const float mid = 0.5f * (grid[i] + grid[i + 1]);  // exact in binary
+      if (a < mid || (a == mid && (i & 1u) == 0)) {
+        best = i;
+        break;
+      }
+    }
+  }
+  return ((f2u(v) >> 28) & 0x8u) | best;
+}
+AGQ_HD uint32_t cvt_e2m1x2(float lo, float hi) {
+#if defined(__CUDA_ARCH__)
+  uint32_t r;
+  asm("{\n.reg .b8 t;\n"
+      "cvt.rn.satfinite.e2m1x2.f32 t, %1, %2;\n"
+      "mov.b32 %0, {t, 0, 0, 0};\n}"
+      : "=r"(r)
+      : "f"(hi), "f"(lo));
+  return r & 0xffu;
+#else
+  return e2m1_rne_signed(lo) | (e2m1_rne_signed(hi) << 4);
+#endif
+}
+
 // E4M3 magnitude of a code as float (exact).
 AGQ_HD float e4m3_value(uint32_t c) {
   const uint32_t e = (c >> 3) & 0xfu, m = c & 7u;

@@ -1054,10 +1054,16 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? AGQ_DEQ
   constexpr bool kBf16Out = sizeof(Tout) == 2;
   __shared__ __align__(16) unsigned char sbuf[kWarpsPerCta][kTileB];
   __shared__ double fp8lut[CODEC == 2 ? 128 : 1];
+  // exact unit values fl64(unit(c)) for the FP32-scale path (linear / FP4):
+  // one LDS.64 + DMUL + F2F per element instead of a double division
+  constexpr int kU = CODEC == 0 ? (1 << BITS) : (CODEC == 1 ? 16 : 1);
+  __shared__ double ulut[kU];
   if (CODEC == 2) {
     fill_fp8_unit_lut(fp8lut);
-    __syncthreads();
+  } else {
+    for (int c = threadIdx.x; c < kU; c += blockDim.x) ulut[c] = unit_value_double(CODEC, BITS, c);
   }
+  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wb = sbuf[warp];
   const uint64_t total = st.tile_begin[st.nseg];
@@ -1156,10 +1162,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? AGQ_DEQ
           v[e] = decode_one<BITS, CODEC>(c, s, true, fp8lut);
         }
       } else {
+        const double sd = (double)s;
 #pragma unroll
         for (int e = 0; e < kPerChunk; ++e) {
           const uint32_t c = (uint32_t)(pk[j] >> (e * PACK)) & ((1u << BITS) - 1u);
-          v[e] = decode_slow(CODEC, BITS, c, s, fp8lut);
+          if constexpr (CODEC == 2) {  // = decode_slow, inlined
+            const uint32_t sg = (c & 0x80u) << 24;
+            v[e] = (c & 0x7fu) == 0x7fu ? u2f(0x7fc00000u | sg)
+                                         : u2f(f2u(d2f_rn(dmul(fp8lut[c & 0x7fu], sd))) | sg);
+          } else {
+            v[e] = d2f_rn(dmul(ulut[c], sd));  // = dequant_double, tabled
+          }
         }
       }
       uint4 o;

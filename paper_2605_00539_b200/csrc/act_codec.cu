@@ -566,7 +566,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tin) == 2 ? AGQ_QUAN
   using TR = InTraits<Tin>;
   constexpr int kChunks = TR::kChunks;
   constexpr uint32_t kTileB = kWarpElems * sizeof(Tin);    // 2 KB / 4 KB
-  constexpr uint32_t kCodeB = kWarpElems * PACK / 8;
   __shared__ __align__(16) unsigned char sbuf[kWarpsPerCta][kTileB];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wb = sbuf[warp];

@@ -67,6 +67,9 @@ __device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) {
 #ifndef AGQ_ACC_TAB
 #define AGQ_ACC_TAB 1
 #endif
+#ifndef AGQ_ACC_TAB_BF16L
+#define AGQ_ACC_TAB_BF16L 0
+#endif
 #ifndef AGQ_RED_TAB
 #define AGQ_RED_TAB 1
 #endif

@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kAccWarps * 32, 3)
     // block-table decode for the FP32-local / FP32-sum kernel (shared-memory
     // bound on the 256-entry table: 86% -> 93% of HBM); the BF16-local and
     // rounded-precision instances measured faster with the full table
-    constexpr bool kTab = AGQ_ACC_TAB && !BF16L && PREC == 0;
+    constexpr bool kTab = AGQ_ACC_TAB && (!BF16L || AGQ_ACC_TAB_BF16L) && PREC == 0;
     if (kTab && dq_fast(sc) && fp8_tab_ok16(cw)) {
       // v = l + dq (exact product, one rounding: = fadd(dq, l))
 #pragma unroll

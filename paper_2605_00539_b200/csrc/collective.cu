@@ -332,8 +332,11 @@ __device__ __forceinline__ void epoch_end(const Args& a) {
   *done_counter = 0u;
 }
 
+#ifndef AGQ_P2P_MINB
+#define AGQ_P2P_MINB 2
+#endif
 template <int NP, int EPT>
-__global__ void __launch_bounds__(256, 2) k_fused_allreduce(FusedArgs a) {
+__global__ void __launch_bounds__(256, AGQ_P2P_MINB) k_fused_allreduce(FusedArgs a) {
   __shared__ double lut[kDqTable];
   __shared__ float btab[8 * (NP > 0 ? NP : 1) * 32];  // 8 warps x NP pieces x 32 entries
   __shared__ int ok;

@@ -381,6 +381,9 @@ __device__ __forceinline__ TileRef locate(const SegTable& st, uint64_t t) {
 #ifndef AGQ_DQ_PREFETCH
 #define AGQ_DQ_PREFETCH 2
 #endif
+#ifndef AGQ_FP8_DQ_TAB
+#define AGQ_FP8_DQ_TAB 1  // FP8 dequant with FP32 scales via per-block tables
+#endif
 #ifndef AGQ_MINIFLOAT_FAST
 #define AGQ_MINIFLOAT_FAST 1  // FP4/FP8 activation rows via the hardware conversions
 #endif
@@ -1057,6 +1060,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? AGQ_DEQ
   // one LDS.64 + DMUL + F2F per element instead of a double division
   constexpr int kU = CODEC == 0 ? (1 << BITS) : (CODEC == 1 ? 16 : 1);
   __shared__ double ulut[kU];
+  // FP8 with FP32 block scales: per-block 8-entry tables (F[m] / 2, see
+  // agq_numerics.cuh:fp8_dq_tab), 8 blocks per warp tile
+  __shared__ __align__(32) float dqtab[CODEC == 2 ? kWarpsPerCta * 64 : 1];
   if (CODEC == 2) {
     fill_fp8_unit_lut(fp8lut);
   } else {
@@ -1145,12 +1151,36 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? AGQ_DEQ
       if constexpr (CODEC == 2) mfast = fast && !fp8_row_has_nan<PACK>(cw);
       else mfast = fast;
     }
+    bool tfast = false;  // FP8, FP32 scale: block-table decode
+    uint32_t tb_s = 0;
+    if constexpr (CODEC == 2 && AGQ_FP8_DQ_TAB) {
+      float* wt = dqtab + (threadIdx.x >> 5) * 64;
+      const int j0 = (lane & 3) * 2;
+      __syncwarp();  // the previous tile's lookups are done
+      wt[(lane >> 2) * 8 + j0] = fp8_tab_entry_half(fp8_t8(j0), s);
+      wt[(lane >> 2) * 8 + j0 + 1] = fp8_tab_entry_half(fp8_t8(j0 + 1), s);
+      __syncwarp();
+      uint32_t unsafe = 0;
+#pragma unroll
+      for (int k = 0; k < PACK; ++k) unsafe |= fp8_tab_unsafe(cw[k]);
+      tfast = !fast && dq_fast(s) && unsafe == 0;
+      tb_s = (uint32_t)__cvta_generic_to_shared(wt + (lane >> 2) * 8);
+    }
     uint64_t pk[kChunks];
     unpack_chunks<kChunkBits>(cw, pk, std::make_integer_sequence<int, kChunks>{});
 #pragma unroll
     for (int j = 0; j < kChunks; ++j) {
       float v[kPerChunk];
-      if (CODEC == 0 && fast) {
+      if (CODEC == 2 && tfast) {
+#pragma unroll
+        for (int q = 0; q < kPerChunk / 4; ++q) {
+          const uint32_t w1[1] = {cw[(j * kPerChunk) / 4 + q]};
+          float a4[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // + 0.0f: exact (entries are never 0)
+          dq_tab_accum<1>(w1, tb_s, a4);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) v[4 * q + e] = a4[e];
+        }
+      } else if (CODEC == 0 && fast) {
         decode_linear_words<BITS, PACK, kPerChunk>(cw, j * kPerChunk, s, v);
       } else if (CODEC != 0 && mfast) {
         minifloat_decode<CODEC == 0 ? 1 : CODEC, PACK, kPerChunk>(cw, j * kPerChunk, s, v);
@@ -1179,7 +1209,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? AGQ_DEQ
         uint32_t h[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          if (CODEC == 2 && !mfast)
+          if (CODEC == 2 && !mfast && !tfast)
             h[k] = bf16_bits_rne(v[2 * k]) | (bf16_bits_rne(v[2 * k + 1]) << 16);
           else {
             __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);

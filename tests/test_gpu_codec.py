@@ -259,3 +259,25 @@ def test_c2_layer_store_sampled(cuda):
                 assert np.array_equal(got, O.pack(c, bits))
                 want = O.bf16_round(O.dequantize(c, s, bits))
                 assert np.array_equal(u32(back[b * 128:(b + 1) * 128].float().cpu().numpy()), u32(want))
+
+
+@pytest.mark.parametrize("out_dtype", [torch.float32, torch.bfloat16])
+def test_dequant_fp8_fp32_scales(cuda, out_dtype):
+    """FP8 codes with FP32 (non-BF16) block scales — the FP8 gradient case:
+    every code in every block, random FP32 scales plus the table path's range
+    edges, vs the oracle's (float)(unit * (double)s)."""
+    rng = np.random.default_rng(3)
+    nblk = 4096
+    codes = np.concatenate([rng.permutation(256).astype(np.uint8)[:128] for _ in range(nblk)])
+    scales = (rng.random(nblk) * 10.0 ** rng.uniform(-20, 20, nblk)).astype(np.float32)
+    scales[:8] = np.array([0.0, 2.0 ** -60, 2.0 ** 60, 2.0 ** -61, 2.0 ** 61, 1e-40, 3e38, 1.0],
+                          np.float32)
+    nz = rng.random(codes.size) < 0.001  # some rows with NaN codes too
+    codes[nz] = 0x7F
+    q = A.QuantizedTensor(t(codes, cuda, torch.uint8), t(scales, cuda), 8, 128, (codes.size,),
+                          A.CodecKind.Fp8E4M3, packed=False)
+    d = A.dequantize_blockwise(q, out_dtype=out_dtype).float().cpu().numpy()
+    want = O.dequantize(codes, scales, 8, 128, O.FP8)
+    if out_dtype == torch.bfloat16:
+        want = O.bf16_round(want)
+    assert np.array_equal(u32(d), u32(want))

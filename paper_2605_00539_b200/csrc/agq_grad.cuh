@@ -91,9 +91,13 @@ __device__ __forceinline__ float lds_f32(uint32_t a) {
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
   return v;
 }
+// 2^(e-15) exponent bias in a register the optimiser cannot see through, so
+// (y & mask) | bias is one LOP3 (a LOP3 takes a single immediate)
+__constant__ uint32_t c_pow2_bias = 0x38000000u;
 template <int NW>
 __device__ __forceinline__ void dq_tab_accum(const uint32_t (&w)[NW], uint32_t tb_s,
                                              float (&acc)[4 * NW]) {
+  const uint32_t bias = c_pow2_bias;
 #pragma unroll
   for (int i = 0; i < NW; ++i) {
     float f[4], p2[4];
@@ -101,7 +105,7 @@ __device__ __forceinline__ void dq_tab_accum(const uint32_t (&w)[NW], uint32_t t
     for (int b = 0; b < 4; ++b) {
       const uint32_t x = b == 3 ? w[i] : (w[i] << (24 - 8 * b));
       const uint32_t y = (uint32_t)((int32_t)x >> 4);
-      p2[b] = u2f((y & 0x87800000u) | 0x38000000u);
+      p2[b] = u2f((y & 0x87800000u) | bias);
       const uint32_t idx = b == 0 ? ((w[i] << 2) & 0x1cu) : ((w[i] >> (8 * b - 2)) & 0x1cu);
       f[b] = lds_f32(idx | tb_s);
     }

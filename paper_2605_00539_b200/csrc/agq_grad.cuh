@@ -73,13 +73,6 @@ __device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) {
 #ifndef AGQ_RED_TAB
 #define AGQ_RED_TAB 1
 #endif
-// Block-table decode of byte k of w (fp8_dq_tab with the byte moved to the
-// top of the word by one PRMT): tab = the block's 8 entries, fp8_tab_entry.
-__device__ __forceinline__ float fp8_dq_tab_w(uint32_t w, int k, const float* tab) {
-  const uint32_t x = __byte_perm(w, 0u, ((uint32_t)k << 12) | 0x0444u);  // byte k -> bits 24..31
-  const uint32_t y = (uint32_t)((int32_t)x >> 4);
-  return fmul(tab[(x >> 24) & 7u], u2f((y & 0x87800000u) + 0x37800000u));
-}
 // Lean table decode + accumulate of NW code words (4 codes each) against
 // this block's table at shared address tb_s (32-byte aligned, 8 entries
 // holding F[m]/2): the entry address comes straight from the code word

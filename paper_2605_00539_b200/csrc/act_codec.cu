@@ -1082,6 +1082,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? AGQ_DEQ
         const uint4 v = ldg128_stream(src + lane * PACK * 4 + k * 16);
         w[4 * k] = v.x; w[4 * k + 1] = v.y; w[4 * k + 2] = v.z; w[4 * k + 3] = v.w;
       }
+    } else if constexpr (PACK % 2 == 0) {  // 8-byte aligned lane rows (b = 6)
+      const uint2* s64 = reinterpret_cast<const uint2*>(src + lane * PACK * 4);
+#pragma unroll
+      for (int k = 0; k < PACK / 2; ++k) {
+        const uint2 v = __ldg(s64 + k);
+        w[2 * k] = v.x;
+        w[2 * k + 1] = v.y;
+      }
     } else {
       const uint32_t* s32 = reinterpret_cast<const uint32_t*>(src) + lane * PACK;
 #pragma unroll

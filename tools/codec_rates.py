@@ -25,6 +25,7 @@ def timeit(fn, iters=10):
 
 
 F32 = "--f32" in sys.argv  # FP32 activations (the C++ drop-in surface's input type)
+BYTES = "--bytes" in sys.argv  # one code per byte (the reference's host layout)
 n = 16384 * 14336
 dev = torch.device("cuda")
 R = 3
@@ -33,19 +34,22 @@ ESZ = 4 if F32 else 2
 DT = L.AGQ_F32 if F32 else L.AGQ_BF16
 sp = torch.cuda.current_stream().cuda_stream
 for name, codec, bits in (("linear", 0, 4), ("linear", 0, 8), ("fp4_e2m1", 1, 4), ("fp8_e4m3", 2, 8)):
-    qs = [A.quantize_blockwise(x, bits, 128, A.CodecKind(codec), check=False) for x in xs]
+    qs = [A.quantize_blockwise(x, bits, 128, A.CodecKind(codec), packed=not BYTES, check=False)
+          for x in xs]
+    CL = L.AGQ_CODES_BYTES if BYTES else L.AGQ_CODES_PACKED
     outs = [torch.empty_like(xs[0]) for _ in range(R)]
-    nb = n * ESZ + n * bits / 8 + n / 128 * 4
+    nb = n * ESZ + n * (1 if BYTES else bits / 8) + n / 128 * 4
 
     def fq(i):
         x, q = xs[i % R], qs[i % R]
         L.check(L.lib.agq_quantize(x.data_ptr(), DT, n, bits, 128, codec, q.codes.data_ptr(),
-                                   L.AGQ_CODES_PACKED, q.scales.data_ptr(), None, sp))
+                                   CL, q.scales.data_ptr(), None, sp))
 
     def fd(i):
         q, o = qs[i % R], outs[i % R]
-        L.check(L.lib.agq_dequantize(q.codes.data_ptr(), L.AGQ_CODES_PACKED, q.scales.data_ptr(), n,
+        L.check(L.lib.agq_dequantize(q.codes.data_ptr(), CL, q.scales.data_ptr(), n,
                                      bits, 128, codec, o.data_ptr(), DT, 0, None, sp))
     tq, td = timeit(fq), timeit(fd)
-    print(json.dumps({"input": "f32" if F32 else "bf16", "codec": name, "bits": bits, "quant_GBs": round(nb / tq / 1e9, 1),
+    print(json.dumps({"input": "f32" if F32 else "bf16", "codes": "bytes" if BYTES else "packed",
+                      "codec": name, "bits": bits, "quant_GBs": round(nb / tq / 1e9, 1),
                       "dequant_GBs": round(nb / td / 1e9, 1)}), flush=True)

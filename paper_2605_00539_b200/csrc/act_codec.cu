@@ -637,32 +637,46 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tin) == 2 ? AGQ_QUAN
   const uint64_t total = st.tile_begin[st.nseg];
   const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
   uint64_t t = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
-  SegCursor icur, pcur;
+  // per-lane swizzled shared offsets (constant), one tile ref per slot, the
+  // loop unrolled by the ring depth so the slot index is a constant
+  const uint32_t wb_s = (uint32_t)__cvta_generic_to_shared(wb);
+  uint32_t sw[kChunks], rd[kChunks];
+#pragma unroll
+  for (int j = 0; j < kChunks; ++j) {
+    sw[j] = swz_of_linear<kChunks>(j * 512 + lane * 16);
+    rd[j] = swz_off<kChunks>(lane, j);
+  }
+  TileRef trq[kStg];
+  SegCursor cur;
   auto issue = [&](uint64_t tt, int slot) {
     if (tt < total) {
-      const TileRef tr = locate_from(st, tt, icur);
-      const unsigned char* src = static_cast<const unsigned char*>(st.src[tr.g]) + tr.lt * kTileB;
+      trq[slot] = locate_from(st, tt, cur);
+      const unsigned char* src = static_cast<const unsigned char*>(st.src[trq[slot].g]) +
+                                 trq[slot].lt * kTileB + lane * 16;
+      const uint32_t base = wb_s + slot * kTileB;
 #pragma unroll
-      for (int j = 0; j < kChunks; ++j)
-        cp_async16(wb + slot * kTileB + swz_of_linear<kChunks>(j * 512 + lane * 16),
-                   src + j * 512 + lane * 16);
+      for (int j = 0; j < kChunks; ++j) cp_async16_s(base + sw[j], src + j * 512);
     }
     cp_async_commit();  // always: keeps the group count uniform
   };
 #pragma unroll
   for (int d = 0; d < kStg; ++d) issue(t + d * nw, d);
-  int slot = 0;
-  for (; t < total; t += nw) {
-    cp_async_wait<kStg - 1>();
-    __syncwarp();
-    const TileRef tr = locate_from(st, t, pcur);
-    uint4 ch[kChunks];
+  while (t < total) {
 #pragma unroll
-    for (int j = 0; j < kChunks; ++j) ch[j] = lds128(wb + slot * kTileB + swz_off<kChunks>(lane, j));
-    __syncwarp();
-    issue(t + kStg * nw, slot);
-    slot = slot + 1 == kStg ? 0 : slot + 1;
-    quant_tile<BITS, PACK, CODEC, Tin>(st, err, tr, lane, ch);
+    for (int slot = 0; slot < kStg; ++slot) {
+      if (t >= total) break;
+      cp_async_wait<kStg - 1>();
+      __syncwarp();
+      const TileRef tr = trq[slot];
+      const uint32_t base = wb_s + slot * kTileB;
+      uint4 ch[kChunks];
+#pragma unroll
+      for (int j = 0; j < kChunks; ++j) ch[j] = lds128_s(base + rd[j]);
+      __syncwarp();
+      issue(t + kStg * nw, slot);
+      quant_tile<BITS, PACK, CODEC, Tin>(st, err, tr, lane, ch);
+      t += nw;
+    }
   }
   cp_async_wait<0>();
 }

@@ -221,6 +221,18 @@ agq_status agq_allreduce_fp8(agq_comm* comm, uint8_t* codes, float* scales,
                              uint64_t n, uint32_t block, int algo,
                              agq_errors* d_err, agq_stream_t stream);
 
+/* Replaces allreduce_naive_fp8 (collective.hpp:338-431) for real ranks: the
+ * overflow-prone strawman, in place on this rank's FP8 gradient. P-1 NCCL
+ * ring steps, each adding in FP8 at the receiver's ORIGINAL scales, then an
+ * all-gather (chunk c from rank (c-1) mod P, with that rank's scales).
+ * d_err->saturated (caller-reset) = CollectiveResult::overflow_elements,
+ * identical on every rank; *d_events (caller-zeroed, or NULL) += this
+ * rank's CollectiveResult::overflow_events entry. */
+agq_status agq_allreduce_naive_fp8(agq_comm* comm, uint8_t* codes, float* scales,
+                                   uint64_t n, uint32_t block, agq_errors* d_err,
+                                   unsigned long long* d_events,
+                                   agq_stream_t stream);
+
 /* The baseline the north star compares against: ncclAllReduce(bf16, sum). */
 agq_status agq_allreduce_bf16_nccl(agq_comm* comm, void* data, uint64_t n,
                                    agq_stream_t stream);

@@ -91,6 +91,7 @@ def _load() -> C.CDLL:
         "agq_comm_rank": (I, [P]),
         "agq_comm_size": (I, [P]),
         "agq_allreduce_fp8": (I, [P, P, P, U64, U32, I, P, S]),
+        "agq_allreduce_naive_fp8": (I, [P, P, P, U64, U32, P, P, S]),
         "agq_allreduce_bf16_nccl": (I, [P, P, U64, S]),
         "agq_quantize_host": (I, [P, U64, I, U32, I, P, P]),
         "agq_dequantize_host": (I, [P, P, U64, I, U32, I, P]),
@@ -118,7 +119,7 @@ EXPORTED = (
     "agq_fp8_accumulate agq_fp8_reduce_requant agq_chunk_assignment agq_allreduce_simulated "
     "agq_allreduce_naive_simulated agq_comm_unique_id agq_comm_init agq_comm_p2p_export "
     "agq_comm_p2p_open agq_comm_p2p_buffers agq_comm_destroy agq_comm_rank agq_comm_size "
-    "agq_allreduce_fp8 agq_allreduce_bf16_nccl agq_quantize_host agq_dequantize_host "
+    "agq_allreduce_fp8 agq_allreduce_naive_fp8 agq_allreduce_bf16_nccl agq_quantize_host agq_dequantize_host "
     "agq_local_accumulate_host agq_allreduce_simulated_host agq_stored_activation_counts "
     "agq_plan_bit_widths").split()
 

@@ -112,6 +112,23 @@ class Communicator:
             err.raise_if_any(L.AGQ_OP_ALLREDUCE)
         return q
 
+    def allreduce_naive_fp8(self, q: QuantizedTensor, stream=None):
+        """allreduce_naive_fp8 (collective.hpp:338-431) across the ranks, in
+        place: the overflow-prone FP8 ring strawman. Returns (q,
+        overflow_elements, this rank's overflow_events) like the reference's
+        CollectiveResult (events of the other ranks stay on those ranks)."""
+        if q.codec_kind != CodecKind.Fp8E4M3:
+            raise L.InvalidArgument("worker gradients are FP8 E4M3 tensors")
+        if q.packed:
+            raise L.InvalidArgument("the all-reduce takes one byte per code (packed=False)")
+        err = ErrorRecord(q.codes.device).reset(stream)
+        ev = torch.zeros(1, dtype=torch.int64, device=q.codes.device)
+        L.check(L.lib.agq_allreduce_naive_fp8(self._h, q.codes.data_ptr(), q.scales.data_ptr(),
+                                              q.num_elements(), q.block_size, err.ptr,
+                                              ev.data_ptr(), _stream(stream)))
+        h = err.raise_if_any(L.AGQ_OP_ALLREDUCE)
+        return q, int(h.saturated), int(ev.item())
+
     def allreduce_bf16(self, t: torch.Tensor, stream=None) -> torch.Tensor:
         """Baseline: ncclAllReduce(bf16, sum) in place."""
         if t.dtype != torch.bfloat16:

@@ -50,6 +50,9 @@ agq_status comm_p2p_buffers(agq_comm* c, uint8_t** codes, float** scales);
 agq_status comm_destroy(agq_comm* c);
 int comm_rank(const agq_comm* c);
 int comm_size(const agq_comm* c);
+agq_status allreduce_naive(agq_comm* c, uint8_t* codes, float* scales, uint64_t n,
+                           uint32_t block, agq_errors* err, unsigned long long* events,
+                           cudaStream_t s);
 agq_status allreduce_fp8(agq_comm* c, uint8_t* codes, float* scales, uint64_t n, uint32_t block,
                          int algo, agq_errors* err, cudaStream_t s);
 agq_status allreduce_bf16_nccl(agq_comm* c, void* data, uint64_t n, cudaStream_t s);
@@ -380,6 +383,14 @@ agq_status agq_allreduce_fp8(agq_comm* comm, uint8_t* codes, float* scales, uint
                              uint32_t block, int algo, agq_errors* d_err, agq_stream_t stream) {
   if (agq_status st = check_args(8, block, AGQ_CODEC_FP8_E4M3)) return st;
   return allreduce_fp8(comm, codes, scales, n, block, algo, d_err, (cudaStream_t)stream);
+}
+
+agq_status agq_allreduce_naive_fp8(agq_comm* comm, uint8_t* codes, float* scales, uint64_t n,
+                                   uint32_t block, agq_errors* d_err,
+                                   unsigned long long* d_events, agq_stream_t stream) {
+  if (agq_status st = check_args(8, block, AGQ_CODEC_FP8_E4M3)) return st;
+  if (!d_err) return set_error(AGQ_ERR_INVALID_ARGUMENT, "naive protocol needs an error record");
+  return allreduce_naive(comm, codes, scales, n, block, d_err, d_events, (cudaStream_t)stream);
 }
 
 agq_status agq_allreduce_bf16_nccl(agq_comm* comm, void* data, uint64_t n, agq_stream_t stream) {

@@ -34,6 +34,11 @@ agq_status reduce_requant_device(int np, const uint8_t* const* pc, const float* 
                                  float* const* os, long long blk_base, agq_errors* err,
                                  cudaStream_t s);
 void chunk_ranges(uint64_t n, uint32_t block, int workers, uint64_t* ranges);
+agq_status naive_step_device(const uint8_t* in_codes, const float* in_scales,
+                             const uint32_t* in_sat, uint8_t* codes, const float* scales,
+                             uint32_t* out_sat, uint64_t len, uint32_t block,
+                             unsigned long long* saturated, unsigned long long* events,
+                             cudaStream_t s);
 }  // namespace agqh
 
 // NCCL is resolved at run time: reuse the libnccl.so.2 already loaded in the
@@ -91,6 +96,11 @@ struct agq_comm {
   uint8_t* recv_codes = nullptr;
   float* recv_scales = nullptr;
   uint64_t recv_chunk_cap = 0;  // elements per peer slot
+  // naive-ring workspace: one incoming chunk + two saturation bitmasks
+  uint8_t* ring_codes = nullptr;
+  float* ring_scales = nullptr;
+  uint32_t* ring_sat = nullptr;
+  uint64_t ring_cap = 0;  // elements
   // v2 symmetric memory
   unsigned char* sym = nullptr;
   size_t sym_bytes = 0;
@@ -803,6 +813,9 @@ agq_status comm_destroy(agq_comm* c) {
   if (c->sym) cudaFree(c->sym);
   if (c->recv_codes) cudaFree(c->recv_codes);
   if (c->recv_scales) cudaFree(c->recv_scales);
+  if (c->ring_codes) cudaFree(c->ring_codes);
+  if (c->ring_scales) cudaFree(c->ring_scales);
+  if (c->ring_sat) cudaFree(c->ring_sat);
   if (c->done_counter) cudaFree(c->done_counter);
   if (c->nccl) nccl().CommDestroy(c->nccl);
   delete c;
@@ -1126,6 +1139,90 @@ agq_status allreduce_fp8(agq_comm* c, uint8_t* codes, float* scales, uint64_t n,
   if (algo == AGQ_AR_FUSED_P2P) return allreduce_p2p(c, codes, scales, n, block, err, s);
   if (algo == AGQ_AR_PUSH_P2P) return allreduce_push(c, codes, scales, n, block, err, s);
   return allreduce_nccl(c, codes, scales, n, block, err, s);
+}
+
+// allreduce_naive_fp8 (collective.hpp:338-431) on real ranks: P-1 ring
+// steps (rank r sends chunk (r-step) mod P to r+1 and folds chunk
+// (r-step-1) mod P from r-1 into its own codes at its original scales), the
+// saturation bitmask riding along with each chunk, then an all-gather in
+// which rank r contributes chunk (r+1) mod P with ITS scales. err->saturated
+// = CollectiveResult::overflow_elements (summed over ranks: each chunk's
+// final owner counts it); *events = this rank's overflow_events entry.
+agq_status allreduce_naive(agq_comm* c, uint8_t* codes, float* scales, uint64_t n,
+                           uint32_t block, agq_errors* err, unsigned long long* events,
+                           cudaStream_t s) {
+  if (n == 0 || c->nranks == 1) return AGQ_OK;
+  const int P = c->nranks, r = c->rank;
+  std::vector<uint64_t> rg(2 * P);
+  chunk_ranges(n, block, P, rg.data());
+  uint64_t maxlen = 0;
+  for (int q = 0; q < P; ++q) maxlen = std::max(maxlen, rg[2 * q + 1] - rg[2 * q]);
+  const uint64_t cap = round_up(maxlen ? maxlen : 1, 256);
+  const uint64_t words = cap / 32;
+  if (c->ring_cap < cap) {
+    if (c->ring_codes) cudaFree(c->ring_codes);
+    if (c->ring_scales) cudaFree(c->ring_scales);
+    if (c->ring_sat) cudaFree(c->ring_sat);
+    c->ring_codes = nullptr;
+    c->ring_scales = nullptr;
+    c->ring_sat = nullptr;
+    c->ring_cap = 0;
+    cudaError_t e = cudaMalloc(&c->ring_codes, cap);
+    if (e == cudaSuccess) e = cudaMalloc(&c->ring_scales, (cap / block + 2) * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&c->ring_sat, 2 * words * 4);
+    if (e != cudaSuccess) return cuda_fail(e, "naive all-reduce: workspace");
+    c->ring_cap = cap;
+  }
+  const int to = (r + 1) % P, from = (r - 1 + P) % P;
+  uint32_t* sat_mine = c->ring_sat;            // mask of the chunk folded last step
+  uint32_t* sat_in = c->ring_sat + c->ring_cap / 32;  // mask arriving with the message
+  for (int step = 0; step < P - 1; ++step) {
+    const int cs = ((r - step) % P + P) % P, cr = ((r - step - 1) % P + P) % P;
+    const uint64_t bs = rg[2 * cs], ls = rg[2 * cs + 1] - bs;
+    const uint64_t br = rg[2 * cr], lr = rg[2 * cr + 1] - br;
+    agq_status st = nccl_fail(nccl().GroupStart(), "ncclGroupStart");
+    if (st) return st;
+    if (ls) {
+      nccl().Send(codes + bs, ls, ncclUint8, to, c->nccl, s);
+      nccl().Send(scales + bs / block, (ls + block - 1) / block, ncclFloat32, to, c->nccl, s);
+      if (step) nccl().Send(sat_mine, (ls + 31) / 32, ncclUint32, to, c->nccl, s);
+    }
+    if (lr) {
+      nccl().Recv(c->ring_codes, lr, ncclUint8, from, c->nccl, s);
+      nccl().Recv(c->ring_scales, (lr + block - 1) / block, ncclFloat32, from, c->nccl, s);
+      if (step) nccl().Recv(sat_in, (lr + 31) / 32, ncclUint32, from, c->nccl, s);
+    }
+    st = nccl_fail(nccl().GroupEnd(), "naive ring step");
+    if (st) return st;
+    const bool last = step == P - 2;
+    st = naive_step_device(c->ring_codes, c->ring_scales, step ? sat_in : nullptr, codes + br,
+                           scales + br / block, last ? nullptr : sat_mine, lr, block,
+                           last ? &err->saturated : nullptr, events, s);
+    if (st) return st;
+  }
+  agq_status st = nccl_fail(nccl().AllReduce(&err->saturated, &err->saturated, 1, ncclUint64,
+                                             ncclSum, c->nccl, s),
+                            "saturation count");
+  if (st) return st;
+  // all-gather: rank q owns chunk (q+1) mod P
+  const int co = (r + 1) % P;
+  const uint64_t bo = rg[2 * co], lo = rg[2 * co + 1] - bo;
+  st = nccl_fail(nccl().GroupStart(), "ncclGroupStart");
+  if (st) return st;
+  for (int q = 0; q < P; ++q) {
+    if (q == r) continue;
+    const int cq = (q + 1) % P;
+    const uint64_t bq = rg[2 * cq], lq = rg[2 * cq + 1] - bq;
+    if (lo) {
+      nccl().Send(codes + bo, lo, ncclUint8, q, c->nccl, s);
+      nccl().Send(scales + bo / block, (lo + block - 1) / block, ncclFloat32, q, c->nccl, s);
+    }
+    if (lq) {
+      nccl().Recv(codes + bq, lq, ncclUint8, q, c->nccl, s);
+      nccl().Recv(scales + bq / block, (lq + block - 1) / block, ncclFloat32, q, c->nccl, s);
+    }
+  }
+  return nccl_fail(nccl().GroupEnd(), "naive all-gather");
 }
 
 agq_status allreduce_bf16_nccl(agq_comm* c, void* data, uint64_t n, cudaStream_t s) {

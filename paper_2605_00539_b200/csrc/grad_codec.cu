@@ -458,6 +458,56 @@ __global__ void k_naive_ring(PieceTable pt, uint64_t n, uint32_t block, const ui
   }
 }
 
+// One ring step of allreduce_naive_fp8 on a REAL rank (collective.hpp:373-400):
+// add the chunk message of rank r-1 into this rank's working codes, re-encode
+// at this rank's ORIGINAL scales (scales never change in the naive protocol,
+// so they are read-only here). The sticky per-element saturation flag
+// (collective.hpp:390-398) travels with the chunk as a bitmask, bit j =
+// element begin+j: in_sat (NULL on step 0) | this step's overflows -> out_sat.
+// On the final step the owner adds the popcount to err->saturated instead.
+// One warp per 32 elements (one mask word).
+__global__ void k_naive_step(const uint8_t* in_codes, const float* in_scales,
+                             const uint32_t* in_sat, uint8_t* codes, const float* scales,
+                             uint32_t* out_sat, uint64_t len, uint32_t block,
+                             unsigned long long* saturated, unsigned long long* events) {
+  __shared__ double lut[128];
+  fill_fp8_unit_lut(lut);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint64_t nwords = (len + 31) / 32;
+  const uint64_t nwarps = gridDim.x * (uint64_t)(blockDim.x >> 5);
+  unsigned long long my_events = 0, my_sat = 0;
+  for (uint64_t w = blockIdx.x * (uint64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); w < nwords;
+       w += nwarps) {
+    const uint64_t j = w * 32 + lane;
+    bool over = false;
+    if (j < len) {
+      const uint64_t b = j / block;
+      const uint8_t ci = in_codes[j], cl = codes[j];
+      const double inc = lut[ci & 0x7f] * (ci & 0x80 ? -1.0 : 1.0) * (double)in_scales[b];
+      const double loc = lut[cl & 0x7f] * (cl & 0x80 ? -1.0 : 1.0) * (double)scales[b];
+      const double sum = inc + loc;
+      const float scale = scales[b];
+      const double unit = scale == 0.0f ? 0.0 : sum / (double)scale;
+      over = (scale == 0.0f && sum != 0.0);
+      const double v = unit * 448.0;
+      if (fabs(v) > 448.0) over = true;
+      codes[j] = (uint8_t)fp8_encode_double(v);
+    }
+    const uint32_t mask = __ballot_sync(0xffffffffu, over);
+    if (lane == 0) {
+      my_events += __popc(mask);
+      const uint32_t sticky = mask | (in_sat ? in_sat[w] : 0u);
+      if (out_sat) out_sat[w] = sticky;
+      else my_sat += __popc(sticky);
+    }
+  }
+  if (lane == 0) {
+    if (events && my_events) atomicAdd(events, my_events);
+    if (saturated && my_sat) atomicAdd(saturated, my_sat);
+  }
+}
+
 }  // namespace agqk
 
 // ===========================================================================
@@ -640,6 +690,18 @@ agq_status naive_ring_device(int world, const uint8_t* const* codes, const float
   k_naive_ring<<<gen_grid(n, 256), 256, 0, s>>>(pt, n, block, d_ranges, oc, os, err, events);
   count_launch();
   return cuda_fail(cudaGetLastError(), "naive ring: launch");
+}
+
+agq_status naive_step_device(const uint8_t* in_codes, const float* in_scales,
+                             const uint32_t* in_sat, uint8_t* codes, const float* scales,
+                             uint32_t* out_sat, uint64_t len, uint32_t block,
+                             unsigned long long* saturated, unsigned long long* events,
+                             cudaStream_t s) {
+  if (len == 0) return AGQ_OK;
+  k_naive_step<<<gen_grid((len + 31) / 32 * 32, 256), 256, 0, s>>>(
+      in_codes, in_scales, in_sat, codes, scales, out_sat, len, block, saturated, events);
+  count_launch();
+  return cuda_fail(cudaGetLastError(), "naive ring step: launch");
 }
 
 }  // namespace agqh

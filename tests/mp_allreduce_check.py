@@ -79,6 +79,35 @@ def main():
             if not ok:
                 fails += 1
                 print(f"rank {rank}: MISMATCH algo={algo} n={n}", flush=True)
+    # allreduce_naive_fp8 (collective.hpp:338-431) on real ranks: codes,
+    # scales and overflow_elements against the oracle; this rank's
+    # overflow_events against the one-device simulation.
+    naive_cases = [(seed, n, None) for seed, n in enumerate([128, 1000, 8192 * 3 + 300, 77, 5000])]
+    naive_cases += [(60, 128 * 40, "every_code"), (61, 4096, "const64")]
+    for seed, n, kind in naive_cases:
+        if kind == "every_code":
+            g = every_code_grads(world, n // 128, seed)
+        elif kind == "const64":  # test_collective.cpp:160-181: naive pins at 64
+            g = [O.quantize(np.full(n, 64.0, np.float32), 8, 128, O.FP8) for _ in range(world)]
+        else:
+            g = grads(world, n, seed)
+        want_c, want_s, want_ov = O.allreduce_naive([c for c, _ in g], [s for _, s in g])
+        mains = [A.QuantizedTensor(torch.from_numpy(c).to(dev), torch.from_numpy(s).to(dev), 8, 128,
+                                   (n,), A.CodecKind.Fp8E4M3, packed=False) for c, s in g]
+        _, _, sim_ev = A.allreduce_naive_simulated(mains, events=True)
+        q = mains[rank]
+        _, ov, ev = comm.allreduce_naive_fp8(q)
+        ok = np.array_equal(q.codes.cpu().numpy(), want_c) and \
+            np.array_equal(q.scales.cpu().numpy().view(np.uint32), want_s.view(np.uint32)) and \
+            ov == want_ov and ev == sim_ev[rank]
+        if kind == "const64" and world > 1:
+            nb = n // 128
+            mine = 128 * (nb // world + (rank < nb % world))
+            ok = ok and ov == n and ev == n - mine and bool((q.codes.cpu().numpy() == want_c[0]).all())
+        if not ok:
+            fails += 1
+            print(f"rank {rank}: NAIVE MISMATCH n={n} kind={kind} ov={ov}/{want_ov} "
+                  f"ev={ev}/{sim_ev[rank]}", flush=True)
     # an fp32 overflow in ONE owner's local reduce aborts the protocol on
     # every rank (collective.hpp:278-281): block 0 (owned by rank 0) holds
     # 3e38 on every rank, so only rank 0's reduce overflows.

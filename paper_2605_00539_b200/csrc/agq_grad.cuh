@@ -78,7 +78,8 @@ __device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) {
 // holding F[m]/2): the entry address comes straight from the code word
 // (shift + one LOP3), the signed power of two 2^(e-15) from an arithmetic
 // shift + one LOP3 ((e | 0x70) = e + 112 for e < 16), products and sums in
-// f32x2 pairs. Per element ~7 issued ops, no F2F, no bank conflicts.
+// f32x2 pairs (one FFMA2 per pair onto acc). Per element ~6 issued ops, no F2F,
+// no bank conflicts.
 __device__ __forceinline__ float lds_f32(uint32_t a) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
@@ -87,6 +88,9 @@ __device__ __forceinline__ float lds_f32(uint32_t a) {
 // 2^(e-15) exponent bias in a register the optimiser cannot see through, so
 // (y & mask) | bias is one LOP3 (a LOP3 takes a single immediate)
 __constant__ uint32_t c_pow2_bias = 0x38000000u;
+#ifndef AGQ_TAB_FMA
+#define AGQ_TAB_FMA 1  // 0: separate FMUL2 + FADD (the previous build, for A/B)
+#endif
 template <int NW>
 __device__ __forceinline__ void dq_tab_accum(const uint32_t (&w)[NW], uint32_t tb_s,
                                              float (&acc)[4 * NW]) {
@@ -104,8 +108,16 @@ __device__ __forceinline__ void dq_tab_accum(const uint32_t (&w)[NW], uint32_t t
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
+      // one FFMA2 = fadd(acc, F*2^k) bit for bit: the product is exact (a
+      // normal float times a power of two), so the fused add rounds once,
+      // exactly like the separate add
+#if AGQ_TAB_FMA
+      const f32x2 a = fma2(pk2(f[2 * h], f[2 * h + 1]), pk2(p2[2 * h], p2[2 * h + 1]),
+                           pk2(acc[4 * i + 2 * h], acc[4 * i + 2 * h + 1]));
+#else
       const f32x2 v = mul2(pk2(f[2 * h], f[2 * h + 1]), pk2(p2[2 * h], p2[2 * h + 1]));
       const f32x2 a = add2(pk2(acc[4 * i + 2 * h], acc[4 * i + 2 * h + 1]), v);
+#endif
       up2(a, acc[4 * i + 2 * h], acc[4 * i + 2 * h + 1]);
     }
   }
@@ -273,6 +285,46 @@ __device__ __forceinline__ uint32_t tab_addr(const float* wtab, int p) {
   return (uint32_t)__cvta_generic_to_shared(wtab + p * (256 / LPB) + (lane / LPB) * 8);
 }
 
+// Absmax, error records, FP8 requant and the stores of one 16-element group.
+__device__ __forceinline__ void reduce_finish(const PieceTable& pt, uint64_t e0, uint64_t len,
+                                              bool whole, bool in_range, uint64_t blk,
+                                              uint32_t sbad, float (&acc)[16],
+                                              long long blk_base, agq_errors* err);
+
+// Decode + FP32 sum + requant + stores of one 16-element group whose NP
+// pieces' code words (cv) and block scales (sc) are already in registers.
+// Every lane of the warp must call (the table build synchronises the warp).
+template <int NP>
+__device__ __forceinline__ void reduce_compute(const PieceTable& pt, uint64_t e0, uint64_t len,
+                                               bool whole, const uint4 (&cv)[NP],
+                                               const float (&sc)[NP], long long blk_base,
+                                               const double* t16, agq_errors* err, float* wtab) {
+  const uint64_t blk = e0 / kBlock;
+  const bool in_range = e0 < len;
+  float acc[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) acc[e] = 0.0f;
+  uint32_t sbad = 0;
+  if (AGQ_RED_TAB && wtab != nullptr) build_tables<NP, 8>(wtab, sc);  // all lanes
+  if (in_range) {
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      sbad |= !(sc[p] >= 0.0f) || !(sc[p] <= 3.402823466e38f);
+      const uint32_t w[4] = {cv[p].x, cv[p].y, cv[p].z, cv[p].w};
+      if (AGQ_RED_TAB && wtab != nullptr && dq_fast(sc[p]) && fp8_tab_ok16(w)) {
+        dq_tab_accum<4>(w, tab_addr<8>(wtab, p), acc);
+      } else {
+        dq_accum<16>(w, sc[p], t16, acc);
+      }
+    }
+    // elements past the end contribute nothing to the absmax
+    if (!whole)
+      for (int e = 0; e < 16; ++e)
+        if (e0 + e >= len) acc[e] = 0.0f;
+  }
+  reduce_finish(pt, e0, len, whole, in_range, blk, sbad, acc, blk_base, err);
+}
+
 // ---------------------------------------------------------------------------
 // K4: block-128 reduce-requant, 16 elements per thread, direct loads.
 // ---------------------------------------------------------------------------
@@ -285,15 +337,10 @@ template <int NP>
 __device__ __forceinline__ void reduce_group(const PieceTable& pt, uint64_t g, uint64_t len,
                                              long long blk_base, const double* t16,
                                              agq_errors* err, bool vec, float* wtab = nullptr) {
-  const int np = NP > 0 ? NP : pt.np;
   const uint64_t e0 = g * 16;
   const uint64_t blk = e0 / kBlock;
   const bool in_range = e0 < len;
   const bool whole = vec && e0 + 16 <= len;
-  float acc[16];
-#pragma unroll
-  for (int e = 0; e < 16; ++e) acc[e] = 0.0f;
-  uint32_t sbad = 0;
   if constexpr (NP > 0) {
     uint4 cv[NP];
     float sc[NP];
@@ -313,22 +360,14 @@ __device__ __forceinline__ void reduce_group(const PieceTable& pt, uint64_t g, u
         cv[p] = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
-    if (AGQ_RED_TAB && wtab != nullptr) build_tables<NP, 8>(wtab, sc);  // all lanes
-    if (in_range) {
+    reduce_compute<NP>(pt, e0, len, whole, cv, sc, blk_base, t16, err, wtab);
+  } else {
+    const int np = pt.np;
+    float acc[16];
 #pragma unroll
-      for (int p = 0; p < NP; ++p) {
-        sbad |= !(sc[p] >= 0.0f) || !(sc[p] <= 3.402823466e38f);
-        const uint32_t w[4] = {cv[p].x, cv[p].y, cv[p].z, cv[p].w};
-        if (AGQ_RED_TAB && wtab != nullptr && dq_fast(sc[p]) && fp8_tab_ok16(w)) {
-          dq_tab_accum<4>(w, tab_addr<8>(wtab, p), acc);
-        } else {
-          dq_accum<16>(w, sc[p], t16, acc);
-        }
-      }
-    }
-  }
-  if (in_range) {
-    if constexpr (NP == 0) {
+    for (int e = 0; e < 16; ++e) acc[e] = 0.0f;
+    uint32_t sbad = 0;
+    if (in_range) {
 #pragma unroll 1
       for (int p = 0; p < np; ++p) {
         const float scp = pt.scales[p][blk];
@@ -343,12 +382,18 @@ __device__ __forceinline__ void reduce_group(const PieceTable& pt, uint64_t g, u
         }
         dq_accum<16>(w, scp, t16, acc);
       }
+      if (!whole)
+        for (int e = 0; e < 16; ++e)
+          if (e0 + e >= len) acc[e] = 0.0f;
     }
-    // elements past the end contribute nothing to the absmax
-    if (!whole)
-      for (int e = 0; e < 16; ++e)
-        if (e0 + e >= len) acc[e] = 0.0f;
+    reduce_finish(pt, e0, len, whole, in_range, blk, sbad, acc, blk_base, err);
   }
+}
+
+__device__ __forceinline__ void reduce_finish(const PieceTable& pt, uint64_t e0, uint64_t len,
+                                              bool whole, bool in_range, uint64_t blk,
+                                              uint32_t sbad, float (&acc)[16],
+                                              long long blk_base, agq_errors* err) {
   const uint32_t m = absmax_bits16(acc);
   const int sub = threadIdx.x & 7;
   if (in_range && sub == 0) {

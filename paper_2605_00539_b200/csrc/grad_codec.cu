@@ -399,6 +399,68 @@ __global__ void __launch_bounds__(256, AGQ_RED_MINB)
     reduce_group<NP>(pt, g, g < ngroups ? len : 0, blk_base, lut, err, vec != 0, wtab);
 }
 
+// K4 with a per-warp cp.async ring (LDGSTS): the NP pieces' code words
+// (16 B per lane per piece) and block scales of warp-group i+S-1 are in
+// flight while warp-group i (512 elements = 4 blocks) is decoded, so a warp
+// keeps HBM requests outstanding through its arithmetic — the direct-load
+// kernel issues a group's loads, then idles the memory system while it
+// decodes. Whole 512-element warp-groups only (16-byte aligned pointers); the
+// ragged tail goes through reduce_group. Same arithmetic (reduce_compute), so
+// bit-identical.
+template <int NP, int S>
+__global__ void __launch_bounds__(256, AGQ_RED_MINB)
+    k_reduce128_pipe(PieceTable pt, uint64_t len, long long blk_base, agq_errors* err) {
+  extern __shared__ __align__(16) unsigned char ring_smem[];
+  __shared__ double lut[kDqTable];
+  __shared__ float btab[8 * NP * 32];
+  fill_fp8_dq_table(lut);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr uint32_t kSlot = NP * 512 + NP * 16;  // codes, then 4 scales per piece
+  unsigned char* ring = ring_smem + (size_t)warp * S * kSlot;
+  float* wtab = btab + warp * NP * 32;
+  const uint64_t nwg = len / 512;
+  const uint64_t wstride = gridDim.x * 8ull;
+  auto issue = [&](uint64_t gi, int k) {
+    if (gi < nwg) {
+      unsigned char* sl = ring + k * kSlot;
+#pragma unroll
+      for (int p = 0; p < NP; ++p) cp_async16(sl + p * 512 + lane * 16, pt.codes[p] + gi * 512 + lane * 16);
+      // block scales one float per lane: a chunk's scale pointer (e.g. the
+      // owner's slice of its own gradient) need not be 16-byte aligned
+      if (lane < 4 * NP) cp_async4(sl + NP * 512 + lane * 4, pt.scales[lane >> 2] + gi * 4 + (lane & 3));
+    }
+    cp_async_commit();
+  };
+  uint64_t wg = blockIdx.x * 8ull + warp;
+#pragma unroll
+  for (int k = 0; k < S - 1; ++k) issue(wg + k * wstride, k);
+  int slot = 0;
+  for (; wg < nwg; wg += wstride) {
+    __syncwarp();  // every lane is done reading the slot refilled next
+    issue(wg + (S - 1) * wstride, slot == 0 ? S - 1 : slot - 1);
+    cp_async_wait<S - 1>();
+    __syncwarp();
+    const unsigned char* sl = ring + slot * kSlot;
+    uint4 cv[NP];
+    float sc[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      cv[p] = lds128(sl + p * 512 + lane * 16);
+      sc[p] = reinterpret_cast<const float*>(sl + NP * 512)[p * 4 + (lane >> 3)];
+    }
+    reduce_compute<NP>(pt, wg * 512 + lane * 16, len, true, cv, sc, blk_base, lut, err, wtab);
+    slot = slot == S - 1 ? 0 : slot + 1;
+  }
+  cp_async_wait<0>();
+  // ragged tail (< 512 elements) in 16-element groups, warp-uniform trip count
+  const uint64_t ngroups = (len + kBlock - 1) / kBlock * 8;
+  const uint64_t gpad = (ngroups + 31) / 32 * 32;
+  for (uint64_t g = nwg * 32 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < gpad;
+       g += gridDim.x * (uint64_t)blockDim.x)
+    reduce_group<NP>(pt, g, g < ngroups ? len : 0, blk_base, lut, err, true, wtab);
+}
+
 // ---------------------------------------------------------------------------
 // allreduce_naive_fp8 strawman (collective.hpp:338-431), simulated on one
 // device: P-1 ring steps adding in FP8 at the receiver's ORIGINAL scales.
@@ -552,9 +614,49 @@ agq_status acc_tiled_prec(int prec, const uint8_t* codes, const float* scales,
   return launch_acc_tiled<BF16L, AGQ_ACC_FP32>(codes, scales, local, ntiles, oc, os, err, s);
 }
 
+// K4 kernel choice: the cp.async ring (default; AGQ_RED_STAGES = ring depth,
+// 2 unless set) or the direct-load kernel (AGQ_RED_PIPE=0, or unaligned
+// pointers / P > 8).
+int red_stages() {
+  static const int v = [] {
+    const char* e = getenv("AGQ_RED_PIPE");
+    if (e && e[0] == '0') return 0;
+    const char* st = getenv("AGQ_RED_STAGES");
+    const int k = st ? atoi(st) : 2;
+    return k < 2 ? 2 : (k > 4 ? 4 : k);
+  }();
+  return v;
+}
+
+template <int NP, int S>
+bool launch_reduce_pipe(const PieceTable& pt, uint64_t len, long long bb, agq_errors* err,
+                        cudaStream_t s) {
+  auto k = k_reduce128_pipe<NP, S>;
+  const size_t smem = (size_t)8 * S * (NP * 512 + NP * 16);
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, smem);
+  if (occ < 1) return false;
+  const uint64_t want = (len / 512 + 7) / 8;
+  const uint64_t cap = (uint64_t)num_sms() * occ;
+  const int grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
+  k<<<grid, 256, smem, s>>>(pt, len, bb, err);
+  return true;
+}
+
 template <int NP>
 void launch_reduce128(const PieceTable& pt, uint64_t len, long long bb, int vec, agq_errors* err,
                       cudaStream_t s) {
+  if constexpr (NP > 0) {
+    const int st = vec && len >= 512 ? red_stages() : 0;
+    if (st == 2 && launch_reduce_pipe<NP, 2>(pt, len, bb, err, s)) return;
+    if (st == 3 && launch_reduce_pipe<NP, 3>(pt, len, bb, err, s)) return;
+    if (st == 4 && launch_reduce_pipe<NP, 4>(pt, len, bb, err, s)) return;
+  }
   const uint64_t groups = (len + kBlock - 1) / kBlock * 8;
   int grid = gen_grid(groups, 256);
   k_reduce128<NP><<<grid, 256, 0, s>>>(pt, len, bb, vec, err);

@@ -304,3 +304,49 @@ def test_nan_codes_abort_like_the_reference(cuda):
     with pytest.raises(A.InvalidArgument) as got:
         A.local_accumulate(fp8q(codes, scales, cuda), t(local, cuda))
     assert str(got.value) == ref.value.args[-1]
+
+
+@pytest.mark.parametrize("n,world", [(512, 2), (513, 3), (1000, 8), (148 * 8 * 512 * 2 + 384, 4),
+                                     ((1 << 22) + 300, 7), (1 << 21, 1)])
+def test_reduce_pipeline_sizes(cuda, n, world):
+    """K4's cp.async-ring kernel (whole 512-element warp-groups, several
+    grid-stride rounds) plus its ragged tail, against the oracle."""
+    rng = np.random.default_rng(n + world)
+    codes, scales = [], []
+    for _ in range(world):
+        mag = np.repeat(10.0 ** rng.uniform(-6, 2, (n + 127) // 128), 128)[:n]
+        c, s = O.quantize((rng.standard_normal(n) * mag).astype(np.float32), 8, 128, O.FP8)
+        codes.append(c)
+        scales.append(s)
+    oc, os_ = O.allreduce_decomposed(codes, scales)
+    same(A.allreduce_simulated([fp8q(c, s, cuda) for c, s in zip(codes, scales)]), oc, os_)
+
+
+@pytest.mark.parametrize("world", [2, 5, 8])
+def test_reduce_unaligned_scale_pointers(cuda, world):
+    """The owner reduces a slice of its own gradient (chunk start = any block
+    index), so piece scale pointers are only 4-byte aligned."""
+    from paper_2605_00539_b200 import _lib as L
+    rng = np.random.default_rng(40 + world)
+    n = 128 * 1000
+    codes, scales = [], []
+    for _ in range(world):
+        c, s = O.quantize((rng.standard_normal(n) * 1e-3).astype(np.float32), 8, 128, O.FP8)
+        codes.append(c)
+        scales.append(s)
+    for skip in (1, 3):
+        lo = skip * 128
+        oc, os_ = O.allreduce_decomposed([c[lo:] for c in codes], [s[skip:] for s in scales])
+        dc = [torch.from_numpy(c).to(cuda) for c in codes]
+        ds = [torch.from_numpy(s).to(cuda) for s in scales]
+        out_c = torch.empty(n - lo, dtype=torch.uint8, device=cuda)
+        out_s = torch.empty(n // 128 - skip, dtype=torch.float32, device=cuda)
+        err = A.ErrorRecord(cuda).reset()
+        L.check(L.lib.agq_fp8_reduce_requant(
+            world, L.ptr_array([c[lo:].data_ptr() for c in dc]),
+            L.ptr_array([s[skip:].data_ptr() for s in ds]), n - lo, 128, 1,
+            L.ptr_array([out_c.data_ptr()]), L.ptr_array([out_s.data_ptr()]), err.ptr,
+            torch.cuda.current_stream().cuda_stream))
+        L.errors_message(err.read(), L.AGQ_OP_ALLREDUCE)
+        assert np.array_equal(out_c.cpu().numpy(), oc)
+        assert np.array_equal(u32(out_s.cpu().numpy()), u32(os_))

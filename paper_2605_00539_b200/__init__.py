@@ -14,7 +14,8 @@ from .codec import (CodecKind, ErrorRecord, QuantizedTensor, check_codec_args,
                     pack_codes, quantize_blockwise, quantize_grouped, roundtrip_relative_delta,
                     unpack_codes, validate)
 from .gradient import (AccumulatePrecision, ChunkAssignment, TraceEvent, allreduce_naive_simulated,
-                       allreduce_simulated, decomposed_trace, local_accumulate, round_bf16)
+                       allreduce_simulated, decomposed_trace, local_accumulate, naive_trace,
+                       round_bf16)
 from .dbca import (ActivationPolicy, ActivationStore, BitWidthPlan, LayerRole, PipelineConfig,
                    PolicyEntry, SaveStrategy, peak_memory_check, plan_bit_widths, plan_reuse_check,
                    stage_policy, stored_activation_counts)

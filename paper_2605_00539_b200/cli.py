@@ -80,7 +80,7 @@ def run_allreduce(args):
         trace = A.decomposed_trace(out.num_elements(), 128, args.workers)
     elif args.protocol == "naive":
         out, overflow = A.allreduce_naive_simulated(mains)
-        trace = None
+        trace = A.naive_trace(out.num_elements(), 128, args.workers)
     else:
         raise ValueError("--protocol: expected decomposed, naive or oracle")
     vals = A.dequantize_blockwise(out).double()

@@ -167,3 +167,29 @@ def decomposed_trace(n: int, block: int, world: int) -> list:
             if r != s:
                 ev.append(TraceEvent("all_gather", s, r, b, e - b, (e - b) + 4 * nsc))
     return ev
+
+
+def naive_trace(n: int, block: int, world: int) -> list:
+    """The MessageTrace allreduce_naive_fp8 records (collective.hpp:356-421):
+    P-1 ring steps in which rank r sends chunk (r - step) mod P to r+1, then
+    the all-gather of chunk c from its owner (c - 1) mod P to every other rank."""
+    a = ChunkAssignment.block_aligned(n, block, world).ranges
+
+    def payload(b, e):
+        return (e - b) + 4 * ((e + block - 1) // block - b // block)
+
+    ev = []
+    for step in range(world - 1):
+        for r in range(world):
+            b, e = a[(r - step) % world]
+            if b != e:
+                ev.append(TraceEvent("reduce_scatter", r, (r + 1) % world, b, e - b, payload(b, e)))
+    for c in range(world):
+        owner = 0 if world == 1 else (c - 1) % world
+        b, e = a[c]
+        if b == e:
+            continue
+        for r in range(world):
+            if r != owner:
+                ev.append(TraceEvent("all_gather", owner, r, b, e - b, payload(b, e)))
+    return ev

@@ -123,6 +123,25 @@ def test_trace_matches_reference(golden):
                 tuple(int(v) for v in r)
 
 
+@pytest.mark.parametrize("n,world", [(1024, 2), (1024, 4), (1024, 8), (300, 4), (128 * 7 + 5, 3), (64, 1)])
+def test_naive_trace_matches_reference(n, world):
+    """naive_trace == the MessageTrace of the reference's own
+    allreduce_naive_fp8 (collective.hpp:356-421), empty chunks included."""
+    rng = np.random.default_rng(n + world)
+    codes, scales = [], []
+    for _ in range(world):
+        c, s = O.quantize(rng.standard_normal(n).astype(np.float32), 8, 128, O.FP8)
+        codes.append(c)
+        scales.append(s)
+    ref = O.ref_allreduce(1, codes, scales)[3]
+    ev = A.naive_trace(n, 128, world)
+    assert len(ev) == len(ref)
+    for e, r in zip(ev, ref):
+        phase = {"all_to_all": 0, "all_gather": 1, "reduce_scatter": 2}[e.phase]
+        assert (phase, e.sender, e.receiver, e.chunk_start, e.chunk_len, e.payload_bytes) == \
+            tuple(int(v) for v in r)
+
+
 def test_scalar_formats_match_oracle():
     for b in range(256):
         x = O.orc.oracle_fp8_decode(b)

@@ -790,6 +790,9 @@ def main():
     if world > 1 and not args.no_allreduce:
         extra["allreduce"] = bench_allreduce(dev, args, world, rank, args.ar_elements)
     clk = clocks.stop()
+    for k in ("c1", "accumulate", "reduce_local"):  # per-kernel share of the HBM peak
+        if k in extra and "GBs" in extra[k]:
+            extra[k]["frac_of_peak"] = round(extra[k]["GBs"] / peak, 4)
 
     dom_name, dom_gbs, other = ("k_quant_warp", q_gbs, {"k_dequant_warp_GBs": round(d_gbs, 1)}) \
         if q_time >= d_time else ("k_dequant_warp", d_gbs, {"k_quant_warp_GBs": round(q_gbs, 1)})

@@ -348,6 +348,9 @@ constexpr int kWarpsPerCta = 8;
 #ifndef AGQ_QUANT_MINB
 #define AGQ_QUANT_MINB 3
 #endif
+#ifndef AGQ_QUANT_MINB_FP4
+#define AGQ_QUANT_MINB_FP4 AGQ_QUANT_MINB
+#endif
 #ifndef AGQ_DEQUANT_MINB
 #define AGQ_DEQUANT_MINB 3
 #endif
@@ -562,7 +565,8 @@ __device__ __forceinline__ void quant_tile(const SegTable& st, agq_errors* err, 
 }
 
 template <int BITS, int PACK, int CODEC, typename Tin>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tin) == 2 ? AGQ_QUANT_MINB : 2)
+__global__ void __launch_bounds__(kWarpsPerCta * 32,
+                                  sizeof(Tin) != 2 ? 2 : CODEC == AGQ_CODEC_FP4_E2M1 ? AGQ_QUANT_MINB_FP4 : AGQ_QUANT_MINB)
     k_quant_warp(SegTable st, agq_errors* err) {
   pdl_launch_dependents();
   pdl_wait();  // the previous kernel's outputs (our inputs) are visible

@@ -70,6 +70,17 @@ __device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) {
 #ifndef AGQ_ACC_TAB_BF16L
 #define AGQ_ACC_TAB_BF16L 0
 #endif
+// block-table decode also for the rounded-precision (BF16 / FP16 sum) K3
+#ifndef AGQ_ACC_TAB_PREC
+#define AGQ_ACC_TAB_PREC 0
+#endif
+// resident CTAs per SM for the FP32-local, BF16-rounded K3 instance: at 3 it
+// spills; 2 runs it 356 -> 315 us at 2^28 (70% -> 79% of HBM),
+// while the FP16-rounded instance is slower at 2 (325 -> 348 us) and keeps 3
+// (profiles/r01_acc_prec_ab.log)
+#ifndef AGQ_ACC_MINB_BF16R
+#define AGQ_ACC_MINB_BF16R 2
+#endif
 #ifndef AGQ_RED_TAB
 #define AGQ_RED_TAB 1
 #endif

@@ -200,7 +200,7 @@ __device__ __noinline__ void acc_report_nonfinite(const unsigned char* wb, int l
 }
 
 template <bool BF16L, int PREC>
-__global__ void __launch_bounds__(kAccWarps * 32, 3)
+__global__ void __launch_bounds__(kAccWarps * 32, !BF16L && PREC == AGQ_ACC_BF16 ? AGQ_ACC_MINB_BF16R : 3)
     k_accumulate_warp(const uint8_t* codes, const float* scales, const void* local,
                       uint64_t ntiles, uint8_t* out_codes, float* out_scales, agq_errors* err) {
   constexpr int kCh = BF16L ? 2 : 4;
@@ -264,7 +264,8 @@ __global__ void __launch_bounds__(kAccWarps * 32, 3)
     // block-table decode for the FP32-local / FP32-sum kernel (shared-memory
     // bound on the 256-entry table: 86% -> 93% of HBM); the BF16-local and
     // rounded-precision instances measured faster with the full table
-    constexpr bool kTab = AGQ_ACC_TAB && (!BF16L || AGQ_ACC_TAB_BF16L) && PREC == 0;
+    constexpr bool kTab = AGQ_ACC_TAB && (!BF16L || AGQ_ACC_TAB_BF16L) &&
+                          (PREC == 0 || AGQ_ACC_TAB_PREC);
     if (kTab && dq_fast(sc) && fp8_tab_ok16(cw)) {
       // v = l + dq (exact product, one rounding: = fadd(dq, l))
 #pragma unroll

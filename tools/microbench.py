@@ -79,7 +79,7 @@ def main():
                                       packed=False, check=False) for _ in range(R)]
         locs = [torch.randn(n, device=dev) * 1e-3 for _ in range(R)]
         err = A.ErrorRecord(dev).reset()
-        for prec in (0, 1):
+        for prec in (0, 1, 2):
             def fa(i):
                 m, l = mains[i % R], locs[i % R]
                 L.lib.agq_fp8_accumulate(m.codes.data_ptr(), m.scales.data_ptr(), l.data_ptr(), L.AGQ_F32, n,

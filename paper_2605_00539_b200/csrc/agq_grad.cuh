@@ -78,6 +78,10 @@ __device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) {
 // spills; 2 runs it 356 -> 315 us at 2^28 (70% -> 79% of HBM),
 // while the FP16-rounded instance is slower at 2 (325 -> 348 us) and keeps 3
 // (profiles/r01_acc_prec_ab.log)
+// resident CTAs per SM for the BF16-local K3 instances
+#ifndef AGQ_ACC_MINB_BF16L
+#define AGQ_ACC_MINB_BF16L 3
+#endif
 #ifndef AGQ_ACC_MINB_BF16R
 #define AGQ_ACC_MINB_BF16R 2
 #endif

@@ -200,7 +200,8 @@ __device__ __noinline__ void acc_report_nonfinite(const unsigned char* wb, int l
 }
 
 template <bool BF16L, int PREC>
-__global__ void __launch_bounds__(kAccWarps * 32, !BF16L && PREC == AGQ_ACC_BF16 ? AGQ_ACC_MINB_BF16R : 3)
+__global__ void __launch_bounds__(kAccWarps * 32, !BF16L && PREC == AGQ_ACC_BF16 ? AGQ_ACC_MINB_BF16R
+                                                  : BF16L && PREC != AGQ_ACC_BF16 ? AGQ_ACC_MINB_BF16L : 3)
     k_accumulate_warp(const uint8_t* codes, const float* scales, const void* local,
                       uint64_t ntiles, uint8_t* out_codes, float* out_scales, agq_errors* err) {
   constexpr int kCh = BF16L ? 2 : 4;

@@ -24,9 +24,19 @@ Also reported on the same line:
                of every stage -> host.
   roofline, cpu_baseline, clocks, gpu_launches: see the bench contract.
 
+Inputs: the activations are the reference's own bytes — make_rng(seed,
+0x1D, index = tensor) + std::normal_distribution<float> (tools/agq.cpp:47-65,
+rng.hpp:9-28; inputs.materialize), BF16-rounded; the reference arm draws the
+same stream through oracle/_ref, so both arms quantize identical values. The
+8e9-element gradient configs (C3/C4) are generated on the device
+(torch.Generator; SURVEY 8d allows counter-based generation at full size)
+and checked against the oracle on sampled blocks.
+
 `--impl reference` times the reference's own CPU implementation
 (oracle/_ref, the unmodified reference headers compiled as-is) of the same
-workload on a bounded sample, on all host threads.
+workload on a bounded sample, on all host threads, plus one pinned core. It
+imports nothing from the package (the stage widths are the literal
+STAGE_BITS, pinned by tests/test_bench_reference.py).
 """
 from __future__ import annotations
 
@@ -50,9 +60,15 @@ LLAMA8B_PARAMS = 8_030_261_248
 METRIC = "act quant+dequant GB/s vs HBM peak; INT8 grad all-reduce bus GB/s @1/2/4/8 GPU"
 
 
+# dbca.hpp:63-78 plan_bit_widths for 8 stages (= A.plan_bit_widths and the
+# oracle's; tests/test_bench_reference.py pins it)
+STAGE_BITS = (4, 4, 5, 5, 6, 7, 8, 8)
+TENSOR_SCALES = (1.0, 1.0, 0.5, 4.0, 1.0)  # per-tensor std
+SEED = 0
+
+
 def stage_bits():
-    import paper_2605_00539_b200 as A
-    return A.plan_bit_widths(A.PipelineConfig(8, 16, 2)).assigned()
+    return list(STAGE_BITS)
 
 
 def act_bytes_per_elem(bits):
@@ -159,10 +175,11 @@ class ActWorkload:
         from paper_2605_00539_b200 import _lib as L
         self.A, self.L, self.torch = A, L, torch
         self.dev = dev
-        g = torch.Generator(device=dev).manual_seed(seed)
-        scales = [1.0, 1.0, 0.5, 4.0, 1.0]  # per-tensor magnitudes
-        self.x = [(torch.randn(T_TOKENS * w, device=dev, generator=g) * s).to(torch.bfloat16)
-                  for (name, w), s in zip(TENSORS, scales)]
+        from paper_2605_00539_b200.inputs import materialize_parallel
+        host = materialize_parallel([T_TOKENS * w for _, w in TENSORS], seed, torch.bfloat16,
+                                    scales=TENSOR_SCALES)
+        self.x = [h.to(dev) for h in host]
+        del host
         self.n = [t.numel() for t in self.x]
         self.N = sum(self.n)
         self.bits = stage_bits()
@@ -190,7 +207,9 @@ class ActWorkload:
                                                      self.err.ptr, stream))
 
     def dequant(self, b, stream):
-        self.L.check(self.L.lib.agq_dequantize_grouped(self.segd[b], 5, self.L.AGQ_BF16, b, 0, stream))
+        # with the reference's validate checks (quantize.hpp:157-179)
+        self.L.check(self.L.lib.agq_dequantize_grouped(self.segd[b], 5, self.L.AGQ_BF16, b, 0, 1,
+                                                       self.err.ptr, stream))
 
     def step(self, stream, ev=None):
         for i, b in enumerate(self.bits):
@@ -204,23 +223,32 @@ class ActWorkload:
             if ev is not None:
                 ev[4 * i + 3].record()
 
-    def verify_sample(self):
-        """Bit-exact spot check of one block per tensor against the oracle."""
+    def verify_sample(self, nblk=16):
+        """Bit-exact check of `nblk` random blocks of every tensor at every
+        stage width against the oracle: packed codes, scales and the BF16
+        reconstruction (the full-size comparison is
+        tests/test_gpu_r02.py::test_c2_full_tensors_every_width)."""
         sys.path.insert(0, os.path.join(ROOT, "tests"))
         import numpy as np
         import oracle_ffi as O
-        b = self.bits[-1]
-        self.quant(b, self.torch.cuda.current_stream().cuda_stream)
-        self.torch.cuda.synchronize()
+        sp = self.torch.cuda.current_stream().cuda_stream
+        rng = np.random.default_rng(3)
         ok = True
-        for i in range(5):
-            blk = (self.n[i] // 128) // 2
-            x = self.x[i][blk * 128:(blk + 1) * 128].float().cpu().numpy()
-            c, s = O.quantize(x, b, 128, 0)
-            codes, scales = self.q[b][i]
-            got = codes[blk * 16 * b:(blk + 1) * 16 * b].cpu().numpy()
-            ok &= bool(np.array_equal(got, O.pack(c, b))) and float(scales[blk]) == float(s[0])
-        return ok
+        for b in sorted(set(self.bits)):
+            self.quant(b, sp)
+            self.dequant(b, sp)
+            self.torch.cuda.synchronize()
+            for i in range(5):
+                codes, scales = self.q[b][i]
+                for blk in rng.integers(0, self.n[i] // 128, nblk):
+                    x = self.x[i][blk * 128:(blk + 1) * 128].float().cpu().numpy()
+                    c, sc = O.quantize(x, b, 128, 0)
+                    got = codes[blk * 16 * b:(blk + 1) * 16 * b].cpu().numpy()
+                    ok &= bool(np.array_equal(got, O.pack(c, b))) and float(scales[blk]) == float(sc[0])
+                    y = self.out[i][blk * 128:(blk + 1) * 128].float().cpu().numpy()
+                    ok &= bool(np.array_equal(y.view(np.uint32),
+                                              O.bf16_round(O.dequantize(c, sc, b)).view(np.uint32)))
+        return bool(ok)
 
 
 def bench_act(wl, args, world):
@@ -255,7 +283,9 @@ def bench_act(wl, args, world):
             dt.append(ev[base + 2].elapsed_time(ev[base + 3]) * 1e-3)
             qb.append(wl.N * act_bytes_per_elem(b)[0])
             db.append(wl.N * act_bytes_per_elem(b)[1])
-    wl.L.errors_message(wl.err.read(), wl.L.AGQ_OP_QUANTIZE)
+    h = wl.err.read()
+    wl.L.errors_message(h, wl.L.AGQ_OP_QUANTIZE)
+    wl.L.errors_message(h, wl.L.AGQ_OP_DEQUANTIZE)
     return sec, launches, (sum(qb) / sum(qt) / 1e9, sum(qt)), (sum(db) / sum(dt) / 1e9, sum(dt))
 
 
@@ -308,7 +338,8 @@ def bench_e2e(wl, args, world, steps, chunks=16, nstreams=4):
                     wl.x[i][e0:e1].copy_(host_in[i][e0:e1], non_blocking=True)
                 for b in wl.bits:
                     L.check(L.lib.agq_quantize_grouped(segq[b], 5, L.AGQ_BF16, b, 0, wl.err.ptr, sp))
-                    L.check(L.lib.agq_dequantize_grouped(segd[b], 5, L.AGQ_BF16, b, 0, sp))
+                    L.check(L.lib.agq_dequantize_grouped(segd[b], 5, L.AGQ_BF16, b, 0, 1,
+                                                         wl.err.ptr, sp))
                     for i, (e0, e1) in enumerate(rng):
                         host_out[i][e0:e1].copy_(wl.out[i][e0:e1], non_blocking=True)
         for st in streams:
@@ -324,7 +355,9 @@ def bench_e2e(wl, args, world, steps, chunks=16, nstreams=4):
     e.record()
     torch.cuda.synchronize()
     sec = max_over_ranks(s.elapsed_time(e) * 1e-3, world)
-    wl.L.errors_message(wl.err.read(), wl.L.AGQ_OP_QUANTIZE)
+    h = wl.err.read()
+    wl.L.errors_message(h, wl.L.AGQ_OP_QUANTIZE)
+    wl.L.errors_message(h, wl.L.AGQ_OP_DEQUANTIZE)
     # the result read back must equal the device result of the last stage
     last = wl.bits[-1]
     ok = all(torch.equal(h[:4096], o[:4096].cpu()) for h, o in zip(host_out, wl.out))
@@ -341,9 +374,10 @@ def bench_c1(dev, args):
     (1.6 GB) so every launch streams from HBM, not the 126 MB L2."""
     import torch
     from paper_2605_00539_b200 import _lib as L
+    from paper_2605_00539_b200.inputs import materialize_parallel
     n, R = 4096 * 4096, 16
-    g = torch.Generator(device=dev).manual_seed(11)
-    xs = [torch.randn(n, device=dev, generator=g).to(torch.bfloat16) for _ in range(R)]
+    # copy 0 = the reference CLI's `--seed 1 --normal 16777216` bytes (BF16)
+    xs = [h.to(dev) for h in materialize_parallel([n] * R, 1, torch.bfloat16)]
     cs = [torch.empty(n // 2, dtype=torch.uint8, device=dev) for _ in range(R)]
     ss = [torch.empty(n // 128, dtype=torch.float32, device=dev) for _ in range(R)]
     ys = [torch.empty_like(xs[0]) for _ in range(R)]
@@ -657,45 +691,76 @@ def load_traffic():
 # ---------------------------------------------------------------------------
 # the reference's CPU implementation (oracle/_ref) on a bounded sample
 # ---------------------------------------------------------------------------
-def cpu_reference_rate(sample_elems, threads, rounds=1, min_seconds=0.0):
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_reference_rate(sample_elems, threads, rounds=1, min_seconds=0.0, pin_core=None):
     """GB/s (same algorithmic bytes as the GPU arm) of quantize_blockwise +
-    dequantize_blockwise of the reference over every stage width, on
-    `sample_elems` BF16-valued inputs, `threads` host threads over disjoint
-    block ranges (blocks are independent, quantize.hpp:103-136)."""
+    dequantize_blockwise of the reference over every stage width, on the
+    first `sample_elems` values of the GPU arm's first C2 tensor (the same
+    make_rng(SEED, 0x1D, 0) normal draws, BF16-rounded), `threads` host
+    threads over disjoint block ranges (blocks are independent,
+    quantize.hpp:103-136). pin_core: run on that one core only (taskset)."""
     import numpy as np
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_ffi as O
     kind = "reference" if O.ref is not None else "port"
     lib = O.ref if O.ref is not None else None
-    rng = np.random.default_rng(0)
-    x = O.bf16_round(rng.standard_normal(sample_elems).astype(np.float32))
+    if lib is not None:
+        x = O.bf16_round(O.ref_normal(SEED, 0x1D, 0, sample_elems))
+    else:
+        x = O.bf16_round(np.random.default_rng(SEED).standard_normal(sample_elems).astype(np.float32))
     codes = np.empty(sample_elems, np.uint8)
     scales = np.empty((sample_elems + 127) // 128, np.float32)
     out = np.empty(sample_elems, np.float32)
-    bits = stage_bits()
-    t0 = time.perf_counter()
-    nbytes = 0.0
-    r = 0
-    while r < rounds or time.perf_counter() - t0 < min_seconds:
-        r += 1
-        for b in bits:
-            if lib is not None:
-                st = lib.ref_quantize_mt(O._p(x), sample_elems, b, 128, 0, O._p(codes), O._p(scales), threads)
-                st |= lib.ref_dequantize_mt(O._p(codes), O._p(scales), sample_elems, b, 128, 0, O._p(out),
-                                            threads)
-                assert st == 0
-            else:
-                c, s = O.quantize(x, b, 128, 0)
-                O.dequantize(c, s, b, 128, 0)
-            nbytes += sample_elems * sum(act_bytes_per_elem(b))
-    sec = time.perf_counter() - t0
+    old = None
+    if pin_core is not None and hasattr(os, "sched_setaffinity"):
+        old = os.sched_getaffinity(0)
+        os.sched_setaffinity(0, {pin_core})
+    try:
+        t0 = time.perf_counter()
+        nbytes = 0.0
+        r = 0
+        while r < rounds or time.perf_counter() - t0 < min_seconds:
+            r += 1
+            for b in STAGE_BITS:
+                if lib is not None:
+                    st = lib.ref_quantize_mt(O._p(x), sample_elems, b, 128, 0, O._p(codes),
+                                             O._p(scales), threads)
+                    st |= lib.ref_dequantize_mt(O._p(codes), O._p(scales), sample_elems, b, 128, 0,
+                                                O._p(out), threads)
+                    assert st == 0
+                else:
+                    c, sc = O.quantize(x, b, 128, 0)
+                    O.dequantize(c, sc, b, 128, 0)
+                nbytes += sample_elems * sum(act_bytes_per_elem(b))
+        sec = time.perf_counter() - t0
+    finally:
+        if old is not None:
+            os.sched_setaffinity(0, old)
     return nbytes / sec / 1e9, kind, sec
 
 
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
 def run_reference(args, world, rank):
+    """The reference arm: oracle/_ref (the unmodified reference headers) on
+    the host cores; loads no library of this repo's package."""
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
+    threads = host_threads()
     sample = 1 << 24
     for _ in range(args.warmup):
         cpu_reference_rate(sample, threads)
@@ -706,16 +771,27 @@ def run_reference(args, world, rank):
         vals.append(v)
     sec = time.perf_counter() - t0
     value = sum(vals) / len(vals)
+    v1, _, s1 = cpu_reference_rate(1 << 22, 1, pin_core=sorted(os.sched_getaffinity(0))[0])
     line = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(sec / args.steps * 1e3, 1), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8 codes / f32 scales (bf16-valued f32 in)",
-            "data": "synthetic N(0,1) rounded to bf16", "impl": "reference",
-            "config": {"workload": "C2 sample: quantize_blockwise+dequantize_blockwise, block 128, "
-                                   "SymmetricLinear, every 8-stage DBCA width (4,4,5,5,6,7,8,8)",
-                       "sample_elements_per_stage": sample},
+            "data": "synthetic: make_rng(0, 0x1D) N(0,1) draws rounded to bf16 (the GPU arm's "
+                    "first C2 tensor)", "impl": "reference",
+            "config": {"workload": "C2: LLaMA-8B block stored activations (seq 4096 x mb 4), "
+                                   "8-stage DBCA policies, quant+dequant",
+                       "stage_bits": list(STAGE_BITS), "block": 128,
+                       "sample_elements_per_stage": sample,
+                       "sample": "each step quantizes+dequantizes a 2^24-element sample of the "
+                                 "workload at every stage width (the full 671M-element step is "
+                                 "~10 min of CPU time)"},
             "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads, "kind": kind,
-                             "sample": f"{sample} elements x 8 stage widths per step"},
+                             "sample": f"{sample} elements x 8 stage widths per step",
+                             "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+                             "single_core": {"value": round(v1, 4), "unit": "GB/s", "cores": 1,
+                                             "pinned": "taskset core 0 (sched_setaffinity)",
+                                             "sample": "2^22 elements x 8 stage widths",
+                                             "seconds": round(s1, 2)}},
             "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -815,11 +891,16 @@ def main():
             "roofline": roofline, "gpu_launches": launches, "parity_sample_bitexact": parity,
             "clocks": clk, **extra}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, kind, csec = cpu_reference_rate(1 << 24, os.cpu_count() or 1, min_seconds=8.0)
-        line["cpu_baseline"] = {"value": round(v, 3), "unit": "GB/s", "cores": os.cpu_count() or 1,
-                                "kind": kind,
-                                "sample": f"2^24 BF16-valued elements x 8 stage widths, repeated "
-                                          f"for {csec:.1f} s of CPU time"}
+        th = host_threads()
+        v, kind, csec = cpu_reference_rate(1 << 24, th, min_seconds=8.0)
+        v1, _, s1 = cpu_reference_rate(1 << 22, 1, pin_core=sorted(os.sched_getaffinity(0))[0])
+        line["cpu_baseline"] = {"value": round(v, 3), "unit": "GB/s", "cores": th,
+                                "kind": kind, "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+                                "sample": f"2^24 elements of the first C2 tensor (same bytes) x 8 "
+                                          f"stage widths, repeated for {csec:.1f} s of CPU time",
+                                "single_core": {"value": round(v1, 4), "unit": "GB/s", "cores": 1,
+                                                "pinned": "core 0 (sched_setaffinity)",
+                                                "sample": "2^22 elements x 8 stage widths"}}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

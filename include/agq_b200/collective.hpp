@@ -115,6 +115,7 @@ inline QuantizedTensor local_accumulate(const QuantizedTensor& main,
     throw std::invalid_argument("main gradient must be FP8 E4M3");
   if (main.num_elements() != local_grad.size())
     throw std::invalid_argument("local gradient shape mismatch");
+  detail::validate_structure(main);  // dequantize_blockwise(main) validates first
   QuantizedTensor out = main;
   detail::throw_status(agq_local_accumulate_host(main.codes.data(), main.scales.data(),
                                                  main.num_elements(), main.block_size,

@@ -121,13 +121,19 @@ typedef struct {
 } agq_segment;
 
 /* Grouped launch over the tensors one pipeline stage stores (dbca.hpp:172-177
- * stage_policy -> layers.hpp:64-75 agoq_default(bits)). All segments share
- * bits/codec/dtype; block is 128. */
+ * stage_policy -> layers.hpp:64-75 agoq_default(bits), layers.hpp:266-301
+ * the stored set of every layer of the stage). All segments share
+ * bits/codec/dtype; block is 128. Any segment count: up to 32 segments go
+ * into one launch, larger groups are split. Error indices in d_err are
+ * group-global (blocks / elements counted over the segments in order).
+ * validate != 0 performs the reference's dequantize-time checks
+ * (quantize.hpp:157-179: code range, finite non-negative scales). */
 agq_status agq_quantize_grouped(const agq_segment* segs, int nseg, int x_dtype,
                                 int bits, int codec, agq_errors* d_err,
                                 agq_stream_t stream);
 agq_status agq_dequantize_grouped(const agq_segment* segs, int nseg,
                                   int out_dtype, int bits, int codec,
+                                  int validate, agq_errors* d_err,
                                   agq_stream_t stream);
 
 /* tensor_io.hpp:63-100 on device */
@@ -208,6 +214,37 @@ agq_status agq_comm_p2p_buffers(agq_comm* comm, uint8_t** codes, float** scales)
 agq_status agq_comm_destroy(agq_comm* comm);
 int agq_comm_rank(const agq_comm* comm);
 int agq_comm_size(const agq_comm* comm);
+/* Device barrier timeout of the P2P algorithms (default 300 s). A barrier
+ * that times out (a peer that never arrived) makes the call report
+ * "all-reduce aborted: peer did not arrive (timeout)" and marks the
+ * communicator failed on every rank: later P2P calls fail fast; destroy and
+ * re-create the communicator. */
+agq_status agq_comm_set_timeout(agq_comm* comm, double seconds);
+
+/* One message of the decomposed all-reduce, as collective.hpp:50-57
+ * TraceEvent (phase 0 = "all_to_all", 1 = "all_gather"; payload = codes +
+ * 4 bytes per block scale, collective.hpp:195-206 deliver). */
+typedef struct {
+  int phase;
+  int sender;
+  int receiver;
+  int reserved;
+  uint64_t chunk_start;
+  uint64_t chunk_len;
+  uint64_t payload_bytes;
+} agq_trace_event;
+
+/* The messages this rank took part in during its last agq_allreduce_fp8
+ * call, recorded by the code that issued the transfers (NCCL: every
+ * send this rank posted; fused P2P: the chunk-r pulls from every peer and
+ * the pushes of the reduced chunk; push P2P: the scatters and pushes). The
+ * union over all ranks, sorted by (phase, sender, receiver), is the
+ * reference's MessageTrace. *count = number of events (may exceed cap).
+ * moved (2 entries, or NULL): for the P2P algorithms the kernel's own
+ * counters of the phase-1 traffic (elements, block scales), synchronising
+ * the call's stream; zeros for NCCL. */
+agq_status agq_comm_last_trace(agq_comm* comm, agq_trace_event* events, int cap,
+                               int* count, unsigned long long* moved);
 
 /* Replaces allreduce_decomposed for real ranks: in-place on this rank's FP8
  * gradient (codes one byte/element + block scales). All ranks call it with
@@ -254,6 +291,18 @@ agq_status agq_allreduce_simulated_host(int world, const uint8_t* const* codes,
                                         uint8_t* out_codes, float* out_scales,
                                         uint64_t* overflow_elements,
                                         uint64_t* overflow_events /* world, or NULL */);
+
+/* ---- synthetic inputs (host) ---------------------------------------------- */
+/* tools/agq.cpp:47-65 InputSpec::materialize + rng.hpp:9-28 make_rng(seed,
+ * stream, index): std::mt19937_64(derive_seed(...)) driving
+ * std::normal_distribution<float>(a, b) (the CLI: a=0, b=1, stream 0x1D,
+ * index 0), std::uniform_real_distribution<float>(a, b) or the constant a —
+ * the reference's bytes (same libstdc++). out: HOST buffer of n F32 values,
+ * or BF16 = their round-to-nearest-even. All-reduce worker r of the CLI uses
+ * seed + r (agq.cpp:279). */
+enum { AGQ_INPUT_NORMAL = 0, AGQ_INPUT_UNIFORM = 1, AGQ_INPUT_CONST = 2 };
+agq_status agq_fill_input(uint64_t seed, uint64_t stream, uint64_t index, int kind,
+                          double a, double b, int out_dtype, void* out, uint64_t n);
 
 /* ---- L2b control plane (dbca.hpp, host) ---------------------------------- */
 /* dbca.hpp:34-41 stored_activation_counts; counts[n_stages]. */

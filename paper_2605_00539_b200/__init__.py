@@ -17,7 +17,8 @@ from .gradient import (AccumulatePrecision, ChunkAssignment, TraceEvent, allredu
                        allreduce_simulated, decomposed_trace, local_accumulate, naive_trace,
                        round_bf16)
 from .dbca import (ActivationPolicy, ActivationStore, BitWidthPlan, LayerRole, PipelineConfig,
-                   PolicyEntry, SaveStrategy, peak_memory_check, plan_bit_widths, plan_reuse_check,
+                   PolicyEntry, SaveStrategy, StageActivationStore, peak_memory_check,
+                   plan_bit_widths, plan_reuse_check,
                    stage_policy, stored_activation_counts)
 from .scalar import fp4_decode, fp4_encode, fp8_decode, fp8_encode
 

@@ -34,6 +34,14 @@ class AgqErrors(C.Structure):
     ]
 
 
+class AgqTraceEvent(C.Structure):
+    """Mirror of agq_trace_event (collective.hpp:50-57 TraceEvent)."""
+
+    _fields_ = [("phase", C.c_int), ("sender", C.c_int), ("receiver", C.c_int),
+                ("reserved", C.c_int), ("chunk_start", C.c_uint64), ("chunk_len", C.c_uint64),
+                ("payload_bytes", C.c_uint64)]
+
+
 class AgqSegment(C.Structure):
     _fields_ = [("x", C.c_void_p), ("codes", C.c_void_p), ("scales", C.c_void_p),
                 ("n", C.c_uint64)]
@@ -71,7 +79,7 @@ def _load() -> C.CDLL:
         "agq_quantize": (I, [P, I, U64, I, U32, I, P, I, P, P, S]),
         "agq_dequantize": (I, [P, I, P, U64, I, U32, I, P, I, I, P, S]),
         "agq_quantize_grouped": (I, [C.POINTER(AgqSegment), I, I, I, I, P, S]),
-        "agq_dequantize_grouped": (I, [C.POINTER(AgqSegment), I, I, I, I, S]),
+        "agq_dequantize_grouped": (I, [C.POINTER(AgqSegment), I, I, I, I, I, P, S]),
         "agq_pack_codes": (I, [P, U64, I, P, S]),
         "agq_unpack_codes": (I, [P, U64, I, P, S]),
         "agq_fp8_accumulate": (I, [P, P, P, I, U64, U32, I, P, P, P, S]),
@@ -90,6 +98,11 @@ def _load() -> C.CDLL:
         "agq_comm_destroy": (I, [P]),
         "agq_comm_rank": (I, [P]),
         "agq_comm_size": (I, [P]),
+        "agq_comm_set_timeout": (I, [P, C.c_double]),
+        "agq_comm_last_trace": (I, [P, C.POINTER(AgqTraceEvent), I, C.POINTER(C.c_int),
+                                    C.POINTER(C.c_ulonglong)]),
+        "agq_fill_input": (I, [C.c_uint64, C.c_uint64, C.c_uint64, I, C.c_double, C.c_double,
+                               I, P, U64]),
         "agq_allreduce_fp8": (I, [P, P, P, U64, U32, I, P, S]),
         "agq_allreduce_naive_fp8": (I, [P, P, P, U64, U32, P, P, S]),
         "agq_allreduce_bf16_nccl": (I, [P, P, U64, S]),
@@ -119,6 +132,7 @@ EXPORTED = (
     "agq_fp8_accumulate agq_fp8_reduce_requant agq_chunk_assignment agq_allreduce_simulated "
     "agq_allreduce_naive_simulated agq_comm_unique_id agq_comm_init agq_comm_p2p_export "
     "agq_comm_p2p_open agq_comm_p2p_buffers agq_comm_destroy agq_comm_rank agq_comm_size "
+    "agq_comm_set_timeout agq_comm_last_trace agq_fill_input "
     "agq_allreduce_fp8 agq_allreduce_naive_fp8 agq_allreduce_bf16_nccl agq_quantize_host agq_dequantize_host "
     "agq_local_accumulate_host agq_allreduce_simulated_host agq_stored_activation_counts "
     "agq_plan_bit_widths").split()

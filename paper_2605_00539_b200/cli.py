@@ -1,9 +1,10 @@
 """`agq`-shaped command line over the B200 path (reference harness:
 /root/reference/proj/tools/agq.cpp:114-152 run_quantize, :240-272 run_dbca,
 :274-324 run_allreduce). Same subcommands, flags and JSON keys; the compute
-runs on the GPU. Inputs are drawn on the device (torch.Generator(seed)), so
-statistics match the reference's in distribution, not bit for bit; exact
-parity is what tests/ check with shared inputs.
+runs on the GPU. Inputs are the reference's own bytes (inputs.materialize:
+make_rng(seed, 0x1D) + std::normal_distribution<float>, agq.cpp:47-65), and
+the statistics are summed on the host in the reference's order, so the JSON
+equals the reference CLI's bit for bit.
 
   python -m paper_2605_00539_b200.cli quantize --normal 4096 --bits 4 [--codec linear] [--dump f]
   python -m paper_2605_00539_b200.cli allreduce-sim --workers 8 --elements 4096 --protocol decomposed
@@ -21,17 +22,24 @@ NAMES = {0: "symmetric_linear", 1: "fp4_e2m1", 2: "fp8_e4m3"}
 
 
 def _input(args, seed, n_default):
-    import torch
+    from paper_2605_00539_b200.inputs import materialize
     n = args.normal or args.elements or n_default
-    g = torch.Generator(device="cuda").manual_seed(seed)
     if args.const is not None:
-        return torch.full((n,), float(args.const), device="cuda")
-    if args.uniform:
+        x = materialize(n, seed, "const", float(args.const))
+    elif args.uniform:
         a, b = args.uniform
         if not a <= b:
             raise ValueError("--uniform needs a <= b")
-        return torch.rand(n, device="cuda", generator=g) * (b - a) + a
-    return torch.randn(n, device="cuda", generator=g)
+        x = materialize(n, seed, "uniform", a, b)
+    else:
+        x = materialize(n, seed, "normal", 0.0, 1.0)
+    return x.cuda()
+
+
+def _seq_sum(v):
+    """Left-to-right double sum (the reference's loops, agq.cpp:123-128)."""
+    import numpy as np
+    return float(np.add.accumulate(np.asarray(v, np.float64))[-1]) if len(v) else 0.0
 
 
 def run_quantize(args):
@@ -41,13 +49,14 @@ def run_quantize(args):
     x = _input(args, args.seed, 4096)
     kind = A.CodecKind(CODECS[args.codec])
     q = A.quantize_blockwise(x, args.bits, args.block, kind)
-    back = A.dequantize_blockwise(q).double()
-    xd = x.double()
-    err = (back - xd).abs()
+    back = A.dequantize_blockwise(q).double().cpu().numpy()
+    xd = x.double().cpu().numpy()
+    err = abs(back - xd)  # exact in double (both are floats)
     nz = xd != 0
     stats = {"elements": x.numel(), "bit_width": args.bits, "block_size": args.block,
-             "codec": NAMES[int(kind)], "mae": float(err.mean()), "max_abs_error": float(err.max()),
-             "max_rel_error": float((err[nz] / xd[nz].abs()).max()) if bool(nz.any()) else 0.0,
+             "codec": NAMES[int(kind)], "mae": _seq_sum(err) / x.numel(),
+             "max_abs_error": float(err.max()),
+             "max_rel_error": float((err[nz] / abs(xd[nz])).max()) if bool(nz.any()) else 0.0,
              "compression_ratio": 4.0 * x.numel() / (math.ceil(x.numel() * args.bits / 8)
                                                      + 4.0 * q.num_blocks())}
     if args.dump:
@@ -73,7 +82,8 @@ def run_allreduce(args):
         oracle += A.dequantize_blockwise(m)
     j = {"protocol": args.protocol, "workers": args.workers, "elements": mains[0].num_elements()}
     if args.protocol == "oracle":
-        j["oracle_l2"] = float(oracle.double().norm())
+        o = oracle.double().cpu().numpy()
+        j["oracle_l2"] = math.sqrt(_seq_sum(o * o))
         return j
     if args.protocol == "decomposed":
         out, overflow = A.allreduce_simulated(mains), 0
@@ -83,9 +93,9 @@ def run_allreduce(args):
         trace = A.naive_trace(out.num_elements(), 128, args.workers)
     else:
         raise ValueError("--protocol: expected decomposed, naive or oracle")
-    vals = A.dequantize_blockwise(out).double()
-    j["result_l2"] = float(vals.norm())
-    j["max_abs_dev_vs_oracle"] = float((vals - oracle.double()).abs().max())
+    vals = A.dequantize_blockwise(out).double().cpu().numpy()
+    j["max_abs_dev_vs_oracle"] = float(abs(vals - oracle.double().cpu().numpy()).max())
+    j["result_l2"] = math.sqrt(_seq_sum(vals * vals))
     j["overflow_total"] = int(overflow)
     if trace is not None:
         j["message_count"] = len(trace)
@@ -143,7 +153,7 @@ def main(argv=None):
     except Exception as e:  # agq.cpp:433-442: JSON error on stderr, non-zero exit
         print(json.dumps({"error": str(e)}), file=sys.stderr)
         return 1
-    text = json.dumps(res, indent=2)
+    text = json.dumps(res, indent=2, sort_keys=True)  # nlohmann::json orders keys
     if args.out:
         with open(args.out, "w") as f:
             f.write(text + "\n")

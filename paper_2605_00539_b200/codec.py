@@ -140,6 +140,9 @@ def validate(q: QuantizedTensor) -> None:
         raise L.InvalidArgument("quantized tensor: shape/code count mismatch")
 
 
+_validate = validate  # (dequantize_grouped's `validate` flag shadows the name)
+
+
 def dequantize_blockwise(q: QuantizedTensor, out_dtype: torch.dtype = torch.float32,
                          stream=None, check: bool = True, out: torch.Tensor | None = None,
                          errors: ErrorRecord | None = None) -> torch.Tensor:
@@ -197,13 +200,53 @@ def unpack_codes(packed: torch.Tensor, bit_width: int, count: int, stream=None) 
     return out
 
 
+def _raise_grouped(err: "ErrorRecord", op: int, ns: Sequence[int]) -> None:
+    """Raise the reference's exception for the first failing tensor of a
+    grouped call. The device record holds group-global indices (blocks, and
+    elements in block-padded coordinates); the reference processes the
+    tensors one after the other, so the tensor with the lowest index fails
+    first, with its own check order (code range before scales) and its own
+    local index in the message. The exception carries `.segment`."""
+    h = err.read()
+    base = [0]
+    for n in ns:
+        base.append(base[-1] + (int(n) + 127) // 128)
+
+    def seg_of(blk: int) -> int:
+        for j in range(len(ns)):
+            if blk < base[j + 1]:
+                return j
+        return len(ns) - 1
+
+    fields = {"nonfinite_block": 1, "bad_code_index": 128, "bad_scale_block": 1}
+    hits = []
+    order = ["bad_code_index", "bad_scale_block"] if op == L.AGQ_OP_DEQUANTIZE else ["nonfinite_block"]
+    for rank, name in enumerate(order):
+        v = getattr(h, name)
+        if v != L.INT64_MAX:
+            hits.append((seg_of(v // fields[name]), rank, name, v))
+    if not hits:
+        return
+    j, _, name, v = min(hits)
+    loc = L.AgqErrors(L.INT64_MAX, L.INT64_MAX, L.INT64_MAX, L.INT64_MAX, L.INT64_MAX, 0)
+    setattr(loc, name, v - base[j] * fields[name])
+    try:
+        L.errors_message(loc, op)
+    except (L.InvalidArgument, L.ProtocolError) as e:
+        e.segment = j
+        raise
+
+
 def quantize_grouped(xs: Sequence[torch.Tensor], bit_width: int,
                      kind: CodecKind = CodecKind.SymmetricLinear, stream=None,
                      check: bool = True, errors: ErrorRecord | None = None,
                      outs: Sequence[QuantizedTensor] | None = None) -> list[QuantizedTensor]:
-    """One launch over all tensors a pipeline stage stores (block 128, packed)."""
+    """One launch (per 32 tensors) over all tensors a pipeline stage stores
+    (layers.hpp:266-301 for every layer of the stage, dbca.hpp:172-177 width;
+    block 128, packed)."""
     if not xs:
         return []
+    check_codec_args(bit_width, 128, kind)
     dt = _dtype_code(xs[0])
     qs = list(outs) if outs is not None else []
     segs = (L.AgqSegment * len(xs))()
@@ -227,12 +270,18 @@ def quantize_grouped(xs: Sequence[torch.Tensor], bit_width: int,
     L.check(L.lib.agq_quantize_grouped(segs, len(xs), dt, bit_width, int(kind),
                                        err.ptr if err is not None else None, _stream(stream)))
     if check and err is not None:
-        err.raise_if_any(L.AGQ_OP_QUANTIZE)
+        _raise_grouped(err, L.AGQ_OP_QUANTIZE, [x.numel() for x in xs])
     return qs
 
 
 def dequantize_grouped(qs: Sequence[QuantizedTensor], out_dtype: torch.dtype = torch.bfloat16,
-                       stream=None, outs: Sequence[torch.Tensor] | None = None) -> list[torch.Tensor]:
+                       stream=None, outs: Sequence[torch.Tensor] | None = None,
+                       check: bool = True, errors: ErrorRecord | None = None,
+                       validate: bool = True) -> list[torch.Tensor]:
+    """dequantize_blockwise (quantize.hpp:178-189, validate :157-176 first)
+    over a group of packed block-128 tensors in one launch per 32 tensors.
+    With validate the device checks code range and scales of every tensor;
+    `check` reads the record and raises the reference's exception."""
     if not qs:
         return []
     res = list(outs) if outs is not None else [
@@ -241,10 +290,20 @@ def dequantize_grouped(qs: Sequence[QuantizedTensor], out_dtype: torch.dtype = t
     for i, q in enumerate(qs):
         if q.bit_width != qs[0].bit_width or q.codec_kind != qs[0].codec_kind or not q.packed:
             raise L.InvalidArgument("grouped tensors must share bits/codec and be packed")
+        if q.block_size != 128:
+            raise L.InvalidArgument("grouped tensors use block 128")
+        _validate(q)
         segs[i] = L.AgqSegment(res[i].data_ptr(), q.codes.data_ptr(), q.scales.data_ptr(),
                                q.num_elements())
+    err = errors if errors is not None else (
+        ErrorRecord(qs[0].codes.device) if (validate or check) else None)
+    if err is not None:
+        err.reset(stream)
     L.check(L.lib.agq_dequantize_grouped(segs, len(qs), _dtype_code(res[0]), qs[0].bit_width,
-                                         int(qs[0].codec_kind), _stream(stream)))
+                                         int(qs[0].codec_kind), 1 if validate else 0,
+                                         err.ptr if err is not None else None, _stream(stream)))
+    if check and validate and err is not None:
+        _raise_grouped(err, L.AGQ_OP_DEQUANTIZE, [q.num_elements() for q in qs])
     return res
 
 

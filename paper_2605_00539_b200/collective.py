@@ -13,7 +13,10 @@ import ctypes as C
 import torch
 
 from . import _lib as L
-from .codec import CodecKind, ErrorRecord, QuantizedTensor, _stream
+from .codec import CodecKind, ErrorRecord, QuantizedTensor, _stream, validate
+from .gradient import TraceEvent
+
+PHASES = ("all_to_all", "all_gather")
 
 
 class _CudaArray:
@@ -27,7 +30,8 @@ class _CudaArray:
 class Communicator:
     ALGOS = {"nccl": L.AGQ_AR_NCCL, "p2p": L.AGQ_AR_FUSED_P2P, "push": L.AGQ_AR_PUSH_P2P}
 
-    def __init__(self, group=None, device: int | None = None, p2p_capacity: int = 0):
+    def __init__(self, group=None, device: int | None = None, p2p_capacity: int = 0,
+                 timeout_s: float | None = None):
         import torch.distributed as dist
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
@@ -42,6 +46,8 @@ class Communicator:
         L.check(L.lib.agq_comm_init(C.byref(self._h), uid, self.world, self.rank, self.device))
         self._group = group
         self.p2p_capacity = 0
+        if timeout_s is not None:
+            self.set_timeout(timeout_s)
         if p2p_capacity:
             self.enable_p2p(p2p_capacity)
 
@@ -83,13 +89,19 @@ class Communicator:
         scales = torch.as_tensor(_CudaArray(s.value, nb, "<f4"), device=f"cuda:{self.device}")
         return codes, scales
 
-    def _in_p2p_buffers(self, q: QuantizedTensor) -> bool:
-        if not self.p2p_capacity or q.num_elements() > self.p2p_capacity or q.block_size != 128:
-            return False
-        c = C.c_void_p()
-        sc = C.c_void_p()
-        L.check(L.lib.agq_comm_p2p_buffers(self._h, C.byref(c), C.byref(sc)))
-        return q.codes.data_ptr() == c.value and q.scales.data_ptr() == sc.value
+    def set_timeout(self, seconds: float):
+        """Device barrier timeout of the P2P algorithms (default 300 s). A
+        timeout aborts the call on every rank ("peer did not arrive") and
+        leaves the communicator failed: re-create it."""
+        L.check(L.lib.agq_comm_set_timeout(self._h, float(seconds)))
+
+    def _auto_algo(self, q: QuantizedTensor) -> str:
+        # Depends only on state every rank shares (the collective
+        # enable_p2p capacity, and n / block, equal on all ranks), never on
+        # where this rank's tensor lives, so all ranks pick the same algorithm.
+        if self.p2p_capacity and q.num_elements() <= self.p2p_capacity and q.block_size == 128:
+            return "p2p"
+        return "nccl"
 
     def allreduce_fp8(self, q: QuantizedTensor, algo: str = "auto", stream=None,
                       check: bool = True, errors: ErrorRecord | None = None) -> QuantizedTensor:
@@ -97,12 +109,16 @@ class Communicator:
 
         algo: "nccl" (grouped send/recv + reduce kernel), "p2p" (one fused
         NVLink kernel), "push" (store-only NVLink variant), or "auto": the
-        fused kernel when the gradient already lives in this communicator's
-        symmetric buffers (p2p_buffers), otherwise NCCL — all bit-identical."""
+        fused kernel whenever peer buffers are enabled and large enough
+        (a tensor outside p2p_buffers is copied in and out), otherwise NCCL —
+        all bit-identical. validate() runs first (collective.hpp:166)."""
         if q.codec_kind != CodecKind.Fp8E4M3:
             raise L.InvalidArgument("worker gradients are FP8 E4M3 tensors")
+        if q.packed and q.bit_width != 8:
+            raise L.InvalidArgument("worker gradients are FP8 E4M3 tensors")
+        validate(q)
         if algo == "auto":
-            algo = "p2p" if self._in_p2p_buffers(q) else "nccl"
+            algo = self._auto_algo(q)
         err = errors if errors is not None else ErrorRecord(q.codes.device)
         err.reset(stream)
         L.check(L.lib.agq_allreduce_fp8(self._h, q.codes.data_ptr(), q.scales.data_ptr(),
@@ -111,6 +127,35 @@ class Communicator:
         if check:
             err.raise_if_any(L.AGQ_OP_ALLREDUCE)
         return q
+
+    def last_trace(self):
+        """(events, moved): the messages this rank took part in during its
+        last allreduce_fp8 (TraceEvent list, collective.hpp:50-57) as issued
+        by the transfer code, and for the P2P algorithms the kernel's own
+        counters of the phase-1 traffic (elements, block scales)."""
+        cnt = C.c_int()
+        moved = (C.c_ulonglong * 2)()
+        L.check(L.lib.agq_comm_last_trace(self._h, None, 0, C.byref(cnt), moved))
+        arr = (L.AgqTraceEvent * max(cnt.value, 1))()
+        L.check(L.lib.agq_comm_last_trace(self._h, arr, cnt.value, C.byref(cnt), moved))
+        ev = [TraceEvent(PHASES[e.phase], e.sender, e.receiver, e.chunk_start, e.chunk_len,
+                         e.payload_bytes) for e in arr[:cnt.value]]
+        return ev, (int(moved[0]), int(moved[1]))
+
+    def gather_trace(self):
+        """The reference's MessageTrace of the last all-reduce across ALL
+        ranks: the union of every rank's last_trace(), de-duplicated and in
+        the reference's order (phase, then sender, then receiver;
+        collective.hpp:239-248, :287-300)."""
+        import torch.distributed as dist
+        mine, _ = self.last_trace()
+        allv = [None] * self.world
+        dist.all_gather_object(allv, [tuple(e.__dict__.values()) for e in mine], group=self._group)
+        uniq = {}
+        for rank_events in allv:
+            for t in rank_events:
+                uniq[(PHASES.index(t[0]), t[1], t[2])] = TraceEvent(*t)
+        return [uniq[k] for k in sorted(uniq)]
 
     def allreduce_naive_fp8(self, q: QuantizedTensor, stream=None):
         """allreduce_naive_fp8 (collective.hpp:338-431) across the ranks, in

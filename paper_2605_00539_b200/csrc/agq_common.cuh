@@ -15,12 +15,13 @@ constexpr int kBlock = 128;          // block size of every fast path
 constexpr int kTileBlocks = 64;      // blocks per tile
 constexpr int kTileElems = kTileBlocks * kBlock;  // 8192 elements
 constexpr int kThreads = 256;        // 32 consecutive elements per thread
-constexpr int kMaxSeg = 8;
+constexpr int kMaxSeg = 32;  // segments per grouped launch (larger groups split)
 constexpr long long kNone = 0x7fffffffffffffffLL;
 
 // A list of equally-coded tensors processed by one launch (grouped launch of
-// the tensors one pipeline stage stores). tile_begin is a prefix sum over
-// full tiles; block_base a prefix sum over blocks (error reporting).
+// the tensors one pipeline stage stores; ~1.3 KB of kernel parameters).
+// tile_begin is a prefix sum over whole warp tiles; block_base the
+// group-global index of each segment's first block (error reporting).
 struct SegTable {
   const void* src[kMaxSeg];
   void* codes[kMaxSeg];

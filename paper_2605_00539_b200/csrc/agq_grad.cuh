@@ -26,28 +26,20 @@ __device__ __forceinline__ float apply_prec(float s) {
   return s;
 }
 
-// Exact FP8 decode with an FP32 block scale, (float)(fl64(e4m3(c)/448)*(double)s).
-// AGQ_FP8DQ selects the implementation (all bit-identical, verified in
-// tests/cpp/numerics_check.cpp):
-//   0: 128-entry double LUT + DMUL + F2F          (LDS bank conflicts)
-//   1: 16-entry table + 2 DMUL + F2F              (conflict free)
-//   2: 16-entry table + DMUL + integer rounding   (no F2F; fast-scale blocks)
-#ifndef AGQ_FP8DQ
-#define AGQ_FP8DQ 0
-#endif
-// Shared table: [0,256) signed unit values fl64(e4m3(c)/448) for every code
-// (NaN for 0x7f/0xff), [256,272) the 16-entry table of the other decoders.
-constexpr int kDqTable = 272;
+// Exact FP8 decode with an FP32 block scale, (float)(fl64(e4m3(c)/448)*(double)s):
+// a shared table of the signed unit values fl64(e4m3(c)/448) for every code
+// (NaN for 0x7f/0xff) + DMUL + F2F. (A 16-entry table with two DMULs and an
+// integer double->float rounding are verified equal in
+// tests/cpp/numerics_check.cpp and measured slower,
+// profiles/r01_microbench_fp8_decode_variants.log.)
+constexpr int kDqTable = 256;
 __device__ __forceinline__ void fill_fp8_dq_table(double* t) {
   for (int c = threadIdx.x; c < 256; c += blockDim.x)
     t[c] = ((c & 0x7f) == 0x7f) ? __longlong_as_double(0x7ff8000000000000LL)
                                 : (double)e4m3_value((uint32_t)c) / 448.0;
-  if (threadIdx.x < 16) t[256 + threadIdx.x] = fp8_t16((int)threadIdx.x);
 }
-__device__ __forceinline__ float fp8_dequant(uint32_t c, double sd, const double* t, bool fastblk) {
-  if (AGQ_FP8DQ == 0) return d2f_rn(dmul(t[c & 0xffu], sd));
-  if (AGQ_FP8DQ == 2 && fastblk) return fp8_dequant_t16i(c, sd, t + 256);
-  return fp8_dequant_t16(c, sd, t + 256);
+__device__ __forceinline__ float fp8_dequant(uint32_t c, double sd, const double* t, bool) {
+  return d2f_rn(dmul(t[c & 0xffu], sd));
 }
 // Signed-LUT decode: one LDS.64 + DMUL + F2F, the sign rides in the table
 // (-0.0 * s = -0.0 as in the reference).
@@ -59,35 +51,10 @@ __device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) {
   return __byte_perm(w, 0u, 0x4440u | (uint32_t)k);
 }
 
-// Gradient decode through the per-block 8-entry table (1) or the 256-entry
-// signed unit table for every element (0); both exact. K3 (one piece per
-// element) is issue/latency bound and measured faster with the full table;
-// the multi-piece reduce kernels are shared-memory bound and use the block
-// table (profiles/r01_acc_tab_ab.log, r01_reduce_tab_ab.log).
-#ifndef AGQ_ACC_TAB
-#define AGQ_ACC_TAB 1
-#endif
-#ifndef AGQ_ACC_TAB_BF16L
-#define AGQ_ACC_TAB_BF16L 0
-#endif
-// block-table decode also for the rounded-precision (BF16 / FP16 sum) K3
-#ifndef AGQ_ACC_TAB_PREC
-#define AGQ_ACC_TAB_PREC 0
-#endif
-// resident CTAs per SM for the FP32-local, BF16-rounded K3 instance: at 3 it
-// spills; 2 runs it 356 -> 315 us at 2^28 (70% -> 79% of HBM),
-// while the FP16-rounded instance is slower at 2 (325 -> 348 us) and keeps 3
-// (profiles/r01_acc_prec_ab.log)
-// resident CTAs per SM for the BF16-local K3 instances
-#ifndef AGQ_ACC_MINB_BF16L
-#define AGQ_ACC_MINB_BF16L 3
-#endif
-#ifndef AGQ_ACC_MINB_BF16R
-#define AGQ_ACC_MINB_BF16R 2
-#endif
-#ifndef AGQ_RED_TAB
-#define AGQ_RED_TAB 1
-#endif
+// Gradient decode through a per-block 8-entry table (dq_tab_accum) where the
+// block allows it, else the 256-entry signed unit table; both exact. The
+// multi-piece reduce kernels and the FP32-local K3 use the block table
+// (profiles/r01_reduce_tab_ab.log, r01_acc_tab_ab2.log).
 // Lean table decode + accumulate of NW code words (4 codes each) against
 // this block's table at shared address tb_s (32-byte aligned, 8 entries
 // holding F[m]/2): the entry address comes straight from the code word
@@ -103,9 +70,6 @@ __device__ __forceinline__ float lds_f32(uint32_t a) {
 // 2^(e-15) exponent bias in a register the optimiser cannot see through, so
 // (y & mask) | bias is one LOP3 (a LOP3 takes a single immediate)
 __constant__ uint32_t c_pow2_bias = 0x38000000u;
-#ifndef AGQ_TAB_FMA
-#define AGQ_TAB_FMA 1  // 0: separate FMUL2 + FADD (the previous build, for A/B)
-#endif
 template <int NW>
 __device__ __forceinline__ void dq_tab_accum(const uint32_t (&w)[NW], uint32_t tb_s,
                                              float (&acc)[4 * NW]) {
@@ -126,13 +90,8 @@ __device__ __forceinline__ void dq_tab_accum(const uint32_t (&w)[NW], uint32_t t
       // one FFMA2 = fadd(acc, F*2^k) bit for bit: the product is exact (a
       // normal float times a power of two), so the fused add rounds once,
       // exactly like the separate add
-#if AGQ_TAB_FMA
       const f32x2 a = fma2(pk2(f[2 * h], f[2 * h + 1]), pk2(p2[2 * h], p2[2 * h + 1]),
                            pk2(acc[4 * i + 2 * h], acc[4 * i + 2 * h + 1]));
-#else
-      const f32x2 v = mul2(pk2(f[2 * h], f[2 * h + 1]), pk2(p2[2 * h], p2[2 * h + 1]));
-      const f32x2 a = add2(pk2(acc[4 * i + 2 * h], acc[4 * i + 2 * h + 1]), v);
-#endif
       up2(a, acc[4 * i + 2 * h], acc[4 * i + 2 * h + 1]);
     }
   }
@@ -152,29 +111,16 @@ __device__ __forceinline__ bool fp8_tab_ok8(const uint32_t (&w)[2]) {
 // A block scale for which fp8_dequant_t16i is exact (zero blocks excluded).
 __device__ __forceinline__ bool dq_fast(float s) { return s >= kFastLo && s <= kFastHi; }
 
-// Elements (bit e of the mask, e mod 16) whose double->float rounding runs on
-// the integer pipes (d2f_rn_bits) instead of F2F.F32.F64. F2F issues at 1/16
-// of the FP32 rate, so decoding every element through it bounds the reduce
-// kernels; splitting the elements balances the F2F pipe against issue slots.
-#ifndef AGQ_DQ_INT_MASK
-#define AGQ_DQ_INT_MASK 0x0u  // measured: all-F2F is fastest (profiles/r01_dq_split.log)
-#endif
 // acc[e] = fadd(acc[e], dequant(code e of w, sc)) for the N codes of one
-// block piece; bit-identical to fp8_dq_lut for every element.
+// block piece through the 256-entry table (zero / subnormal / NaN codes and
+// extreme scales). (Rounding part of the elements on the integer pipes
+// instead of F2F measured slower, profiles/r01_dq_split.log.)
 template <int N>
 __device__ __forceinline__ void dq_accum(const uint32_t (&w)[N / 4], float sc, const double* t,
                                          float (&acc)[N]) {
   const double sd = (double)sc;
-  if (AGQ_DQ_INT_MASK != 0u && dq_fast(sc)) {
 #pragma unroll
-    for (int e = 0; e < N; ++e) {
-      const double p = dmul(t[byte_of(w[e >> 2], e & 3)], sd);
-      acc[e] = fadd(acc[e], ((AGQ_DQ_INT_MASK >> (e & 15)) & 1u) ? d2f_rn_bits(p) : d2f_rn(p));
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < N; ++e) acc[e] = fadd(acc[e], fp8_dq_lut(byte_of(w[e >> 2], e & 3), sd, t));
-  }
+  for (int e = 0; e < N; ++e) acc[e] = fadd(acc[e], fp8_dq_lut(byte_of(w[e >> 2], e & 3), sd, t));
 }
 
 // Requantize 16 fp32 values of a block whose absmax is `a` (all 8 threads of
@@ -300,6 +246,17 @@ __device__ __forceinline__ uint32_t tab_addr(const float* wtab, int p) {
   return (uint32_t)__cvta_generic_to_shared(wtab + p * (256 / LPB) + (lane / LPB) * 8);
 }
 
+// Bad block scale of the all-reduce's inputs: the reference validates the
+// workers in order (collective.hpp:158-168 check_workers -> validate), so the
+// error is the lowest block of the lowest sender with a bad scale; the record
+// holds (sender << 40) | block and agq_errors_message prints the block.
+__device__ __forceinline__ long long bad_scale_key(uint32_t piece_mask, long long blk) {
+  return ((long long)(__ffs(piece_mask) - 1) << 40) | blk;
+}
+__device__ __forceinline__ uint32_t bad_scale_bit(float s, int p) {
+  return (uint32_t)(!(s >= 0.0f) || !(s <= 3.402823466e38f)) << p;
+}
+
 // Absmax, error records, FP8 requant and the stores of one 16-element group.
 __device__ __forceinline__ void reduce_finish(const PieceTable& pt, uint64_t e0, uint64_t len,
                                               bool whole, bool in_range, uint64_t blk,
@@ -320,13 +277,13 @@ __device__ __forceinline__ void reduce_compute(const PieceTable& pt, uint64_t e0
 #pragma unroll
   for (int e = 0; e < 16; ++e) acc[e] = 0.0f;
   uint32_t sbad = 0;
-  if (AGQ_RED_TAB && wtab != nullptr) build_tables<NP, 8>(wtab, sc);  // all lanes
+  if (wtab != nullptr) build_tables<NP, 8>(wtab, sc);  // all lanes
   if (in_range) {
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-      sbad |= !(sc[p] >= 0.0f) || !(sc[p] <= 3.402823466e38f);
+      sbad |= bad_scale_bit(sc[p], p);
       const uint32_t w[4] = {cv[p].x, cv[p].y, cv[p].z, cv[p].w};
-      if (AGQ_RED_TAB && wtab != nullptr && dq_fast(sc[p]) && fp8_tab_ok16(w)) {
+      if (wtab != nullptr && dq_fast(sc[p]) && fp8_tab_ok16(w)) {
         dq_tab_accum<4>(w, tab_addr<8>(wtab, p), acc);
       } else {
         dq_accum<16>(w, sc[p], t16, acc);
@@ -386,7 +343,7 @@ __device__ __forceinline__ void reduce_group(const PieceTable& pt, uint64_t g, u
 #pragma unroll 1
       for (int p = 0; p < np; ++p) {
         const float scp = pt.scales[p][blk];
-        sbad |= !(scp >= 0.0f) || !(scp <= 3.402823466e38f);
+        sbad |= bad_scale_bit(scp, p);
         uint32_t w[4] = {0, 0, 0, 0};
         if (whole) {
           const uint4 v = *reinterpret_cast<const uint4*>(pt.codes[p] + e0);
@@ -412,7 +369,7 @@ __device__ __forceinline__ void reduce_finish(const PieceTable& pt, uint64_t e0,
   const uint32_t m = absmax_bits16(acc);
   const int sub = threadIdx.x & 7;
   if (in_range && sub == 0) {
-    if (sbad) err_min(&err->bad_scale_block, blk_base + (long long)blk);
+    if (sbad) err_min(&err->bad_scale_block, bad_scale_key(sbad, blk_base + (long long)blk));
     if (m >= 0x7f800000u) err_min(&err->overflow_block, blk_base + (long long)blk);
   }
   if (!in_range) return;

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -25,7 +26,7 @@ agq_status dequantize_device(const void* codes, int layout, const float* scales,
 agq_status quantize_grouped_device(const agq_segment* segs, int nseg, int x_dtype, int bits,
                                    int codec, agq_errors* err, cudaStream_t s);
 agq_status dequantize_grouped_device(const agq_segment* segs, int nseg, int out_dtype, int bits,
-                                     int codec, cudaStream_t s);
+                                     int codec, int validate, agq_errors* err, cudaStream_t s);
 agq_status pack_device(const uint8_t* codes, uint64_t n, int bits, uint8_t* packed,
                        cudaStream_t s);
 agq_status unpack_device(const uint8_t* packed, uint64_t n, int bits, uint8_t* codes,
@@ -48,6 +49,9 @@ agq_status comm_p2p_export(agq_comm* c, uint64_t capacity, unsigned char handle[
 agq_status comm_p2p_open(agq_comm* c, const unsigned char* handles);
 agq_status comm_p2p_buffers(agq_comm* c, uint8_t** codes, float** scales);
 agq_status comm_destroy(agq_comm* c);
+agq_status comm_set_timeout(agq_comm* c, double seconds);
+agq_status comm_last_trace(agq_comm* c, agq_trace_event* events, int cap, int* count,
+                           unsigned long long* moved);
 int comm_rank(const agq_comm* c);
 int comm_size(const agq_comm* c);
 agq_status allreduce_naive(agq_comm* c, uint8_t* codes, float* scales, uint64_t n,
@@ -222,8 +226,10 @@ agq_status agq_errors_message(const agq_errors* h, int op, char* msg, size_t msg
         inv("non-finite input element in block " + std::to_string(h->nonfinite_block));
       break;
     case AGQ_OP_ALLREDUCE:
+      // key = (sender << 40) | block: the lowest sender's lowest bad block
       if (h->bad_scale_block != LLONG_MAX)
-        inv("quantized tensor: bad scale at block " + std::to_string(h->bad_scale_block));
+        inv("quantized tensor: bad scale at block " +
+            std::to_string(h->bad_scale_block & ((1LL << 40) - 1)));
       else if (h->overflow_block == -1)
         rt("all-reduce aborted: peer did not arrive (timeout)");
       else if (h->overflow_block != LLONG_MAX)
@@ -271,14 +277,20 @@ agq_status agq_quantize_grouped(const agq_segment* segs, int nseg, int x_dtype, 
                                 int codec, agq_errors* d_err, agq_stream_t stream) {
   if (agq_status st = check_args(bits, 128, codec)) return st;
   if (agq_status st = check_device()) return st;
+  if (nseg < 0) return set_error(AGQ_ERR_INVALID_ARGUMENT, "negative segment count");
   return quantize_grouped_device(segs, nseg, x_dtype, bits, codec, d_err, (cudaStream_t)stream);
 }
 
 agq_status agq_dequantize_grouped(const agq_segment* segs, int nseg, int out_dtype, int bits,
-                                  int codec, agq_stream_t stream) {
+                                  int codec, int validate, agq_errors* d_err,
+                                  agq_stream_t stream) {
   if (agq_status st = check_args(bits, 128, codec)) return st;
   if (agq_status st = check_device()) return st;
-  return dequantize_grouped_device(segs, nseg, out_dtype, bits, codec, (cudaStream_t)stream);
+  if (nseg < 0) return set_error(AGQ_ERR_INVALID_ARGUMENT, "negative segment count");
+  if (validate && !d_err)
+    return set_error(AGQ_ERR_INVALID_ARGUMENT, "validate needs an error record");
+  return dequantize_grouped_device(segs, nseg, out_dtype, bits, codec, validate, d_err,
+                                   (cudaStream_t)stream);
 }
 
 agq_status agq_pack_codes(const uint8_t* codes, uint64_t n, int bits, uint8_t* packed,
@@ -377,6 +389,15 @@ agq_status agq_comm_p2p_buffers(agq_comm* comm, uint8_t** codes, float** scales)
 }
 agq_status agq_comm_destroy(agq_comm* comm) { return comm_destroy(comm); }
 int agq_comm_rank(const agq_comm* comm) { return comm_rank(comm); }
+agq_status agq_comm_set_timeout(agq_comm* comm, double seconds) {
+  if (!comm) return set_error(AGQ_ERR_INVALID_ARGUMENT, "null communicator");
+  return comm_set_timeout(comm, seconds);
+}
+agq_status agq_comm_last_trace(agq_comm* comm, agq_trace_event* events, int cap, int* count,
+                               unsigned long long* moved) {
+  if (!comm || !count) return set_error(AGQ_ERR_INVALID_ARGUMENT, "null communicator");
+  return comm_last_trace(comm, events, cap, count, moved);
+}
 int agq_comm_size(const agq_comm* comm) { return comm_size(comm); }
 
 agq_status agq_allreduce_fp8(agq_comm* comm, uint8_t* codes, float* scales, uint64_t n,
@@ -533,6 +554,49 @@ agq_status agq_allreduce_simulated_host(int world, const uint8_t* const* codes,
   cudaMemcpyAsync(out_codes, ocd, n, cudaMemcpyDeviceToHost, s);
   cudaMemcpyAsync(out_scales, osd, nb * 4, cudaMemcpyDeviceToHost, s);
   return cuda_fail(cudaStreamSynchronize(s), "allreduce_host");
+}
+
+// ---- synthetic inputs (host) ----------------------------------------------------
+// tools/agq.cpp:47-65 InputSpec::materialize with rng.hpp:9-28 make_rng: the
+// same libstdc++ engine and distributions, hence the same bytes as the
+// reference CLI for (seed, stream 0x1D, index 0).
+agq_status agq_fill_input(uint64_t seed, uint64_t stream, uint64_t index, int kind, double a,
+                          double b, int out_dtype, void* out, uint64_t n) {
+  if (kind < AGQ_INPUT_NORMAL || kind > AGQ_INPUT_CONST)
+    return set_error(AGQ_ERR_INVALID_ARGUMENT, "unknown input kind");
+  if (out_dtype != AGQ_F32 && out_dtype != AGQ_BF16)
+    return set_error(AGQ_ERR_INVALID_ARGUMENT, "output dtype must be F32 or BF16");
+  if (kind == AGQ_INPUT_UNIFORM && !(a <= b))
+    return set_error(AGQ_ERR_INVALID_ARGUMENT, "--uniform needs a <= b");
+  if (n && !out) return set_error(AGQ_ERR_INVALID_ARGUMENT, "null output");
+  auto mix = [](uint64_t z) {  // rng.hpp:10-15 splitmix64
+    z += 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  };
+  std::mt19937_64 rng(mix(mix(seed ^ (stream * 0xd1342543de82ef95ULL)) + index));  // :19-28
+  auto put = [&](uint64_t i, float x) {
+    if (out_dtype == AGQ_F32) {
+      static_cast<float*>(out)[i] = x;
+    } else {  // round to nearest even (BF16-valued configs)
+      uint32_t u;
+      std::memcpy(&u, &x, 4);
+      if ((u & 0x7fffffffu) > 0x7f800000u) u |= 0x00400000u;
+      else u += 0x7fffu + ((u >> 16) & 1u);
+      static_cast<uint16_t*>(out)[i] = (uint16_t)(u >> 16);
+    }
+  };
+  if (kind == AGQ_INPUT_CONST) {
+    for (uint64_t i = 0; i < n; ++i) put(i, static_cast<float>(a));
+  } else if (kind == AGQ_INPUT_UNIFORM) {
+    std::uniform_real_distribution<float> u(static_cast<float>(a), static_cast<float>(b));
+    for (uint64_t i = 0; i < n; ++i) put(i, u(rng));
+  } else {
+    std::normal_distribution<float> g(static_cast<float>(a), static_cast<float>(b));
+    for (uint64_t i = 0; i < n; ++i) put(i, g(rng));
+  }
+  return AGQ_OK;
 }
 
 // ---- DBCA control plane (dbca.hpp) ----------------------------------------------

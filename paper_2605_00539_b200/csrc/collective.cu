@@ -14,6 +14,17 @@
 //   read and written only by rank r, so the only cross-GPU synchronisation is
 //   a start barrier (inputs final) and an end barrier (all chunks written),
 //   both as system-scope release/acquire flags with a timeout.
+// AGQ_AR_PUSH_P2P (v3): the same decomposition with every NVLink transfer a
+//   store: scatter chunk q into rank q's inbox, then reduce from local memory
+//   and store the result into every rank's buffer.
+//
+// Failure handling: a timed-out barrier (a peer that never arrived) records
+// overflow_block = -1 (agq_errors_message: "peer did not arrive") and marks
+// the communicator failed on every rank (a sticky flag each kernel checks
+// first), so later calls fail fast instead of reading stale peer data.
+// Data errors are shared: every rank reports the same bad-scale / overflow
+// error, as the reference aborts all workers (collective.hpp:158-168,
+// :278-281).
 //
 // Chunk ownership follows ChunkAssignment::block_aligned (collective.hpp:
 // 23-39); results do not depend on it (per-block reduce, sender-rank order).
@@ -34,6 +45,7 @@ agq_status reduce_requant_device(int np, const uint8_t* const* pc, const float* 
                                  float* const* os, long long blk_base, agq_errors* err,
                                  cudaStream_t s);
 void chunk_ranges(uint64_t n, uint32_t block, int workers, uint64_t* ranges);
+agq_status comm_destroy(agq_comm* c);
 agq_status naive_step_device(const uint8_t* in_codes, const float* in_scales,
                              const uint32_t* in_sat, uint8_t* codes, const float* scales,
                              uint32_t* out_sat, uint64_t len, uint32_t block,
@@ -84,31 +96,45 @@ const NcclApi& nccl() {
 
 // Symmetric buffer layout (identical offsets on every rank).
 namespace {
-constexpr size_t kFlagsBytes = 4096;  // ready[16] | done[16] | err words
-constexpr int kReadyOff = 0, kDoneOff = 16, kScatterOff = 32;
+constexpr size_t kFlagsBytes = 4096;
+// u64 words of the flags page
+constexpr int kReadyOff = 0;       // [16] start barrier, epoch per sender
+constexpr int kDoneOff = 16;       // [16] end barrier, epoch per sender
+constexpr int kScatteredOff = 32;  // [16] push algorithm: inbox slot written
+constexpr int kFailOff = 48;       // sticky: a barrier of this communicator timed out
+constexpr int kOverflowOff = 64;   // [16] overflow block reported by each rank
+constexpr int kBadScaleOff = 80;   // [16] bad-scale key reported by each rank
 size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 }  // namespace
 
 struct agq_comm {
   ncclComm_t nccl = nullptr;
   int nranks = 0, rank = 0, device = 0;
-  // v1 workspace
+  uint64_t timeout_ns = 300ull * 1000000000ull;  // device barrier timeout
+  // v1 workspace: P-1 receive slots of one chunk (codes + block scales)
   uint8_t* recv_codes = nullptr;
   float* recv_scales = nullptr;
-  uint64_t recv_chunk_cap = 0;  // elements per peer slot
+  uint64_t recv_chunk_cap = 0;  // elements per slot
+  uint64_t recv_scale_cap = 0;  // floats per slot
   // naive-ring workspace: one incoming chunk + two saturation bitmasks
   uint8_t* ring_codes = nullptr;
   float* ring_scales = nullptr;
   uint32_t* ring_sat = nullptr;
   uint64_t ring_cap = 0;  // elements
-  // v2 symmetric memory
+  uint32_t ring_block = 0;
+  // v2/v3 symmetric memory
   unsigned char* sym = nullptr;
   size_t sym_bytes = 0;
   uint64_t sym_cap = 0;  // elements
   unsigned char* peer[AGQ_MAX_WORLD] = {};
   bool p2p_ready = false;
-  unsigned int* done_counter = nullptr;  // local, per kernel
+  unsigned int* done_counter = nullptr;  // local, one per kernel in flight
+  unsigned long long* stats = nullptr;   // device: [elements, blocks] moved per peer
   uint64_t epoch = 0;
+  // message trace of the last all-reduce issued by this rank
+  std::vector<agq_trace_event> trace;
+  int trace_algo = -1;
+  cudaStream_t trace_stream = nullptr;
 };
 
 namespace agqk {
@@ -131,29 +157,50 @@ struct FusedArgs {
   unsigned char* base[AGQ_MAX_WORLD];  // symmetric buffer of every rank (self included)
   uint64_t scales_off, codes_off;      // byte offsets inside the buffer
   uint64_t begin, len;                 // my chunk (elements, block aligned)
-  uint64_t epoch;
+  uint64_t epoch, timeout_ns;
   unsigned int* done_counter;
+  unsigned long long* stats;           // [elements, blocks] pulled from the peers
   agq_errors* err;
   int rank, P;
-  int copy_only;
 };
 
-// Spin until flag >= epoch; returns false on timeout (20 s).
-__device__ bool wait_flag(const uint64_t* f, uint64_t epoch) {
+// Spin until *f >= epoch. False on timeout or when the communicator has
+// been marked failed (by this rank or a peer).
+__device__ bool wait_flag(const uint64_t* f, uint64_t epoch, const uint64_t* fail,
+                          uint64_t timeout_ns) {
   const uint64_t t0 = globaltimer();
   while (ld_acquire_sys(f) < epoch) {
-    if (globaltimer() - t0 > 20000000000ull) return false;
+    if (ld_acquire_sys(fail) != 0) return false;
+    if (globaltimer() - t0 > timeout_ns) return false;
     __nanosleep(200);
   }
   return true;
 }
 
-// AGQ_P2P_COPYONLY=1 (measurement only): identical NVLink traffic, no
-// dequant/reduce/requant — bounds the transfer-only time of the kernel.
+// Mark the communicator failed on every rank (sticky, see agq_comm_set_timeout).
+template <class Args>
+__device__ void mark_failed(const Args& a) {
+  for (int s = 0; s < a.P; ++s) st_release_sys(reinterpret_cast<uint64_t*>(a.base[s]) + kFailOff, 1);
+  err_min(&a.err->overflow_block, -1);
+}
+
+// Start barrier of a P2P epoch (thread 0 of each CTA; CTA 0 announces).
+template <class Args>
+__device__ bool start_barrier(const Args& a, int wait_off, bool skip_self) {
+  uint64_t* my_flags = reinterpret_cast<uint64_t*>(a.base[a.rank]);
+  if (ld_acquire_sys(my_flags + kFailOff) != 0) return false;
+  bool ok = true;
+  for (int s = 0; s < a.P; ++s)
+    if (!(skip_self && s == a.rank) &&
+        !wait_flag(my_flags + wait_off + s, a.epoch, my_flags + kFailOff, a.timeout_ns))
+      ok = false;
+  return ok;
+}
+
 // One 16-element group of the fused all-reduce with every pointer in
 // registers (compile-time NP): chunk r of every rank is read over NVLink
-// (rank order = ascending sender rank), reduced from +0.0f in FP32, requantized
-// and written back in place to all ranks.
+// (rank order = ascending sender rank), reduced from +0.0f in FP32,
+// requantized and written back in place to all ranks.
 template <int NP>
 __device__ __forceinline__ void fused_group(unsigned char* const (&base)[NP], uint64_t coff,
                                             uint64_t soff, uint64_t g, uint64_t len,
@@ -187,13 +234,13 @@ __device__ __forceinline__ void fused_group(unsigned char* const (&base)[NP], ui
         cv[p] = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
-    if (AGQ_RED_TAB) build_tables<NP, 8>(wtab, sc);  // every lane of the warp
+    build_tables<NP, 8>(wtab, sc);  // every lane of the warp
     if (in_range) {
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
-        sbad |= !(sc[p] >= 0.0f) || !(sc[p] <= 3.402823466e38f);
+        sbad |= bad_scale_bit(sc[p], p);
         const uint32_t w[4] = {cv[p].x, cv[p].y, cv[p].z, cv[p].w};
-        if (AGQ_RED_TAB && dq_fast(sc[p]) && fp8_tab_ok16(w))
+        if (dq_fast(sc[p]) && fp8_tab_ok16(w))
           dq_tab_accum<4>(w, tab_addr<8>(wtab, p), acc);
         else
           dq_accum<16>(w, sc[p], t16, acc);
@@ -206,7 +253,7 @@ __device__ __forceinline__ void fused_group(unsigned char* const (&base)[NP], ui
   const uint32_t m = absmax_bits16(acc);
   const int sub = threadIdx.x & 7;
   if (in_range && sub == 0) {
-    if (sbad) err_min(&err->bad_scale_block, blk_base + (long long)blk);
+    if (sbad) err_min(&err->bad_scale_block, bad_scale_key(sbad, blk_base + (long long)blk));
     if (m >= 0x7f800000u) err_min(&err->overflow_block, blk_base + (long long)blk);
   }
   if (!in_range) return;
@@ -228,144 +275,76 @@ __device__ __forceinline__ void fused_group(unsigned char* const (&base)[NP], ui
   }
 }
 
-// 8 elements per thread (16 lanes per block) for large worlds: half the
-// per-piece registers so NP = 5..8 keeps two CTAs per SM without spills.
-template <int NP>
-__device__ __forceinline__ void fused_group8(unsigned char* const (&base)[NP], uint64_t coff,
-                                             uint64_t soff, uint64_t g, uint64_t len,
-                                             long long blk_base, const double* t16,
-                                             agq_errors* err, float* wtab) {
-  const uint64_t e0 = g * 8;
-  const uint64_t blk = e0 / kBlock;
-  const bool in_range = e0 < len;
-  const bool whole = e0 + 8 <= len;
-  float acc[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
-  uint32_t sbad = 0;
-  {
-    uint2 cv[NP];
-    float sc[NP];
-#pragma unroll
-    for (int p = 0; p < NP; ++p) {
-      cv[p] = make_uint2(0, 0);
-      sc[p] = blk * kBlock < len ? reinterpret_cast<const float*>(base[p] + soff)[blk] : 0.0f;
-      if (!in_range) continue;
-      if (whole) {
-        cv[p] = *reinterpret_cast<const uint2*>(base[p] + coff + e0);
-      } else {
-        uint32_t w[2] = {0, 0};
-        for (int e = 0; e < 8 && e0 + e < len; ++e)
-          w[e >> 2] |= (uint32_t)base[p][coff + e0 + e] << (8 * (e & 3));
-        cv[p] = make_uint2(w[0], w[1]);
-      }
-    }
-    if (AGQ_RED_TAB) build_tables<NP, 16>(wtab, sc);  // every lane of the warp
-    if (in_range) {
-#pragma unroll
-      for (int p = 0; p < NP; ++p) {
-        sbad |= !(sc[p] >= 0.0f) || !(sc[p] <= 3.402823466e38f);
-        const uint32_t w[2] = {cv[p].x, cv[p].y};
-        if (AGQ_RED_TAB && dq_fast(sc[p]) && fp8_tab_ok8(w))
-          dq_tab_accum<2>(w, tab_addr<16>(wtab, p), acc);
-        else
-          dq_accum<8>(w, sc[p], t16, acc);
-      }
-      if (!whole)
-        for (int e = 0; e < 8; ++e)
-          if (e0 + e >= len) acc[e] = 0.0f;
-    }
-  }
-  const uint32_t m = absmax_bits8(acc);
-  const int sub = threadIdx.x & 15;
-  if (in_range && sub == 0) {
-    if (sbad) err_min(&err->bad_scale_block, blk_base + (long long)blk);
-    if (m >= 0x7f800000u) err_min(&err->overflow_block, blk_base + (long long)blk);
-  }
-  if (!in_range) return;
-  const float a = u2f(m);
-  uint32_t ow[2];
-  if (m >= 0x7f800000u) {
-    ow[0] = ow[1] = 0;
-  } else {
-    fp8_requant8(acc, a, ow);
-  }
-#pragma unroll
-  for (int o = 0; o < NP; ++o) {
-    if (whole) {
-      *reinterpret_cast<uint2*>(base[o] + coff + e0) = make_uint2(ow[0], ow[1]);
-    } else {
-      for (int e = 0; e < 8 && e0 + e < len; ++e)
-        base[o][coff + e0 + e] = (uint8_t)(ow[e >> 2] >> (8 * (e & 3)));
-    }
-    if (sub == 0) reinterpret_cast<float*>(base[o] + soff)[blk] = a;
-  }
-}
 
-// End of an all-reduce epoch (every CTA calls it): the last CTA of this
-// rank's grid to finish publishes "done" to every rank and waits for all of
-// them, so the kernel completes only when every rank has finished writing
-// into this rank's buffer (and reading from it). A local-reduce overflow is
-// shared with every rank first (collective.hpp:278-281 aborts all ranks).
+// End of an all-reduce epoch. EVERY CTA calls it exactly once (also after a
+// failed start), so the per-kernel CTA counter always returns to zero. The
+// last CTA of this rank's grid shares this rank's data errors with every
+// rank, publishes "done" to every rank and waits for all of them, so the
+// kernel completes only when every rank has finished writing into (and
+// reading from) this rank's buffer; then it merges the peers' errors.
 template <class Args>
-__device__ __forceinline__ void epoch_end(const Args& a) {
+__device__ __forceinline__ void epoch_end(const Args& a, bool ok) {
   unsigned char* const* base = a.base;
   const int P = a.P, rank = a.rank;
-  const uint64_t epoch = a.epoch;
-  unsigned int* done_counter = a.done_counter;
   agq_errors* err = a.err;
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x != 0) return;
-  const unsigned int prev = atomicAdd(done_counter, 1u);
+  const unsigned int prev = atomicAdd(a.done_counter, 1u);
   if (prev != gridDim.x * gridDim.y - 1) return;
   __threadfence_system();
   uint64_t* my_flags = reinterpret_cast<uint64_t*>(base[rank]);
+  // a CTA that failed its start barrier recorded -1 (min over the record)
   const long long ov = *reinterpret_cast<volatile long long*>(&err->overflow_block);
-  for (int s = 0; s < P; ++s) {
-    uint64_t* peer_flags = reinterpret_cast<uint64_t*>(base[s]);
-    if (ov != kNone) atomicMin(reinterpret_cast<long long*>(peer_flags + 64 + rank), ov);
+  if (ok && ov != -1) {
+    const long long bs = *reinterpret_cast<volatile long long*>(&err->bad_scale_block);
+    for (int s = 0; s < P; ++s) {
+      uint64_t* pf = reinterpret_cast<uint64_t*>(base[s]);
+      if (ov != kNone) atomicMin(reinterpret_cast<long long*>(pf + kOverflowOff + rank), ov);
+      if (bs != kNone) atomicMin(reinterpret_cast<long long*>(pf + kBadScaleOff + rank), bs);
+    }
+    __threadfence_system();
+    for (int s = 0; s < P; ++s)
+      st_release_sys(reinterpret_cast<uint64_t*>(base[s]) + kDoneOff + rank, a.epoch);
+    bool fine = true;
+    for (int s = 0; s < P; ++s)
+      if (!wait_flag(my_flags + kDoneOff + s, a.epoch, my_flags + kFailOff, a.timeout_ns))
+        fine = false;
+    for (int s = 0; s < P; ++s) {
+      volatile long long* o = reinterpret_cast<volatile long long*>(my_flags + kOverflowOff + s);
+      volatile long long* b = reinterpret_cast<volatile long long*>(my_flags + kBadScaleOff + s);
+      if (*o != kNone) err_min(&err->overflow_block, *o);
+      if (*b != kNone) err_min(&err->bad_scale_block, *b);
+      *o = kNone;  // reset for the next epoch (peers enter it only after
+      *b = kNone;  // this kernel: its start barrier needs our next "ready")
+    }
+    if (!fine) mark_failed(a);
+  } else {
+    mark_failed(a);
   }
-  __threadfence_system();
-  for (int s = 0; s < P; ++s)
-    st_release_sys(reinterpret_cast<uint64_t*>(base[s]) + kDoneOff + rank, epoch);
-  bool fine = true;
-  for (int s = 0; s < P; ++s)
-    if (!wait_flag(my_flags + kDoneOff + s, epoch)) fine = false;
-  for (int s = 0; s < P; ++s) {
-    const long long o = *reinterpret_cast<volatile long long*>(my_flags + 64 + s);
-    if (o != kNone) err_min(&err->overflow_block, o);
-    // reset for the next epoch
-    *reinterpret_cast<volatile long long*>(my_flags + 64 + s) = kNone;
-  }
-  if (!fine) err_min(&err->overflow_block, -1);
-  *done_counter = 0u;
+  __threadfence();
+  *a.done_counter = 0u;
 }
 
-#ifndef AGQ_P2P_MINB
-#define AGQ_P2P_MINB 2
-#endif
-template <int NP, int EPT>
-__global__ void __launch_bounds__(256, AGQ_P2P_MINB) k_fused_allreduce(FusedArgs a) {
+template <int NP>
+__global__ void __launch_bounds__(256, 2) k_fused_allreduce(FusedArgs a) {
   __shared__ double lut[kDqTable];
   __shared__ float btab[8 * (NP > 0 ? NP : 1) * 32];  // 8 warps x NP pieces x 32 entries
   __shared__ int ok;
   fill_fp8_dq_table(lut);
   float* wtab = btab + (threadIdx.x >> 5) * (NP > 0 ? NP : 1) * 32;
   const int tid = threadIdx.x;
-  uint64_t* my_flags = reinterpret_cast<uint64_t*>(a.base[a.rank]);
   // start barrier: announce "my input is final" to every rank, then wait for
   // every rank's announcement (each CTA waits; only CTA 0 announces).
   if (blockIdx.x == 0 && tid < a.P)
     st_release_sys(reinterpret_cast<uint64_t*>(a.base[tid]) + kReadyOff + a.rank, a.epoch);
   if (tid == 0) {
-    ok = 1;
-    for (int s = 0; s < a.P; ++s)
-      if (!wait_flag(my_flags + kReadyOff + s, a.epoch)) ok = 0;
+    ok = start_barrier(a, kReadyOff, false) ? 1 : 0;
+    if (!ok) err_min(&a.err->overflow_block, -1);
   }
   __syncthreads();
   if (!ok) {
-    if (tid == 0) err_min(&a.err->overflow_block, -1);
+    epoch_end(a, false);
     return;
   }
 
@@ -374,32 +353,18 @@ __global__ void __launch_bounds__(256, AGQ_P2P_MINB) k_fused_allreduce(FusedArgs
   const uint64_t ngroups = nblocks * 8;
   const uint64_t gpad = (ngroups + 31) / 32 * 32;
   const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
+  unsigned long long n_el = 0, n_blk = 0;  // what this thread moved per peer
   if constexpr (NP > 0) {
     unsigned char* bs[NP];
 #pragma unroll
     for (int s = 0; s < NP; ++s) bs[s] = a.base[s];
     const uint64_t coff = a.codes_off + a.begin, soff = a.scales_off + 4 * b0;
-    if (a.copy_only) {
-      for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + tid; g < ngroups; g += stride) {
-        const uint64_t e0 = g * 16;
-        if (e0 + 16 > a.len) continue;
-        uint4 x = make_uint4(0, 0, 0, 0);
-#pragma unroll
-        for (int p = 0; p < NP; ++p) {
-          const uint4 v = *reinterpret_cast<const uint4*>(bs[p] + coff + e0);
-          x.x ^= v.x; x.y ^= v.y; x.z ^= v.z; x.w ^= v.w;
-        }
-#pragma unroll
-        for (int o = 0; o < NP; ++o) *reinterpret_cast<uint4*>(bs[o] + coff + e0) = x;
-      }
-    } else {
-      if constexpr (EPT == 8) {
-        const uint64_t ng8 = nblocks * 16, gp8 = (ng8 + 31) / 32 * 32;
-        for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + tid; g < gp8; g += stride)
-          fused_group8<NP>(bs, coff, soff, g, g < ng8 ? a.len : 0, (long long)b0, lut, a.err, wtab);
-      } else {
-        for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + tid; g < gpad; g += stride)
-          fused_group<NP>(bs, coff, soff, g, g < ngroups ? a.len : 0, (long long)b0, lut, a.err, wtab);
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + tid; g < gpad; g += stride) {
+      const uint64_t len = g < ngroups ? a.len : 0;
+      fused_group<NP>(bs, coff, soff, g, len, (long long)b0, lut, a.err, wtab);
+      if (g * 16 < len) {
+        n_el += min((uint64_t)16, len - g * 16);
+        n_blk += (tid & 7) == 0;
       }
     }
   } else {
@@ -412,167 +377,26 @@ __global__ void __launch_bounds__(256, AGQ_P2P_MINB) k_fused_allreduce(FusedArgs
       pt.out_codes[s] = a.base[s] + a.codes_off + a.begin;
       pt.out_scales[s] = reinterpret_cast<float*>(a.base[s] + a.scales_off) + b0;
     }
-    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + tid; g < gpad; g += stride)
-      reduce_group<0>(pt, g, g < ngroups ? a.len : 0, (long long)b0, lut, a.err, true);
-  }
-
-  epoch_end(a);
-}
-
-// ---------------------------------------------------------------------------
-// Fused all-reduce, TMA-pipelined variant (AGQ_P2P_TMA=1): the same pull /
-// reduce / push as k_fused_allreduce, but each warp keeps kStages warp tiles
-// (512 elements = 4 blocks) of every piece in flight with 1-D bulk copies
-// from the peers' buffers (lane 0 issues NP x (512 B codes + a 32 B aligned
-// window holding the tile's 4 scales) per stage, one mbarrier per stage), so
-// the NVLink pull latency overlaps the decode/reduce/requant of earlier
-// tiles instead of sitting in front of every group. The partial last tile
-// uses the per-thread path.
-// ---------------------------------------------------------------------------
-template <int NP>
-struct TmaCfg {
-  static constexpr int kStages = NP <= 4 ? 4 : 3;
-  static constexpr uint32_t kPiece = 512 + 32;
-  static constexpr uint32_t kStage = NP * kPiece;
-  static constexpr uint32_t kWarpBytes = kStages * kStage;
-  static constexpr size_t kSmem = 8 * (size_t)kWarpBytes;
-};
-
-// Decode + reduce (ascending piece order from +0.0f), requantize and store to
-// every rank one whole 16-element group whose codes/scales are in registers.
-template <int NP>
-__device__ __forceinline__ void reduce_store16(unsigned char* const (&bs)[NP], uint64_t coff,
-                                               uint64_t soff, uint64_t e0,
-                                               const uint32_t (&cw)[NP][4], const float (&sc)[NP],
-                                               long long blk_base, const double* t16,
-                                               agq_errors* err, float* wtab) {
-  const uint64_t blk = e0 / kBlock;
-  float acc[16];
-#pragma unroll
-  for (int e = 0; e < 16; ++e) acc[e] = 0.0f;
-  uint32_t sbad = 0;
-  if (AGQ_RED_TAB) build_tables<NP, 8>(wtab, sc);
-#pragma unroll
-  for (int p = 0; p < NP; ++p) {
-    sbad |= !(sc[p] >= 0.0f) || !(sc[p] <= 3.402823466e38f);
-    if (AGQ_RED_TAB && dq_fast(sc[p]) && fp8_tab_ok16(cw[p]))
-      dq_tab_accum<4>(cw[p], tab_addr<8>(wtab, p), acc);
-    else
-      dq_accum<16>(cw[p], sc[p], t16, acc);
-  }
-  const uint32_t m = absmax_bits16(acc);
-  const int sub = threadIdx.x & 7;
-  if (sub == 0) {
-    if (sbad) err_min(&err->bad_scale_block, blk_base + (long long)blk);
-    if (m >= 0x7f800000u) err_min(&err->overflow_block, blk_base + (long long)blk);
-  }
-  const float a = u2f(m);
-  uint32_t ow[4];
-  if (m >= 0x7f800000u) {
-    ow[0] = ow[1] = ow[2] = ow[3] = 0;
-  } else {
-    fp8_requant16(acc, a, ow);
-  }
-#pragma unroll
-  for (int o = 0; o < NP; ++o) {
-    *reinterpret_cast<uint4*>(bs[o] + coff + e0) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
-    if (sub == 0) reinterpret_cast<float*>(bs[o] + soff)[blk] = a;
-  }
-}
-
-template <int NP>
-__global__ void __launch_bounds__(256, 1) k_fused_tma(FusedArgs a) {
-  using C = TmaCfg<NP>;
-  extern __shared__ __align__(128) unsigned char dsm[];
-  __shared__ double lut[kDqTable];
-  __shared__ float btab[8 * NP * 32];
-  __shared__ __align__(8) uint64_t bars[8 * C::kStages];
-  __shared__ int ok;
-  fill_fp8_dq_table(lut);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  uint64_t* my_flags = reinterpret_cast<uint64_t*>(a.base[a.rank]);
-  if (blockIdx.x == 0 && tid < a.P)
-    st_release_sys(reinterpret_cast<uint64_t*>(a.base[tid]) + kReadyOff + a.rank, a.epoch);
-  if (tid == 0) {
-    ok = 1;
-    for (int s = 0; s < a.P; ++s)
-      if (!wait_flag(my_flags + kReadyOff + s, a.epoch)) ok = 0;
-  }
-  __syncthreads();
-  if (!ok) {
-    if (tid == 0) err_min(&a.err->overflow_block, -1);
-    return;
-  }
-  // the peers' data was published to the generic proxy; the bulk copies
-  // below read it through the async proxy
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-
-  unsigned char* bs[NP];
-#pragma unroll
-  for (int s = 0; s < NP; ++s) bs[s] = a.base[s];
-  const uint64_t b0 = a.begin / kBlock;
-  const uint64_t coff = a.codes_off + a.begin, soff = a.scales_off + 4 * b0;
-  float* wtab = btab + warp * NP * 32;
-  unsigned char* ring = dsm + warp * C::kWarpBytes;
-  uint64_t* wb = bars + warp * C::kStages;
-  if (lane == 0) {
-    for (int s = 0; s < C::kStages; ++s) mbar_init(&wb[s], 1);
-    fence_mbar_init();
-  }
-  __syncwarp();
-  const uint64_t ntile = a.len / 512;
-  const uint64_t nw = (uint64_t)gridDim.x * 8;
-  const uint64_t gw = (uint64_t)blockIdx.x * 8 + warp;
-  const uint64_t policy = policy_evict_first();
-  auto issue = [&](uint64_t w, int s) {
-    if (lane == 0 && w < ntile) {
-      unsigned char* stg = ring + s * C::kStage;
-      mbar_arrive_expect_tx(&wb[s], C::kStage);
-#pragma unroll
-      for (int p = 0; p < NP; ++p) {
-        bulk_g2s(stg + p * C::kPiece, bs[p] + coff + w * 512, 512, &wb[s], policy);
-        const uint64_t sa = reinterpret_cast<uint64_t>(bs[p] + soff + 16 * w);
-        bulk_g2s(stg + p * C::kPiece + 512, reinterpret_cast<const void*>(sa & ~15ull), 32, &wb[s],
-                 policy);
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + tid; g < gpad; g += stride) {
+      const uint64_t len = g < ngroups ? a.len : 0;
+      reduce_group<0>(pt, g, len, (long long)b0, lut, a.err, true);
+      if (g * 16 < len) {
+        n_el += min((uint64_t)16, len - g * 16);
+        n_blk += (tid & 7) == 0;
       }
     }
-  };
-#pragma unroll
-  for (int s = 0; s < C::kStages; ++s) issue(gw + s * nw, s);
-  uint32_t phase = 0;
-  int s = 0;
-  for (uint64_t w = gw; w < ntile; w += nw) {
-    mbar_wait(&wb[s], (phase >> s) & 1u);
-    phase ^= 1u << s;
-    const unsigned char* stg = ring + s * C::kStage;
-    // every rank's buffer has the same layout: the window offset is common
-    const int so = (int)(((a.scales_off + 4 * b0 + 16 * w) & 15u) >> 2) + (lane >> 3);
-    uint32_t cw[NP][4];
-    float sc[NP];
-#pragma unroll
-    for (int p = 0; p < NP; ++p) {
-      const uint4 v = lds128(stg + p * C::kPiece + lane * 16);
-      cw[p][0] = v.x; cw[p][1] = v.y; cw[p][2] = v.z; cw[p][3] = v.w;
-      sc[p] = reinterpret_cast<const float*>(stg + p * C::kPiece + 512)[so];
-    }
-    __syncwarp();  // the stage is free again
-    issue(w + C::kStages * nw, s);
-    s = s + 1 == C::kStages ? 0 : s + 1;
-    reduce_store16<NP>(bs, coff, soff, w * 512 + lane * 16, cw, sc, (long long)b0, lut, a.err,
-                       wtab);
   }
-  // the partial last tile: per-thread path (whole warps, tables)
-  const uint64_t nblocks = (a.len + kBlock - 1) / kBlock;
-  const uint64_t ngroups = nblocks * 8;
-  const uint64_t g0 = ntile * 32;
-  if (g0 < ngroups) {
-    const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
-    const uint64_t gpad = g0 + (ngroups - g0 + 31) / 32 * 32;
-    for (uint64_t g = g0 + blockIdx.x * (uint64_t)blockDim.x + tid; g < gpad; g += stride)
-      fused_group<NP>(bs, a.codes_off + a.begin, a.scales_off + 4 * b0, g, g < ngroups ? a.len : 0,
-                      (long long)b0, lut, a.err, wtab);
+  // per-warp sums -> the communicator's counters (trace of what was moved)
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    n_el += __shfl_xor_sync(0xffffffffu, n_el, o);
+    n_blk += __shfl_xor_sync(0xffffffffu, n_blk, o);
   }
-  epoch_end(a);
+  if ((tid & 31) == 0 && n_el) {  // read from each of the P - 1 peers
+    atomicAdd(&a.stats[0], n_el * (a.P - 1));
+    atomicAdd(&a.stats[1], n_blk * (a.P - 1));
+  }
+  epoch_end(a, true);
 }
 
 // ---------------------------------------------------------------------------
@@ -594,8 +418,9 @@ struct PushArgs {
   uint64_t in_scales_off, in_codes_off;        // inbox (P slots, indexed by sender)
   uint64_t slot_scales, slot_codes;            // bytes per inbox slot
   uint64_t rg[2 * AGQ_MAX_WORLD];              // chunk [begin, end) per owner (elements)
-  uint64_t epoch;
+  uint64_t epoch, timeout_ns;
   unsigned int* done_counter;
+  unsigned long long* stats;                   // [elements, blocks] scattered (all peers)
   agq_errors* err;
   int rank, P;
 };
@@ -626,6 +451,20 @@ __global__ void __launch_bounds__(256) k_push_scatter(PushArgs a) {
   float* ds = reinterpret_cast<float*>(a.base[q] + a.in_scales_off +
                                        (uint64_t)a.rank * a.slot_scales);
   for (uint64_t j = tid; j < nbq; j += nth) ds[j] = ss[j];
+  // what this thread moved (16-byte vectors, tail bytes, scales), per warp
+  unsigned long long n_el = 0, n_blk = 0;
+  if (tid < nv) n_el += 16 * ((nv - 1 - tid) / nth + 1);
+  if (nv * 16 + tid < len) n_el += (len - nv * 16 - 1 - tid) / nth + 1;
+  if (tid < nbq) n_blk += (nbq - 1 - tid) / nth + 1;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    n_el += __shfl_xor_sync(0xffffffffu, n_el, o);
+    n_blk += __shfl_xor_sync(0xffffffffu, n_blk, o);
+  }
+  if ((threadIdx.x & 31) == 0 && (n_el | n_blk)) {
+    atomicAdd(&a.stats[0], n_el);
+    atomicAdd(&a.stats[1], n_blk);
+  }
   // publish "scattered" once every CTA's stores are performed system-wide
   __threadfence_system();
   __syncthreads();
@@ -635,35 +474,31 @@ __global__ void __launch_bounds__(256) k_push_scatter(PushArgs a) {
       __threadfence_system();
       for (int s = 0; s < a.P; ++s)
         if (s != a.rank)
-          st_release_sys(reinterpret_cast<uint64_t*>(a.base[s]) + kScatterOff + a.rank, a.epoch);
+          st_release_sys(reinterpret_cast<uint64_t*>(a.base[s]) + kScatteredOff + a.rank, a.epoch);
       *a.done_counter = 0u;
     }
   }
 }
 
+
 // pt: pieces in ascending sender rank (my own chunk, else my inbox slot of
 // that sender) and outputs = chunk [me] of every rank's buffer; built on the
-// host so it stays in the parameter bank.
+// host so it stays in the parameter bank. 2 CTAs per SM (3 measured equal at
+// 4 GPUs and spills the NP = 8 instance).
 template <int NP>
-#ifndef AGQ_PUSH_MINB
-#define AGQ_PUSH_MINB 2  // 3 measured equal at 4 GPUs and spills the NP = 8 instance
-#endif
-__global__ void __launch_bounds__(256, AGQ_PUSH_MINB) k_push_reduce(PushArgs a, PieceTable pt) {
+__global__ void __launch_bounds__(256, 2) k_push_reduce(PushArgs a, PieceTable pt) {
   __shared__ double lut[kDqTable];
   __shared__ float btab[8 * (NP > 0 ? NP : 1) * 32];
   __shared__ int ok;
   fill_fp8_dq_table(lut);
   const int tid = threadIdx.x;
-  uint64_t* my_flags = reinterpret_cast<uint64_t*>(a.base[a.rank]);
   if (tid == 0) {
-    ok = 1;
-    for (int s = 0; s < a.P; ++s)
-      if (s != a.rank && !wait_flag(my_flags + kScatterOff + s, a.epoch)) ok = 0;
+    ok = start_barrier(a, kScatteredOff, true) ? 1 : 0;
+    if (!ok) err_min(&a.err->overflow_block, -1);
   }
   __syncthreads();
   if (!ok) {
-    if (tid == 0) err_min(&a.err->overflow_block, -1);
-    epoch_end(a);
+    epoch_end(a, false);
     return;
   }
   const uint64_t begin = a.rg[2 * a.rank], len = a.rg[2 * a.rank + 1] - begin;
@@ -675,13 +510,13 @@ __global__ void __launch_bounds__(256, AGQ_PUSH_MINB) k_push_reduce(PushArgs a, 
   float* wtab = NP > 0 ? btab + (tid >> 5) * NP * 32 : nullptr;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + tid; g < gpad; g += stride)
     reduce_group<NP>(pt, g, g < ngroups ? len : 0, (long long)b0, lut, a.err, true, wtab);
-  epoch_end(a);
+  epoch_end(a, true);
 }
 
 __global__ void k_init_flags(uint64_t* flags) {
   const int i = threadIdx.x;
-  if (i < 64) flags[i] = 0;
-  else if (i < 64 + AGQ_MAX_WORLD) flags[i] = (uint64_t)kNone;
+  if (i < kOverflowOff) flags[i] = 0;
+  else if (i < kBadScaleOff + AGQ_MAX_WORLD) flags[i] = (uint64_t)kNone;
 }
 
 }  // namespace agqk
@@ -726,10 +561,21 @@ agq_status comm_init(agq_comm** out, const unsigned char id[128], int nranks, in
     delete c;
     return st;
   }
-  e = cudaMalloc(&c->done_counter, sizeof(unsigned int));
-  if (e == cudaSuccess) e = cudaMemset(c->done_counter, 0, sizeof(unsigned int));
-  if (e != cudaSuccess) return cuda_fail(e, "comm_init: counter");
+  e = cudaMalloc(&c->done_counter, 64);
+  if (e == cudaSuccess) e = cudaMemset(c->done_counter, 0, 64);
+  if (e == cudaSuccess) e = cudaMalloc(&c->stats, 2 * sizeof(unsigned long long));
+  if (e != cudaSuccess) {
+    comm_destroy(c);
+    return cuda_fail(e, "comm_init: counters");
+  }
   *out = c;
+  return AGQ_OK;
+}
+
+agq_status comm_set_timeout(agq_comm* c, double seconds) {
+  if (!(seconds > 0.0) || seconds > 1e6)
+    return set_error(AGQ_ERR_INVALID_ARGUMENT, "timeout must be in (0, 1e6] seconds");
+  c->timeout_ns = (uint64_t)(seconds * 1e9);
   return AGQ_OK;
 }
 
@@ -817,6 +663,7 @@ agq_status comm_destroy(agq_comm* c) {
   if (c->ring_scales) cudaFree(c->ring_scales);
   if (c->ring_sat) cudaFree(c->ring_sat);
   if (c->done_counter) cudaFree(c->done_counter);
+  if (c->stats) cudaFree(c->stats);
   if (c->nccl) nccl().CommDestroy(c->nccl);
   delete c;
   return AGQ_OK;
@@ -827,6 +674,32 @@ int comm_size(const agq_comm* c) { return c->nranks; }
 
 namespace {
 
+// One chunk message (collective.hpp:195-206 deliver: payload = codes + 4 *
+// scales of the block-aligned chunk).
+agq_trace_event chunk_event(int phase, int sender, int receiver, uint64_t begin, uint64_t len,
+                            uint32_t block) {
+  agq_trace_event e;
+  e.phase = phase;
+  e.sender = sender;
+  e.receiver = receiver;
+  e.chunk_start = begin;
+  e.chunk_len = len;
+  e.payload_bytes = len + 4 * ((len + block - 1) / block);
+  return e;
+}
+
+// Share this rank's data errors with every rank (min over ranks): the
+// reference's workers all abort on the same bad scale / overflow.
+agq_status share_errors(agq_comm* c, agq_errors* err, cudaStream_t s) {
+  if (!err) return AGQ_OK;
+  agq_status st = nccl_fail(nccl().GroupStart(), "ncclGroupStart");
+  if (st) return st;
+  nccl().AllReduce(&err->overflow_block, &err->overflow_block, 1, ncclInt64, ncclMin, c->nccl, s);
+  nccl().AllReduce(&err->bad_scale_block, &err->bad_scale_block, 1, ncclInt64, ncclMin, c->nccl,
+                   s);
+  return nccl_fail(nccl().GroupEnd(), "error flags");
+}
+
 agq_status allreduce_nccl(agq_comm* c, uint8_t* codes, float* scales, uint64_t n, uint32_t block,
                           agq_errors* err, cudaStream_t s) {
   const int P = c->nranks, r = c->rank;
@@ -834,22 +707,23 @@ agq_status allreduce_nccl(agq_comm* c, uint8_t* codes, float* scales, uint64_t n
   chunk_ranges(n, block, P, rg.data());
   uint64_t maxlen = 0;
   for (int q = 0; q < P; ++q) maxlen = std::max(maxlen, rg[2 * q + 1] - rg[2 * q]);
-  const uint64_t maxblk = (maxlen + block - 1) / block;
-  if (c->recv_chunk_cap < maxlen || !c->recv_codes) {
+  // receive slots sized for this call's chunk and block size
+  const uint64_t cap = round_up(maxlen ? maxlen : 1, 256);
+  const uint64_t scap = round_up((cap + block - 1) / block, 64);
+  if (!c->recv_codes || c->recv_chunk_cap < cap || c->recv_scale_cap < scap) {
     if (c->recv_codes) cudaFree(c->recv_codes);
     if (c->recv_scales) cudaFree(c->recv_scales);
     c->recv_codes = nullptr;
     c->recv_scales = nullptr;
+    c->recv_chunk_cap = c->recv_scale_cap = 0;
     const uint64_t slots = P > 1 ? P - 1 : 1;
-    const uint64_t cap = round_up(maxlen ? maxlen : 1, 256);
     cudaError_t e = cudaMalloc(&c->recv_codes, slots * cap);
-    if (e == cudaSuccess) e = cudaMalloc(&c->recv_scales, slots * round_up(cap / 128 * 4 + 1024, 256));
+    if (e == cudaSuccess) e = cudaMalloc(&c->recv_scales, slots * scap * 4);
     if (e != cudaSuccess) return cuda_fail(e, "allreduce: workspace");
     c->recv_chunk_cap = cap;
+    c->recv_scale_cap = scap;
   }
-  const uint64_t cap = c->recv_chunk_cap;
-  const uint64_t scap = round_up(cap / 128 * 4 + 1024, 256) / 4;
-  (void)maxblk;
+  const uint64_t ccap = c->recv_chunk_cap, sccap = c->recv_scale_cap;
   auto slot = [&](int q) { return q < r ? q : q - 1; };
   const uint64_t br = rg[2 * r], er = rg[2 * r + 1], lr = er - br;
   const uint64_t nbr = (lr + block - 1) / block;
@@ -862,10 +736,11 @@ agq_status allreduce_nccl(agq_comm* c, uint8_t* codes, float* scales, uint64_t n
     if (lq) {
       nccl().Send(codes + bq, lq, ncclUint8, q, c->nccl, s);
       nccl().Send(scales + bq / block, (lq + block - 1) / block, ncclFloat32, q, c->nccl, s);
+      c->trace.push_back(chunk_event(0, r, q, bq, lq, block));
     }
     if (lr) {
-      nccl().Recv(c->recv_codes + slot(q) * cap, lr, ncclUint8, q, c->nccl, s);
-      nccl().Recv(c->recv_scales + slot(q) * scap, nbr, ncclFloat32, q, c->nccl, s);
+      nccl().Recv(c->recv_codes + slot(q) * ccap, lr, ncclUint8, q, c->nccl, s);
+      nccl().Recv(c->recv_scales + slot(q) * sccap, nbr, ncclFloat32, q, c->nccl, s);
     }
   }
   st = nccl_fail(nccl().GroupEnd(), "all-to-all");
@@ -879,8 +754,8 @@ agq_status allreduce_nccl(agq_comm* c, uint8_t* codes, float* scales, uint64_t n
         pc[q] = codes + br;
         ps[q] = scales + br / block;
       } else {
-        pc[q] = c->recv_codes + slot(q) * cap;
-        ps[q] = c->recv_scales + slot(q) * scap;
+        pc[q] = c->recv_codes + slot(q) * ccap;
+        ps[q] = c->recv_scales + slot(q) * sccap;
       }
     }
     uint8_t* oc = codes + br;
@@ -889,13 +764,9 @@ agq_status allreduce_nccl(agq_comm* c, uint8_t* codes, float* scales, uint64_t n
                                (long long)(br / block), err, s);
     if (st) return st;
   }
-  // share an overflow with every rank (collective.hpp:278-281 aborts all)
-  if (err) {
-    st = nccl_fail(nccl().AllReduce(&err->overflow_block, &err->overflow_block, 1, ncclInt64,
-                                 ncclMin, c->nccl, s),
-                   "overflow flag");
-    if (st) return st;
-  }
+  // every rank raises the same error (collective.hpp:158-168, :278-281)
+  st = share_errors(c, err, s);
+  if (st) return st;
   // 3) all-gather: reduced chunk r -> every rank, received in place
   st = nccl_fail(nccl().GroupStart(), "ncclGroupStart");
   if (st) return st;
@@ -905,6 +776,7 @@ agq_status allreduce_nccl(agq_comm* c, uint8_t* codes, float* scales, uint64_t n
     if (lr) {
       nccl().Send(codes + br, lr, ncclUint8, q, c->nccl, s);
       nccl().Send(scales + br / block, nbr, ncclFloat32, q, c->nccl, s);
+      c->trace.push_back(chunk_event(1, r, q, br, lr, block));
     }
     if (lq) {
       nccl().Recv(codes + bq, lq, ncclUint8, q, c->nccl, s);
@@ -914,47 +786,12 @@ agq_status allreduce_nccl(agq_comm* c, uint8_t* codes, float* scales, uint64_t n
   return nccl_fail(nccl().GroupEnd(), "all-gather");
 }
 
-// Elements per thread: 16 (measured ~10% faster than 8 at 4 GPUs,
-// profiles/r01_p2p_ept_ctas_n4.log; with the block-table decode the NP = 8
-// instance fits 128 registers without spills). AGQ_P2P_EPT=8 selects the
-// 8-element kernel (16 lanes per block) for comparison.
-int fused_ept(int P) {
-  (void)P;
-  static const int forced = [] {
-    const char* e = getenv("AGQ_P2P_EPT");
-    return e ? atoi(e) : 0;
-  }();
-  return forced == 8 ? 8 : 16;
-}
+// Fused kernel grid: 2 co-resident CTAs per SM (256 threads, small smem).
+constexpr int kP2PCtasPerSm = 2;
 
-bool fused_tma() {
-  static const bool v = [] {
-    const char* e = getenv("AGQ_P2P_TMA");
-    return e && e[0] == '1';
-  }();
-  return v;
-}
-template <int NP>
-void launch_fused_tma(const FusedArgs& a, cudaStream_t s) {
-  using C = TmaCfg<NP>;
-  static const int occ = [] {
-    cudaFuncSetAttribute(k_fused_tma<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)C::kSmem);
-    int o = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_fused_tma<NP>, 256, C::kSmem);
-    return o < 1 ? 1 : o;
-  }();
-  k_fused_tma<NP><<<num_sms() * occ, 256, C::kSmem, s>>>(a);
-}
 template <int NP>
 void launch_fused(const FusedArgs& a, int grid, cudaStream_t s) {
-  if constexpr (NP > 0) {
-    if (fused_tma()) return launch_fused_tma<NP>(a, s);
-  }
-  if (fused_ept(a.P) == 8)
-    k_fused_allreduce<NP, 8><<<grid, 256, 0, s>>>(a);
-  else
-    k_fused_allreduce<NP, 16><<<grid, 256, 0, s>>>(a);
+  k_fused_allreduce<NP><<<grid, 256, 0, s>>>(a);
 }
 
 agq_status allreduce_p2p(agq_comm* c, uint8_t* codes, float* scales, uint64_t n, uint32_t block,
@@ -982,21 +819,21 @@ agq_status allreduce_p2p(agq_comm* c, uint8_t* codes, float* scales, uint64_t n,
   a.begin = rg[2 * r];
   a.len = rg[2 * r + 1] - rg[2 * r];
   a.epoch = ++c->epoch;
+  a.timeout_ns = c->timeout_ns;
   a.done_counter = c->done_counter;
+  a.stats = c->stats;
   a.err = err;
   a.rank = r;
   a.P = P;
-  static const int copy_only = getenv("AGQ_P2P_COPYONLY") ? 1 : 0;
-  a.copy_only = copy_only;
-  const uint64_t groups = (a.len + kBlock - 1) / kBlock * (fused_ept(P) == 8 && P <= 8 ? 16 : 8);
+  // trace: rank r pulls chunk r from every peer (sender s -> receiver r) and
+  // pushes the reduced chunk r to every peer (sender r -> receiver s)
+  for (int q = 0; q < P; ++q)
+    if (q != r && a.len) c->trace.push_back(chunk_event(0, q, r, a.begin, a.len, block));
+  for (int q = 0; q < P; ++q)
+    if (q != r && a.len) c->trace.push_back(chunk_event(1, r, q, a.begin, a.len, block));
+  const uint64_t groups = (a.len + kBlock - 1) / kBlock * 8;
   uint64_t grid = (groups + 255) / 256;
-  // co-resident grid (256 threads, small smem); AGQ_P2P_CTAS_PER_SM tunes it
-  static const int per_sm = [] {
-    const char* e = getenv("AGQ_P2P_CTAS_PER_SM");
-    const int v = e ? atoi(e) : 2;
-    return v < 1 ? 1 : (v > 8 ? 8 : v);
-  }();
-  const uint64_t cap = (uint64_t)num_sms() * per_sm;
+  const uint64_t cap = (uint64_t)num_sms() * kP2PCtasPerSm;
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
   switch (P) {
@@ -1031,6 +868,8 @@ agq_status allreduce_push(agq_comm* c, uint8_t* codes, float* scales, uint64_t n
   if (block != (uint32_t)kBlock) return set_error(AGQ_ERR_INVALID_ARGUMENT, "push all-reduce needs block 128");
   if (n > c->sym_cap) return set_error(AGQ_ERR_INVALID_ARGUMENT, "all-reduce larger than p2p capacity");
   if (!err) return set_error(AGQ_ERR_INVALID_ARGUMENT, "push all-reduce needs an error record");
+  const int P = c->nranks, r = c->rank;
+  if (P > 8) return set_error(AGQ_ERR_INVALID_ARGUMENT, "push all-reduce: world size 2..8");
   const SymLayout L = sym_layout(c->sym_cap, c->nranks);
   uint8_t* sc_codes = c->sym + L.codes_off;
   float* sc_scales = reinterpret_cast<float*>(c->sym + L.scales_off);
@@ -1040,7 +879,6 @@ agq_status allreduce_push(agq_comm* c, uint8_t* codes, float* scales, uint64_t n
     cudaMemcpyAsync(sc_codes, codes, n, cudaMemcpyDeviceToDevice, s);
     cudaMemcpyAsync(sc_scales, scales, nb * 4, cudaMemcpyDeviceToDevice, s);
   }
-  const int P = c->nranks, r = c->rank;
   std::vector<uint64_t> rg(2 * P);
   chunk_ranges(n, block, P, rg.data());
   PushArgs a{};
@@ -1053,32 +891,32 @@ agq_status allreduce_push(agq_comm* c, uint8_t* codes, float* scales, uint64_t n
   a.slot_scales = L.slot_scales;
   a.slot_codes = L.slot_codes;
   a.epoch = ++c->epoch;
+  a.timeout_ns = c->timeout_ns;
   a.done_counter = c->done_counter;
+  a.stats = c->stats;
   a.err = err;
   a.rank = r;
   a.P = P;
   uint64_t maxlen = 0;
   for (int q = 0; q < P; ++q) maxlen = std::max<uint64_t>(maxlen, rg[2 * q + 1] - rg[2 * q]);
+  const uint64_t begin = rg[2 * r], len = rg[2 * r + 1] - begin;
+  for (int q = 0; q < P; ++q) {
+    const uint64_t lq = rg[2 * q + 1] - rg[2 * q];
+    if (q != r && lq) c->trace.push_back(chunk_event(0, r, q, rg[2 * q], lq, block));
+  }
+  for (int q = 0; q < P; ++q)
+    if (q != r && len) c->trace.push_back(chunk_event(1, r, q, begin, len, block));
   // scatter: ~2 CTAs per SM in total across the P-1 peers
   uint64_t gx = (maxlen / 16 + 1023) / 1024;
   const uint64_t cap_x = std::max<uint64_t>(1, (uint64_t)num_sms() * 2 / (P - 1));
   gx = std::min<uint64_t>(std::max<uint64_t>(gx, 1), cap_x);
-  // AGQ_PUSH_TIMING=1 (diagnostics only): per-phase device time on stderr
-  static const bool timing = getenv("AGQ_PUSH_TIMING") != nullptr;
-  cudaEvent_t ev[3];
-  if (timing) {
-    for (auto& e : ev) cudaEventCreate(&e);
-    cudaEventRecord(ev[0], s);
-  }
   k_push_scatter<<<dim3((unsigned)gx, (unsigned)(P - 1)), 256, 0, s>>>(a);
   count_launch();
-  if (timing) cudaEventRecord(ev[1], s);
   agq_status st = cuda_fail(cudaGetLastError(), "push all-reduce: scatter launch");
   if (st) return st;
   PieceTable pt{};
   pt.np = P;
   pt.nout = P;
-  const uint64_t begin = rg[2 * r];
   for (int q = 0; q < P; ++q) {
     if (q == r) {
       pt.codes[q] = c->peer[r] + L.codes_off + begin;
@@ -1091,9 +929,10 @@ agq_status allreduce_push(agq_comm* c, uint8_t* codes, float* scales, uint64_t n
     pt.out_codes[q] = c->peer[q] + L.codes_off + begin;
     pt.out_scales[q] = reinterpret_cast<float*>(c->peer[q] + L.scales_off) + begin / kBlock;
   }
-  const uint64_t groups = (rg[2 * r + 1] - rg[2 * r] + kBlock - 1) / kBlock * 8;
+  const uint64_t groups = (len + kBlock - 1) / kBlock * 8;
   uint64_t grid = (groups + 255) / 256;
-  grid = std::min<uint64_t>(std::max<uint64_t>(grid, 1), (uint64_t)num_sms() * AGQ_PUSH_MINB);
+  grid = std::min<uint64_t>(std::max<uint64_t>(grid, 1), (uint64_t)num_sms() * 2);
+  // the scatter kernel reset the CTA counter; the reduce kernel reuses it
   switch (P) {
     case 2: launch_push_reduce<2>(a, pt, (int)grid, s); break;
     case 3: launch_push_reduce<3>(a, pt, (int)grid, s); break;
@@ -1107,16 +946,6 @@ agq_status allreduce_push(agq_comm* c, uint8_t* codes, float* scales, uint64_t n
   count_launch();
   st = cuda_fail(cudaGetLastError(), "push all-reduce: reduce launch");
   if (st) return st;
-  if (timing) {
-    cudaEventRecord(ev[2], s);
-    cudaEventSynchronize(ev[2]);
-    float t1 = 0, t2 = 0;
-    cudaEventElapsedTime(&t1, ev[0], ev[1]);
-    cudaEventElapsedTime(&t2, ev[1], ev[2]);
-    fprintf(stderr, "push all-reduce rank %d n=%llu: scatter %.3f ms, reduce+gather %.3f ms\n", r,
-            (unsigned long long)n, t1, t2);
-    for (auto& e : ev) cudaEventDestroy(e);
-  }
   if (!inplace) {
     cudaMemcpyAsync(codes, sc_codes, n, cudaMemcpyDeviceToDevice, s);
     cudaMemcpyAsync(scales, sc_scales, nb * 4, cudaMemcpyDeviceToDevice, s);
@@ -1128,17 +957,44 @@ agq_status allreduce_push(agq_comm* c, uint8_t* codes, float* scales, uint64_t n
 
 agq_status allreduce_fp8(agq_comm* c, uint8_t* codes, float* scales, uint64_t n, uint32_t block,
                          int algo, agq_errors* err, cudaStream_t s) {
+  c->trace.clear();
+  c->trace_algo = algo;
+  c->trace_stream = s;
   if (n == 0) return AGQ_OK;
-  if (c->nranks == 1) {
+  if (c->nranks == 1 && algo == AGQ_AR_NCCL) {
     // P = 1: the reference still re-quantizes acc = 0 + dequant (signed
-    // zeros normalise), so run the reduce with one piece.
+    // zeros normalise), so run the reduce with one piece. No messages.
     const uint8_t* pc = codes;
     const float* ps = scales;
     return reduce_requant_device(1, &pc, &ps, n, block, 1, &codes, &scales, 0, err, s);
   }
-  if (algo == AGQ_AR_FUSED_P2P) return allreduce_p2p(c, codes, scales, n, block, err, s);
-  if (algo == AGQ_AR_PUSH_P2P) return allreduce_push(c, codes, scales, n, block, err, s);
+  if (algo == AGQ_AR_FUSED_P2P || algo == AGQ_AR_PUSH_P2P) {
+    cudaError_t e = cudaMemsetAsync(c->stats, 0, 2 * sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return cuda_fail(e, "all-reduce: stats");
+    // one rank: the fused kernel (barriers and reduce with itself); the
+    // push algorithm has no peer to scatter to
+    return algo == AGQ_AR_FUSED_P2P || c->nranks == 1
+               ? allreduce_p2p(c, codes, scales, n, block, err, s)
+               : allreduce_push(c, codes, scales, n, block, err, s);
+  }
   return allreduce_nccl(c, codes, scales, n, block, err, s);
+}
+
+agq_status comm_last_trace(agq_comm* c, agq_trace_event* events, int cap, int* count,
+                           unsigned long long* moved) {
+  *count = (int)c->trace.size();
+  for (int i = 0; i < (int)c->trace.size() && i < cap; ++i) events[i] = c->trace[i];
+  if (moved) {
+    moved[0] = moved[1] = 0;
+    if (c->trace_algo == AGQ_AR_FUSED_P2P || c->trace_algo == AGQ_AR_PUSH_P2P) {
+      // kernel-side counters of the last P2P call (elements, blocks)
+      if (c->trace_stream) cudaStreamSynchronize(c->trace_stream);
+      cudaError_t e = cudaMemcpy(moved, c->stats, 2 * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) return cuda_fail(e, "last_trace: counters");
+    }
+  }
+  return AGQ_OK;
 }
 
 // allreduce_naive_fp8 (collective.hpp:338-431) on real ranks: P-1 ring

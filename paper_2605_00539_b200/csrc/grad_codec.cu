@@ -8,11 +8,10 @@
 //   sum      = fp32 adds in the reference's order (+0.0f first for K4)
 //   requant  = fresh block absmax, exact E4M3 rounding (agq_numerics.cuh)
 //
-// K3 tiled path (block 128): 512-thread CTAs, two per SM, 16 elements per
-// thread (8 threads per block), 8192-element tiles double-buffered through
-// shared memory by 1-D TMA bulk loads (codes + scales + local gradient in
-// one mbarrier transaction) and drained by bulk stores. One pass over HBM:
-// 1 + 4/128 bytes in, 4 (or 2) bytes of local gradient in, 1 + 4/128 out.
+// K3 (block 128): warp-autonomous persistent kernel, 16 elements per lane
+// (8 lanes per block), one pass over HBM: 1 + 4/128 bytes in, 4 (or 2) bytes
+// of local gradient in, 1 + 4/128 out. (A TMA tile pipeline was built,
+// verified bit-exact and measured slower.)
 //
 // K4 uses plain 128-bit loads so that any piece may live in another GPU's
 // memory (NVLink peer pointers) — the fused all-reduce runs the same code.
@@ -23,141 +22,7 @@
 namespace agqk {
 
 // ---------------------------------------------------------------------------
-// K3: tiled fused accumulate
-// ---------------------------------------------------------------------------
-constexpr int kAccThreads = 512;
-
-template <bool BF16L, int PREC>
-__global__ void __launch_bounds__(kAccThreads, 2)
-    k_accumulate_tiled(const uint8_t* codes, const float* scales, const void* local,
-                       uint64_t ntiles, uint8_t* out_codes, float* out_scales,
-                       agq_errors* err) {
-  constexpr int kStages = 2;
-  constexpr uint32_t kCodeB = kTileElems;                 // 8192
-  constexpr uint32_t kScB = kTileBlocks * 4;              // 256
-  constexpr uint32_t kLocB = kTileElems * (BF16L ? 2 : 4);
-  constexpr uint32_t kStageB = kCodeB + kScB + kLocB;
-  constexpr uint32_t kOutB = kCodeB + kScB;
-
-  extern __shared__ __align__(128) unsigned char smem[];
-  unsigned char* in_buf = smem;
-  unsigned char* out_buf = smem + kStages * kStageB;
-  double* lut = reinterpret_cast<double*>(out_buf + 2 * kOutB);
-  uint64_t* full = reinterpret_cast<uint64_t*>(lut + kDqTable);
-
-  const int tid = threadIdx.x;
-  const uint64_t policy = policy_evict_first();
-  fill_fp8_dq_table(lut);
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  auto issue_load = [&](uint64_t t, int s) {
-    unsigned char* d = in_buf + s * kStageB;
-    mbar_arrive_expect_tx(&full[s], kStageB);
-    bulk_g2s(d, codes + t * kCodeB, kCodeB, &full[s], policy);
-    bulk_g2s(d + kCodeB, scales + t * kTileBlocks, kScB, &full[s], policy);
-    bulk_g2s(d + kCodeB + kScB, static_cast<const unsigned char*>(local) + t * kLocB, kLocB,
-             &full[s], policy);
-  };
-  if (tid == 0)
-    for (int s = 0; s < kStages; ++s) {
-      const uint64_t t = blockIdx.x + (uint64_t)s * gridDim.x;
-      if (t < ntiles) issue_load(t, s);
-    }
-
-  // f32 local: 4 chunks of 4 elements, rotation (tid>>1)&3 (conflict-free
-  // 64-byte rows); bf16 local: 2 chunks of 8, rotation (tid>>2)&1. Code
-  // words (4 codes each) are rotated to match: r = rot (f32) / 2*rot (bf16).
-  const int rot = BF16L ? ((tid >> 2) & 1) : ((tid >> 1) & 3);
-  const int wrot = BF16L ? 2 * rot : rot;
-  const int lblk = tid >> 3;
-
-  for (uint64_t it = 0;; ++it) {
-    const uint64_t t = blockIdx.x + it * gridDim.x;
-    if (t >= ntiles) break;
-    const int s = (int)(it % kStages);
-    mbar_wait(&full[s], (uint32_t)((it / kStages) & 1));
-    const unsigned char* sb = in_buf + s * kStageB;
-    const uint4 cv = lds128(sb + tid * 16);
-    uint32_t cw[4] = {cv.x, cv.y, cv.z, cv.w};
-    rotl4(cw, wrot);
-    const float sc = reinterpret_cast<const float*>(sb + kCodeB)[lblk];
-    const unsigned char* lrow = sb + kCodeB + kScB + tid * (BF16L ? 32 : 64);
-    float l[16];
-    if constexpr (BF16L) {
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const uint4 v = lds128(lrow + ((j + rot) & 1) * 16);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          l[8 * j + 2 * k] = u2f(w[k] << 16);
-          l[8 * j + 2 * k + 1] = u2f(w[k] & 0xffff0000u);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint4 v = lds128(lrow + ((j + rot) & 3) * 16);
-        l[4 * j] = u2f(v.x); l[4 * j + 1] = u2f(v.y);
-        l[4 * j + 2] = u2f(v.z); l[4 * j + 3] = u2f(v.w);
-      }
-    }
-    const uint64_t gblk = t * kTileBlocks + lblk;
-    if (!(sc >= 0.0f) || !(sc <= 3.402823466e38f)) {
-      if ((tid & 7) == 0) err_min(&err->bad_scale_block, (long long)gblk);
-    }
-    const double sd = (double)sc;
-    float v[16];
-    uint32_t lbad = 0;
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const uint32_t c = (cw[e >> 2] >> (8 * (e & 3))) & 0xffu;
-      lbad |= (uint32_t)((f2u(l[e]) & 0x7f800000u) == 0x7f800000u) << e;
-      v[e] = apply_prec<PREC>(fadd(fp8_dequant(c, sd, lut, dq_fast(sc)), l[e]));
-    }
-    if (lbad) {
-      // lowest non-finite local element of this thread (slot order -> index)
-      for (int e = 0; e < 16; ++e)
-        if (lbad >> e & 1) {
-          const int per = BF16L ? 8 : 4, nch = BF16L ? 2 : 4;
-          const int slot = e / per, within = e % per;
-          const int chunk = (slot + rot) & (nch - 1);
-          err_min(&err->nonfinite_local,
-                  (long long)(t * kTileElems + tid * 16 + chunk * per + within));
-        }
-    }
-    const uint32_t m = absmax_bits16(v);
-    if (m >= 0x7f800000u && (tid & 7) == 0) err_min(&err->nonfinite_block, (long long)gblk);
-    const float a = u2f(m);
-    uint32_t ow[4];
-    fp8_requant16(v, a, ow);
-    rotr4(ow, wrot);
-
-    const int ob = (int)(it & 1);
-    if (tid == 0) bulk_wait_read<1>();
-    __syncthreads();
-    unsigned char* obuf = out_buf + ob * kOutB;
-    sts128(obuf + tid * 16, make_uint4(ow[0], ow[1], ow[2], ow[3]));
-    if ((tid & 7) == 0) reinterpret_cast<float*>(obuf + kCodeB)[lblk] = a;
-    fence_proxy_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-      bulk_s2g(out_codes + t * kCodeB, obuf, kCodeB);
-      bulk_s2g(out_scales + t * kTileBlocks, obuf + kCodeB, kScB);
-      bulk_commit();
-      const uint64_t nt = t + (uint64_t)kStages * gridDim.x;
-      if (nt < ntiles) issue_load(nt, s);
-    }
-  }
-  if (tid == 0) bulk_wait_all<0>();
-}
-
-// ---------------------------------------------------------------------------
-// K3 warp-autonomous variant (default): each warp streams 512-element tiles
+// K3: each warp streams 512-element tiles
 // (16 per lane, 8 lanes per 128-block). Codes (16 B/lane) and the block
 // scale are loaded straight to registers; the local gradient is loaded with
 // coalesced 128-bit loads into a private swizzled shared slot so each lane
@@ -199,9 +64,11 @@ __device__ __noinline__ void acc_report_nonfinite(const unsigned char* wb, int l
   if ((lane & 7) == 0) err_min(&err->nonfinite_block, (long long)gblk);
 }
 
+// Resident CTAs per SM: 3, except the FP32-local BF16-rounded instance,
+// which spills at 3 and runs 356 -> 315 us at 2^28 at 2
+// (profiles/r01_acc_prec_ab.log).
 template <bool BF16L, int PREC>
-__global__ void __launch_bounds__(kAccWarps * 32, !BF16L && PREC == AGQ_ACC_BF16 ? AGQ_ACC_MINB_BF16R
-                                                  : BF16L && PREC != AGQ_ACC_BF16 ? AGQ_ACC_MINB_BF16L : 3)
+__global__ void __launch_bounds__(kAccWarps * 32, !BF16L && PREC == AGQ_ACC_BF16 ? 2 : 3)
     k_accumulate_warp(const uint8_t* codes, const float* scales, const void* local,
                       uint64_t ntiles, uint8_t* out_codes, float* out_scales, agq_errors* err) {
   constexpr int kCh = BF16L ? 2 : 4;
@@ -265,8 +132,7 @@ __global__ void __launch_bounds__(kAccWarps * 32, !BF16L && PREC == AGQ_ACC_BF16
     // block-table decode for the FP32-local / FP32-sum kernel (shared-memory
     // bound on the 256-entry table: 86% -> 93% of HBM); the BF16-local and
     // rounded-precision instances measured faster with the full table
-    constexpr bool kTab = AGQ_ACC_TAB && (!BF16L || AGQ_ACC_TAB_BF16L) &&
-                          (PREC == 0 || AGQ_ACC_TAB_PREC);
+    constexpr bool kTab = !BF16L && PREC == 0;
     if (kTab && dq_fast(sc) && fp8_tab_ok16(cw)) {
       // v = l + dq (exact product, one rounding: = fadd(dq, l))
 #pragma unroll
@@ -350,12 +216,9 @@ __global__ void k_reduce_generic(PieceTable pt, uint64_t len, uint32_t block, ui
   const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
   for (uint64_t b = warp; b < nblocks; b += nwarps) {
     const uint64_t beg = b * block, end = min(len, beg + block);
-    uint32_t m = 0;
-    for (int p = 0; p < pt.np; ++p) {
-      const float sc = pt.scales[p][b];
-      if (lane == 0 && (!(sc >= 0.0f) || !(sc <= 3.402823466e38f)))
-        err_min(&err->bad_scale_block, blk_base + (long long)b);
-    }
+    uint32_t m = 0, sbad = 0;
+    for (int p = 0; p < pt.np; ++p) sbad |= bad_scale_bit(pt.scales[p][b], p);
+    if (lane == 0 && sbad) err_min(&err->bad_scale_block, bad_scale_key(sbad, blk_base + (long long)b));
     for (uint64_t i = beg + lane; i < end; i += 32) {
       float acc = 0.0f;
       for (int p = 0; p < pt.np; ++p)
@@ -381,11 +244,8 @@ __global__ void k_reduce_generic(PieceTable pt, uint64_t len, uint32_t block, ui
   }
 }
 
-#ifndef AGQ_RED_MINB
-#define AGQ_RED_MINB 1
-#endif
 template <int NP>
-__global__ void __launch_bounds__(256, AGQ_RED_MINB)
+__global__ void __launch_bounds__(256, 1)
     k_reduce128(PieceTable pt, uint64_t len, long long blk_base, int vec, agq_errors* err) {
   __shared__ double lut[kDqTable];
   __shared__ float btab[NP > 0 ? 8 * NP * 32 : 1];  // 8 warps x NP pieces x 32 entries
@@ -410,7 +270,7 @@ __global__ void __launch_bounds__(256, AGQ_RED_MINB)
 // ragged tail goes through reduce_group. Same arithmetic (reduce_compute), so
 // bit-identical.
 template <int NP, int S>
-__global__ void __launch_bounds__(256, AGQ_RED_MINB)
+__global__ void __launch_bounds__(256, 1)
     k_reduce128_pipe(PieceTable pt, uint64_t len, long long blk_base, agq_errors* err) {
   extern __shared__ __align__(16) unsigned char ring_smem[];
   __shared__ double lut[kDqTable];
@@ -588,47 +448,10 @@ int gen_grid(uint64_t work, int threads) {
   return (int)(g < 1 ? 1 : (g > cap ? cap : g));
 }
 
-template <bool BF16L, int PREC>
-agq_status launch_acc_tiled(const uint8_t* codes, const float* scales, const void* local,
-                            uint64_t ntiles, uint8_t* oc, float* os, agq_errors* err,
-                            cudaStream_t s) {
-  const size_t stage = kTileElems + kTileBlocks * 4 + (size_t)kTileElems * (BF16L ? 2 : 4);
-  const size_t smem = 2 * stage + 2 * (kTileElems + kTileBlocks * 4) + kDqTable * 8 + 2 * 8;
-  auto k = k_accumulate_tiled<BF16L, PREC>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return cuda_fail(e, "accumulate: smem attribute");
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kAccThreads, smem);
-  if (occ < 1) occ = 1;
-  const uint64_t g = (uint64_t)num_sms() * occ;
-  k<<<(int)(ntiles < g ? ntiles : g), kAccThreads, smem, s>>>(codes, scales, local, ntiles, oc,
-                                                               os, err);
-  count_launch();
-  return cuda_fail(cudaGetLastError(), "accumulate: launch");
-}
-
-template <bool BF16L>
-agq_status acc_tiled_prec(int prec, const uint8_t* codes, const float* scales,
-                          const void* local, uint64_t ntiles, uint8_t* oc, float* os,
-                          agq_errors* err, cudaStream_t s) {
-  if (prec == AGQ_ACC_BF16) return launch_acc_tiled<BF16L, AGQ_ACC_BF16>(codes, scales, local, ntiles, oc, os, err, s);
-  if (prec == AGQ_ACC_FP16) return launch_acc_tiled<BF16L, AGQ_ACC_FP16>(codes, scales, local, ntiles, oc, os, err, s);
-  return launch_acc_tiled<BF16L, AGQ_ACC_FP32>(codes, scales, local, ntiles, oc, os, err, s);
-}
-
-// K4 kernel choice: the cp.async ring (default; AGQ_RED_STAGES = ring depth,
-// 2 unless set) or the direct-load kernel (AGQ_RED_PIPE=0, or unaligned
-// pointers / P > 8).
-int red_stages() {
-  static const int v = [] {
-    const char* e = getenv("AGQ_RED_PIPE");
-    if (e && e[0] == '0') return 0;
-    const char* st = getenv("AGQ_RED_STAGES");
-    const int k = st ? atoi(st) : 2;
-    return k < 2 ? 2 : (k > 4 ? 4 : k);
-  }();
-  return v;
-}
+// K4: the cp.async ring kernel (2 stages; 3 tie, 4 lose at P = 8,
+// profiles/r01_reduce_pipe_ab.log) for 16-byte aligned pieces of >= 512
+// elements, else the direct-load kernel.
+constexpr int kRedStages = 2;
 
 template <int NP, int S>
 bool launch_reduce_pipe(const PieceTable& pt, uint64_t len, long long bb, agq_errors* err,
@@ -654,10 +477,7 @@ template <int NP>
 void launch_reduce128(const PieceTable& pt, uint64_t len, long long bb, int vec, agq_errors* err,
                       cudaStream_t s) {
   if constexpr (NP > 0) {
-    const int st = vec && len >= 512 ? red_stages() : 0;
-    if (st == 2 && launch_reduce_pipe<NP, 2>(pt, len, bb, err, s)) return;
-    if (st == 3 && launch_reduce_pipe<NP, 3>(pt, len, bb, err, s)) return;
-    if (st == 4 && launch_reduce_pipe<NP, 4>(pt, len, bb, err, s)) return;
+    if (vec && len >= 512 && launch_reduce_pipe<NP, kRedStages>(pt, len, bb, err, s)) return;
   }
   const uint64_t groups = (len + kBlock - 1) / kBlock * 8;
   int grid = gen_grid(groups, 256);
@@ -666,16 +486,6 @@ void launch_reduce128(const PieceTable& pt, uint64_t len, long long bb, int vec,
 }  // namespace
 
 namespace {
-// K3 variant: warp-autonomous (default) or the TMA tile pipeline
-// (AGQ_ACC_KERNEL=tma).
-bool acc_warp() {
-  static const bool w = [] {
-    const char* e = getenv("AGQ_ACC_KERNEL");
-    return !(e && e[0] == 't');
-  }();
-  return w;
-}
-
 template <bool BF16L, int PREC>
 agq_status launch_acc_warp(const uint8_t* codes, const float* scales, const void* local,
                            uint64_t ntiles, uint8_t* oc, float* os, agq_errors* err,
@@ -707,19 +517,15 @@ agq_status accumulate_device(const uint8_t* codes, const float* scales, const vo
                              uint8_t* oc, float* os, agq_errors* err, cudaStream_t s) {
   if (n == 0) return AGQ_OK;
   const bool bf16l = local_dtype == AGQ_BF16;
-  const uint64_t unit = acc_warp() ? (uint64_t)kAccWarpElems : (uint64_t)kTileElems;
+  const uint64_t unit = kAccWarpElems;
   uint64_t ntiles = 0;
   if (block == (uint32_t)kBlock && aligned16(codes) && aligned16(scales) && aligned16(local) &&
       aligned16(oc) && aligned16(os))
     ntiles = n / unit;
   if (ntiles) {
-    agq_status r;
-    if (acc_warp())
-      r = bf16l ? acc_warp_prec<true>(prec, codes, scales, local, ntiles, oc, os, err, s)
-                : acc_warp_prec<false>(prec, codes, scales, local, ntiles, oc, os, err, s);
-    else
-      r = bf16l ? acc_tiled_prec<true>(prec, codes, scales, local, ntiles, oc, os, err, s)
-                : acc_tiled_prec<false>(prec, codes, scales, local, ntiles, oc, os, err, s);
+    const agq_status r =
+        bf16l ? acc_warp_prec<true>(prec, codes, scales, local, ntiles, oc, os, err, s)
+              : acc_warp_prec<false>(prec, codes, scales, local, ntiles, oc, os, err, s);
     if (r != AGQ_OK) return r;
   }
   const uint64_t done = ntiles * unit;

@@ -227,3 +227,65 @@ class ActivationStore:
         for e in self.entries.values():
             tot += e.nbytes() if isinstance(e, QuantizedTensor) else e.numel() * e.element_size()
         return tot
+
+
+class StageActivationStore:
+    """Every layer's SavedActivations (layers.hpp:180-192, stored set
+    :266-301) of one pipeline stage under the stage's policy
+    (dbca.hpp:172-177 stage_policy): store() quantizes the quantized tensors
+    of ALL layers in one grouped launch per width (LLaMA-8B at 8 stages: 4
+    layers x 5 tensors = 20 tensors, one launch); read_all() dequantizes them
+    back in one grouped launch with the reference's validate checks."""
+
+    def __init__(self, policy: ActivationPolicy):
+        policy.validate()
+        self.policy = policy
+        self.layers: list = []
+
+    def store(self, layers, stream=None, check: bool = True, errors: ErrorRecord | None = None):
+        self.layers = [dict() for _ in layers]
+        by_bits: Dict[int, list] = {}
+        for li, tensors in enumerate(layers):
+            for name, t in tensors.items():
+                e = self.policy.at(STORED_TENSORS[name])
+                if e.bit_width == 0:
+                    self.layers[li][name] = t
+                else:
+                    by_bits.setdefault(e.bit_width, []).append((li, name))
+        for bits, keys in by_bits.items():
+            qs = quantize_grouped([layers[li][n] for li, n in keys], bits,
+                                  CodecKind.SymmetricLinear, stream=stream, check=check,
+                                  errors=errors)
+            for (li, n), q in zip(keys, qs):
+                self.layers[li][n] = q
+
+    def read(self, layer: int, name: str, out_dtype: torch.dtype = torch.bfloat16, stream=None):
+        if layer >= len(self.layers) or name not in self.layers[layer]:
+            raise RuntimeError(f"saved activations: missing tensor '{name}' required by the policy")
+        e = self.layers[layer][name]
+        if isinstance(e, QuantizedTensor):
+            return dequantize_grouped([e], out_dtype, stream=stream)[0]
+        return e
+
+    def read_all(self, out_dtype: torch.dtype = torch.bfloat16, stream=None, check: bool = True):
+        out = [dict() for _ in self.layers]
+        by_bits: Dict[int, list] = {}
+        for li, d in enumerate(self.layers):
+            for name, e in d.items():
+                if isinstance(e, QuantizedTensor):
+                    by_bits.setdefault(e.bit_width, []).append((li, name))
+                else:
+                    out[li][name] = e
+        for bits, keys in by_bits.items():
+            ts = dequantize_grouped([self.layers[li][n] for li, n in keys], out_dtype,
+                                    stream=stream, check=check)
+            for (li, n), t in zip(keys, ts):
+                out[li][n] = t
+        return out
+
+    def nbytes(self) -> int:
+        tot = 0
+        for d in self.layers:
+            for e in d.values():
+                tot += e.nbytes() if isinstance(e, QuantizedTensor) else e.numel() * e.element_size()
+        return tot

@@ -17,7 +17,7 @@ from typing import Sequence
 import torch
 
 from . import _lib as L
-from .codec import CodecKind, ErrorRecord, QuantizedTensor, _require_cuda, _stream
+from .codec import CodecKind, ErrorRecord, QuantizedTensor, _require_cuda, _stream, validate
 
 
 class AccumulatePrecision(enum.IntEnum):  # collective.hpp:99
@@ -43,6 +43,7 @@ def local_accumulate(main: QuantizedTensor, local_grad: torch.Tensor,
     n = main.num_elements()
     if local_grad.numel() != n:
         raise L.InvalidArgument("local gradient shape mismatch")
+    validate(main)  # dequantize_blockwise's structural checks (data checks on device)
     _require_cuda(local_grad, "local_grad")
     ldt = L.AGQ_BF16 if local_grad.dtype == torch.bfloat16 else L.AGQ_F32
     if local_grad.dtype not in (torch.float32, torch.bfloat16):
@@ -93,6 +94,7 @@ def _check_world(mains: Sequence[QuantizedTensor]):
     for q in mains:
         if q.shape != s0 or q.block_size != b0:
             raise L.InvalidArgument("all-reduce aborted: main gradient shapes must match")
+        validate(q)  # collective.hpp:166 (structural part; data checks on device)
 
 
 def allreduce_simulated(mains: Sequence[QuantizedTensor], stream=None, check: bool = True,

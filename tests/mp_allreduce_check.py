@@ -3,7 +3,10 @@ one process per GPU). Every rank regenerates every rank's FP8 gradient from
 its seed, so each rank checks its result against the CPU oracle's
 allreduce_decomposed bit for bit, for both algorithms (NCCL grouped
 send/recv + reduce kernel; fused NVLink peer-memory kernel), ragged sizes,
-P=1..world, and the overflow abort (collective.hpp:278-281) on every rank."""
+P=1..world, the overflow and bad-scale aborts on every rank
+(collective.hpp:158-168, :278-281), the message trace each algorithm
+records against the reference's MessageTrace (collective.hpp:195-206), and
+the barrier timeout (a rank that never arrives fails every rank)."""
 import os
 import sys
 
@@ -79,6 +82,26 @@ def main():
             if not ok:
                 fails += 1
                 print(f"rank {rank}: MISMATCH algo={algo} n={n}", flush=True)
+            # trace of what the real collective issued == the reference's trace
+            mine, moved = comm.last_trace()
+            full = comm.gather_trace()
+            want_t = A.decomposed_trace(n, 128, world)
+            if [tuple(e.__dict__.values()) for e in full] != \
+                    [tuple(e.__dict__.values()) for e in want_t]:
+                fails += 1
+                print(f"rank {rank}: TRACE MISMATCH algo={algo} n={n} {full[:3]} vs {want_t[:3]}",
+                      flush=True)
+            alg = "p2p" if algo == "auto" else algo
+            if alg in ("p2p", "push") and world > 1:
+                # the kernel's own counters of the phase-1 traffic
+                if alg == "p2p":
+                    a2a = [e for e in mine if e.phase == "all_to_all" and e.receiver == rank]
+                else:
+                    a2a = [e for e in mine if e.phase == "all_to_all" and e.sender == rank]
+                want_m = (sum(e.chunk_len for e in a2a), sum((e.chunk_len + 127) // 128 for e in a2a))
+                if moved != want_m:
+                    fails += 1
+                    print(f"rank {rank}: MOVED {moved} != {want_m} algo={algo} n={n}", flush=True)
     # allreduce_naive_fp8 (collective.hpp:338-431) on real ranks: codes,
     # scales and overflow_elements against the oracle; this rank's
     # overflow_events against the one-device simulation.
@@ -136,6 +159,63 @@ def main():
                 if "fp32 overflow" not in str(e):
                     fails += 1
                     print(f"rank {rank}: wrong error {e}", flush=True)
+    # a bad (negative) block scale on some workers aborts every rank with
+    # the reference's error: the lowest worker's lowest bad block
+    # (collective.hpp:158-168 check_workers -> validate, quantize.hpp:170-175)
+    n = 8192 * 3 + 300
+    nb = (n + 127) // 128
+    bad = {min(1, world - 1): [150, 40], world - 1: [7]}
+    want_blk = min(bad[min(bad)])
+    for algo in ("nccl", "p2p", "push"):
+        c, s = grads(world, n, 123)[rank]
+        s = s.copy()
+        for b in bad.get(rank, []):
+            s[b % nb] = -1.0
+        if algo in ("p2p", "push"):
+            pc, ps = comm.p2p_buffers(n)
+            pc.copy_(torch.from_numpy(c))
+            ps.copy_(torch.from_numpy(s))
+            q = A.QuantizedTensor(pc, ps, 8, 128, (n,), A.CodecKind.Fp8E4M3, packed=False)
+        else:
+            q = A.QuantizedTensor(torch.from_numpy(c).to(dev), torch.from_numpy(s).to(dev), 8, 128,
+                                  (n,), A.CodecKind.Fp8E4M3, packed=False)
+        try:
+            comm.allreduce_fp8(q, algo=algo)
+            fails += 1
+            print(f"rank {rank}: no bad-scale error algo={algo}", flush=True)
+        except A.InvalidArgument as e:
+            if str(e) != f"quantized tensor: bad scale at block {want_blk}":
+                fails += 1
+                print(f"rank {rank}: wrong bad-scale error algo={algo}: {e}", flush=True)
+    # the barrier timeout: the last rank never calls; every other rank's call
+    # times out, and the failure is sticky on ALL ranks (later calls fail fast)
+    if world > 1:
+        comm2 = Communicator(device=local, p2p_capacity=4096, timeout_s=3.0)
+        pc, ps = comm2.p2p_buffers(4096)
+        q = A.QuantizedTensor(pc, ps, 8, 128, (4096,), A.CodecKind.Fp8E4M3, packed=False)
+        q.codes.zero_()
+        q.scales.zero_()
+        if rank != world - 1:
+            try:
+                comm2.allreduce_fp8(q, algo="p2p")
+                fails += 1
+                print(f"rank {rank}: no timeout raised", flush=True)
+            except A.ProtocolError as e:
+                if "did not arrive" not in str(e):
+                    fails += 1
+                    print(f"rank {rank}: wrong timeout error {e}", flush=True)
+        dist.barrier()
+        import time
+        t0 = time.time()
+        try:
+            comm2.allreduce_fp8(q, algo="p2p")
+            fails += 1
+            print(f"rank {rank}: failed communicator did not raise", flush=True)
+        except A.ProtocolError:
+            if time.time() - t0 > 2.5:
+                fails += 1
+                print(f"rank {rank}: failed communicator waited {time.time() - t0:.1f} s", flush=True)
+        comm2.close()
     t = torch.tensor([fails], device=dev)
     dist.all_reduce(t)
     if rank == 0:

@@ -166,3 +166,26 @@ def test_no_device_means_error_not_fallback():
     s = np.zeros(1, np.float32)
     st = L.lib.agq_quantize_host(x.ctypes.data, 16, 4, 128, 0, c.ctypes.data, s.ctypes.data)
     assert st == L.AGQ_ERR_CUDA
+
+
+def test_fill_input_is_the_reference_rng():
+    """agq_fill_input (host) = make_rng(seed, stream, index) +
+    std::normal_distribution<float> of the reference (rng.hpp:9-28,
+    agq.cpp:47-65), byte for byte; BF16 output = its RNE."""
+    import torch
+    from paper_2605_00539_b200.inputs import materialize, materialize_parallel
+    if O.ref is None:
+        pytest.skip("oracle/_ref not built")
+    for seed, idx, n, std in [(0, 0, 4096, 1.0), (1, 0, 100003, 1.0), (7, 3, 5000, 1e-3),
+                              (2**63 + 5, 1, 257, 4.0)]:
+        a = materialize(n, seed, b=std, index=idx).numpy()
+        assert np.array_equal(a.view(np.uint32), O.ref_normal(seed, 0x1D, idx, n, std).view(np.uint32))
+        h = materialize(n, seed, b=std, index=idx, dtype=torch.bfloat16).float().numpy()
+        assert np.array_equal(h.view(np.uint32), O.bf16_round(O.ref_normal(seed, 0x1D, idx, n, std))
+                              .view(np.uint32))
+    outs = materialize_parallel([1000, 3000], 4, torch.float32, scales=[1.0, 0.5])
+    assert np.array_equal(outs[1].numpy(), O.ref_normal(4, 0x1D, 1, 3000, 0.5))
+    c = materialize(10, 0, "const", 2.5).numpy()
+    assert (c == 2.5).all()
+    with pytest.raises(A.InvalidArgument, match="a <= b"):
+        materialize(10, 0, "uniform", 1.0, 0.0)

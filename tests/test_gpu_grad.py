@@ -350,3 +350,41 @@ def test_reduce_unaligned_scale_pointers(cuda, world):
         L.errors_message(err.read(), L.AGQ_OP_ALLREDUCE)
         assert np.array_equal(out_c.cpu().numpy(), oc)
         assert np.array_equal(u32(out_s.cpu().numpy()), u32(os_))
+
+
+def test_accumulate_validates_main_first(cuda):
+    """local_accumulate dequantizes main first, so validate(main) runs before
+    anything touches the data (collective.hpp:135 -> quantize.hpp:157-176)."""
+    mc, ms = O.quantize(np.ones(300, np.float32), 8, 128, O.FP8)
+    g = t(np.zeros(300, np.float32), cuda)
+    bad = fp8q(mc, ms[:2], cuda)  # 3 blocks, 2 scales
+    with pytest.raises(A.InvalidArgument, match="wrong number of scales"):
+        A.local_accumulate(bad, g)
+    q = fp8q(mc, ms, cuda)
+    q.bit_width = 7
+    with pytest.raises(A.InvalidArgument, match="fp8_e4m3 requires bit_width 8"):
+        A.local_accumulate(q, g)
+    q = fp8q(mc, ms, cuda)
+    q.scales[1] = -2.0
+    with pytest.raises(A.InvalidArgument, match="bad scale at block 1$"):
+        A.local_accumulate(q, g)
+
+
+@pytest.mark.parametrize("world", [3, 8, 12])
+def test_allreduce_bad_scale_reports_lowest_worker(cuda, world):
+    """check_workers validates the workers in order (collective.hpp:158-168):
+    the error names the lowest bad block of the LOWEST worker with one, not
+    the lowest bad block over all workers."""
+    rng = np.random.default_rng(world)
+    n = 8192 * 2 + 300
+    mains = []
+    for r in range(world):
+        c, s = O.quantize(rng.standard_normal(n).astype(np.float32), 8, 128, O.FP8)
+        if r == 1:
+            s[100] = -1.0
+            s[40] = np.nan
+        if r == world - 1:
+            s[3] = -0.5
+        mains.append(fp8q(c, s, cuda))
+    with pytest.raises(A.InvalidArgument, match="bad scale at block 40$"):
+        A.allreduce_simulated(mains)

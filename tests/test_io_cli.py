@@ -64,3 +64,55 @@ def test_cli_quantize_and_allreduce(cuda, tmp_path):
             "--protocol", "decomposed", "--trace", str(tmp_path / "tr.jsonl"))
     assert j["overflow_total"] == 0 and j["max_abs_dev_vs_oracle"] == 0.0
     assert j["message_count"] == len(open(tmp_path / "tr.jsonl").readlines())
+
+
+def _seq(v):
+    return float(np.add.accumulate(np.asarray(v, np.float64))[-1])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bits,codec", [(4, 0), (6, 0), (4, 1), (8, 2)])
+def test_cli_quantize_stats_equal_reference(cuda, bits, codec):
+    """`quantize --normal 4096 --bits b` JSON equals the reference CLI's
+    (agq.cpp:114-152) bit for bit: the reference RNG's inputs, its quantizer
+    (oracle/_ref) and its left-to-right double sums."""
+    if O.ref is None:
+        pytest.skip("oracle/_ref not built")
+    name = {0: "linear", 1: "fp4", 2: "fp8"}[codec]
+    out = subprocess.run([sys.executable, "-m", "paper_2605_00539_b200.cli", "--seed", "3",
+                          "quantize", "--normal", "4096", "--bits", str(bits), "--codec", name],
+                         cwd=ROOT, capture_output=True, text=True, check=True).stdout
+    j = json.loads(out)
+    x = O.ref_normal(3, 0x1D, 0, 4096)
+    c, s = O.quantize(x, bits, 128, codec, lib=O.ref)
+    back = O.dequantize(c, s, bits, 128, codec, lib=O.ref).astype(np.float64)
+    err = np.abs(back - x.astype(np.float64))
+    nz = x != 0
+    want = {"elements": 4096, "bit_width": bits, "block_size": 128,
+            "codec": {0: "symmetric_linear", 1: "fp4_e2m1", 2: "fp8_e4m3"}[codec],
+            "mae": _seq(err) / 4096, "max_abs_error": float(err.max()),
+            "max_rel_error": float((err[nz] / np.abs(x[nz].astype(np.float64))).max()),
+            "compression_ratio": 4.0 * 4096 / (np.ceil(4096 * bits / 8.0) + 4.0 * s.size)}
+    assert j == want
+    assert list(j) == sorted(j)  # nlohmann::json key order
+
+
+@pytest.mark.gpu
+def test_cli_allreduce_stats_equal_reference(cuda):
+    """`allreduce-sim --workers 4 --normal 1000` (agq.cpp:274-324): worker r
+    from seed + r, the reference's all-reduce, oracle deviation and L2 in its
+    summation order, its message trace totals."""
+    if O.ref is None:
+        pytest.skip("oracle/_ref not built")
+    out = subprocess.run([sys.executable, "-m", "paper_2605_00539_b200.cli", "--seed", "5",
+                          "allreduce-sim", "--workers", "4", "--normal", "1000"],
+                         cwd=ROOT, capture_output=True, text=True, check=True).stdout
+    j = json.loads(out)
+    mains = [O.quantize(O.ref_normal(5 + r, 0x1D, 0, 1000), 8, 128, 2, lib=O.ref) for r in range(4)]
+    oc, os_, ov, ev, _ = O.ref_allreduce(0, [m[0] for m in mains], [m[1] for m in mains])
+    vals = O.dequantize(oc, os_, 8, 128, 2, lib=O.ref).astype(np.float64)
+    orc = O.allreduce_oracle([m[0] for m in mains], [m[1] for m in mains]).astype(np.float64)
+    assert j["result_l2"] == float(np.sqrt(_seq(vals * vals)))
+    assert j["max_abs_dev_vs_oracle"] == float(np.abs(vals - orc).max())
+    assert j["overflow_total"] == ov == 0
+    assert j["message_count"] == len(ev) and j["payload_bytes"] == int(ev[:, 5].sum())

@@ -1,6 +1,7 @@
-"""Multi-GPU decomposed all-reduce parity (needs >= 2 GPUs on one box):
-launches tests/mp_allreduce_check.py under torchrun with every visible GPU,
-once per fused-kernel shape (16 elements per thread, the default, and 8)."""
+"""Real-rank decomposed all-reduce parity: launches tests/mp_allreduce_check.py
+under torchrun with one process per visible GPU — also on a 1-GPU box, where
+P = 1 still runs NCCL communicator init, the IPC export/open of the symmetric
+buffer, the epoch flags and the fused kernel k_fused_allreduce<1>."""
 import os
 import subprocess
 import sys
@@ -12,16 +13,13 @@ pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-@pytest.mark.parametrize("ept", ["16", "8"])
-def test_allreduce_multigpu_bitexact(ept):
-    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
-        pytest.skip("needs >= 2 GPUs")
+def test_allreduce_real_ranks_bitexact():
     n = torch.cuda.device_count()
+    assert n >= 1, "needs a GPU"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", f"--master-port={29533 + int(ept)}",
+           "--master-addr=127.0.0.1", "--master-port=29541",
            os.path.join(HERE, "mp_allreduce_check.py")]
-    env = dict(os.environ, AGQ_P2P_EPT=ept)
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
-    print(r.stdout[-4000:], r.stderr[-4000:])
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    print(r.stdout[-6000:], r.stderr[-6000:])
     assert r.returncode == 0
     assert "failures=0" in r.stdout

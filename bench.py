@@ -368,6 +368,121 @@ def bench_e2e(wl, args, world, steps, chunks=16, nstreams=4):
     return wl.bytes_per_step() * steps * world / sec / 1e9, bi, bo
 
 
+def bench_c2_stage(wl, args, layers=4, widths=(4, 8)):
+    """A whole pipeline stage in ONE grouped call: LLaMA-8B at 8 stages holds
+    4 layers per stage, each storing the five C2 tensors (layers.hpp:266-301)
+    under the stage policy (dbca.hpp:172-177) -> 20 tensors (2.68e9
+    elements) per quantize call and per dequantize call (validate on)."""
+    import torch
+    L = wl.L
+    xs = [x.clone() for _ in range(layers) for x in wl.x]
+    outs = [torch.empty_like(x) for x in xs]
+    sp = torch.cuda.current_stream().cuda_stream
+    res = {"config": f"C2 stage: {layers} layers x 5 stored tensors = {5 * layers} tensors per "
+                     f"grouped call", "elements": sum(x.numel() for x in xs)}
+    for b in widths:
+        qs = [(torch.empty(int(L.lib.agq_packed_bytes(x.numel(), b)), dtype=torch.uint8,
+                           device=x.device),
+               torch.empty((x.numel() + 127) // 128, dtype=torch.float32, device=x.device))
+              for x in xs]
+        sq = (L.AgqSegment * len(xs))()
+        sd = (L.AgqSegment * len(xs))()
+        for i, (x, o, (c, sc)) in enumerate(zip(xs, outs, qs)):
+            sq[i] = L.AgqSegment(x.data_ptr(), c.data_ptr(), sc.data_ptr(), x.numel())
+            sd[i] = L.AgqSegment(o.data_ptr(), c.data_ptr(), sc.data_ptr(), x.numel())
+
+        def run():
+            L.check(L.lib.agq_quantize_grouped(sq, len(xs), L.AGQ_BF16, b, 0, wl.err.ptr, sp))
+            L.check(L.lib.agq_dequantize_grouped(sd, len(xs), L.AGQ_BF16, b, 0, 1, wl.err.ptr, sp))
+        run()
+        torch.cuda.synchronize()
+        n0 = wl.A.launch_count()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        iters = 5
+        s.record()
+        for _ in range(iters):
+            run()
+        e.record()
+        torch.cuda.synchronize()
+        sec = s.elapsed_time(e) * 1e-3 / iters
+        h = wl.err.read()
+        L.errors_message(h, L.AGQ_OP_QUANTIZE)
+        L.errors_message(h, L.AGQ_OP_DEQUANTIZE)
+        nbytes = res["elements"] * sum(act_bytes_per_elem(b))
+        res[f"b{b}"] = {"ms": round(sec * 1e3, 3), "GBs": round(nbytes / sec / 1e9, 1),
+                        "launches_per_call_pair": (wl.A.launch_count() - n0) // iters}
+        del qs
+    res["GBs"] = min(res[f"b{b}"]["GBs"] for b in widths)
+    del xs, outs
+    torch.cuda.empty_cache()
+    return res
+
+
+def pcie_rates(dev, mb=256, reps=3):
+    """Pinned-host <-> device copy rates (GB/s) of this box, one direction at
+    a time: the bound the host-buffer API runs against."""
+    import torch
+    n = mb << 20
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    out = {}
+    for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)),
+                     ("d2h", lambda: h.copy_(d, non_blocking=True))):
+        best = 1e9
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            fn()
+            e.record()
+            torch.cuda.synchronize()
+            best = min(best, s.elapsed_time(e) * 1e-3)
+        out[name] = n / best / 1e9
+    del h, d
+    return out
+
+
+def bench_dropin(dev):
+    """e2e through the C++ drop-in API (tools/dropin_bench.cpp): host
+    std::vector in/out, as a reference-side C++ caller, beside the reference's
+    own single-threaded calls; against this box's pinned PCIe rates."""
+    exe = os.path.join(ROOT, "paper_2605_00539_b200", "build", "dropin_bench")
+    ref = os.path.join(ROOT, "oracle", "_ref", "libagq_ref.so")
+    if not os.path.exists(exe):
+        return {"error": "dropin_bench not built"}
+    pc = pcie_rates(dev)
+    r = subprocess.run([exe, ref], capture_output=True, text=True, timeout=600)
+    try:
+        j = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception:
+        return {"error": (r.stdout + r.stderr)[-300:]}
+    # lower bound of each call on this box: its larger direction at the
+    # pinned rate (the pipeline overlaps the two directions)
+    bq = max(j["quantize_h2d_bytes"] / pc["h2d"], j["quantize_d2h_bytes"] / pc["d2h"]) / 1e9
+    bd = max(j["dequantize_h2d_bytes"] / pc["h2d"], j["dequantize_d2h_bytes"] / pc["d2h"]) / 1e9
+    ba = max(j["accumulate_h2d_bytes"] / pc["h2d"], j["accumulate_d2h_bytes"] / pc["d2h"]) / 1e9
+    rt = j["roundtrip_ms"] * 1e-3
+    moved = (j["quantize_h2d_bytes"] + j["quantize_d2h_bytes"] + j["dequantize_h2d_bytes"] +
+             j["dequantize_d2h_bytes"])
+    n = j["elements"]
+    res = {"config": j["config"], "pinned_pcie_GBs": {k: round(v, 1) for k, v in pc.items()},
+           "roundtrip_ms": j["roundtrip_ms"], "quantize_ms": j["quantize_ms"],
+           "dequantize_ms": j["dequantize_ms"],
+           "api_bytes_per_roundtrip": int(moved),
+           "GBs_api_bytes": round(moved / rt / 1e9, 1),
+           "frac_of_pinned_pcie_bound": round((bq + bd) / rt, 3),
+           # the metric's algorithmic bytes for FP32 in/out, b = 4
+           "GBs_algorithmic": round(2 * n * (4 + 0.5 + 4 / 128) / rt / 1e9, 2),
+           "accumulate_ms": j["accumulate_ms"],
+           "accumulate_frac_of_pinned_pcie_bound": round(ba / (j["accumulate_ms"] * 1e-3), 3),
+           "reference_1thread": {"roundtrip_ms": round(j["ref_quantize_ms"] + j["ref_dequantize_ms"], 2),
+                                 "accumulate_ms": j["ref_accumulate_ms"]},
+           "speedup_vs_reference_1thread": round((j["ref_quantize_ms"] + j["ref_dequantize_ms"]) /
+                                                 j["roundtrip_ms"], 1),
+           "bitexact_vs_reference": j["bitexact_vs_ref"] and j["accumulate_bitexact_vs_ref"]}
+    return res
+
+
 def bench_c1(dev, args):
     """C1: INT4 block-128 quantize/dequantize round trip of a 4096x4096 BF16
     activation (the reference's CPU-runnable config). 16 rotating copies
@@ -444,7 +559,10 @@ def bench_reduce_local(dev, args, P=8):
 
 
 def bench_accumulate(dev, args, n_params):
-    """C3: FP8 local_accumulate over an 8B-param gradient, FP32 local grads."""
+    """C3: FP8 local_accumulate over an 8B-param gradient, in place. Headline:
+    FP32 local gradient, FP32 sum (6.0625 B/param). Variants on the same
+    buffers: BF16 / FP16-rounded sums (collective.hpp:141-142) and a BF16
+    local gradient (4.0625 B/param)."""
     import torch
     import paper_2605_00539_b200 as A
     from paper_2605_00539_b200 import _lib as L
@@ -461,35 +579,77 @@ def bench_accumulate(dev, args, n_params):
                                    torch.cuda.current_stream().cuda_stream))
         local[off:off + m].normal_(0.0, 1e-3, generator=g)
         del x
+    local16 = local.to(torch.bfloat16)
     err = A.ErrorRecord(dev).reset()
     sp = torch.cuda.current_stream().cuda_stream
 
-    def run():
-        L.check(L.lib.agq_fp8_accumulate(codes.data_ptr(), scales.data_ptr(), local.data_ptr(),
-                                         L.AGQ_F32, n_params, 128, 0, codes.data_ptr(),
-                                         scales.data_ptr(), err.ptr, sp))
-    for _ in range(2):
-        run()
-    torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    iters = max(3, min(args.steps, 10))
-    s.record()
-    for _ in range(iters):
-        run()
-    e.record()
-    torch.cuda.synchronize()
-    sec = s.elapsed_time(e) * 1e-3 / iters
-    L.errors_message(err.read(), L.AGQ_OP_ACCUMULATE)
-    nbytes = n_params * (1 + 4 / 128) * 2 + n_params * 4
-    del codes, scales, local
+    def timed(loc, ldt, prec):
+        def run():
+            L.check(L.lib.agq_fp8_accumulate(codes.data_ptr(), scales.data_ptr(), loc.data_ptr(),
+                                             ldt, n_params, 128, prec, codes.data_ptr(),
+                                             scales.data_ptr(), err.ptr, sp))
+        for _ in range(2):
+            run()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        iters = max(3, min(args.steps, 10))
+        s.record()
+        for _ in range(iters):
+            run()
+        e.record()
+        torch.cuda.synchronize()
+        L.errors_message(err.read(), L.AGQ_OP_ACCUMULATE)
+        sec = s.elapsed_time(e) * 1e-3 / iters
+        bpp = 2 * (1 + 4 / 128) + loc.element_size()
+        return {"ms": round(sec * 1e3, 3), "GBs": round(n_params * bpp / sec / 1e9, 1),
+                "bytes_per_param": bpp}
+
+    res = {"config": "C3 FP8 local_accumulate, LLaMA-8B params, fp32 local, in place",
+           "params": n_params, **timed(local, L.AGQ_F32, 0)}
+    res["variants"] = {"fp32_local_bf16_sum": timed(local, L.AGQ_F32, 1),
+                       "fp32_local_fp16_sum": timed(local, L.AGQ_F32, 2),
+                       "bf16_local": timed(local16, L.AGQ_BF16, 0),
+                       "bf16_local_bf16_sum": timed(local16, L.AGQ_BF16, 1)}
+    del codes, scales, local, local16
     torch.cuda.empty_cache()
-    return {"config": "C3 FP8 local_accumulate, LLaMA-8B params, fp32 local, in place",
-            "params": n_params, "ms": round(sec * 1e3, 3), "GBs": round(nbytes / sec / 1e9, 1),
-            "bytes_per_param": 6.0625}
+    return res
+
+
+def allreduce_oracle_sample(src_codes, src_scales, result, world, rank, nsample=64, seed=5):
+    """Check `nsample` random whole blocks of the real-rank all-reduce result
+    against the CPU oracle's allreduce_decomposed (collective.hpp:226-333)
+    over every rank's input blocks (gathered to every rank). Blocks are
+    reduced independently, so the sampled blocks form a valid all-reduce of
+    their own."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_ffi as O
+    nfull = src_codes.numel() // 128
+    blks = torch.from_numpy(np.sort(np.random.default_rng(seed).choice(nfull, nsample, False)))
+    blks = blks.to(src_codes.device)
+    idx = (blks[:, None] * 128 + torch.arange(128, device=blks.device)[None, :]).reshape(-1)
+    mine_c, mine_s = src_codes[idx].contiguous(), src_scales[blks].contiguous()
+    all_c = [torch.empty_like(mine_c) for _ in range(world)]
+    all_s = [torch.empty_like(mine_s) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(all_c, mine_c)
+        dist.all_gather(all_s, mine_s)
+    else:
+        all_c, all_s = [mine_c], [mine_s]
+    want_c, want_s = O.allreduce_decomposed([c.cpu().numpy() for c in all_c],
+                                            [x.cpu().numpy() for x in all_s])
+    got_c = result.codes[idx].cpu().numpy()
+    got_s = result.scales[blks].cpu().numpy()
+    return bool(np.array_equal(got_c, want_c) and
+                np.array_equal(got_s.view(np.uint32), want_s.view(np.uint32)))
 
 
 def bench_allreduce(dev, args, world, rank, n):
-    """C4: decomposed 8-bit all-reduce vs BF16 ncclAllReduce, same gradient."""
+    """C4: decomposed 8-bit all-reduce vs BF16 ncclAllReduce, same gradient;
+    64 sampled blocks of every algorithm's result checked against the CPU
+    oracle over all ranks' inputs."""
     import torch
     import paper_2605_00539_b200 as A
     from paper_2605_00539_b200 import _lib as L
@@ -559,7 +719,9 @@ def bench_allreduce(dev, args, world, rank, n):
             continue
         res[algo] = {"ms": round(sec * 1e3, 3), "bus_GBs_wire": round(fac * wire / sec / 1e9, 1),
                      "bus_GBs_bf16_equiv": round(fac * 2 * n / sec / 1e9, 1),
-                     "frac_of_nvlink_900": round(fac * wire / sec / 1e9 / NVLINK_GBS, 4)}
+                     "frac_of_nvlink_900": round(fac * wire / sec / 1e9 / NVLINK_GBS, 4),
+                     "oracle_64_blocks_bitexact": allreduce_oracle_sample(src_codes, src_scales, qq,
+                                                                          world, rank)}
         if algo in ("p2p", "push") and "ms" in res.get("nccl", {}):
             ok = torch.equal(qq.codes, q.codes) and torch.equal(qq.scales, q.scales)
             res[algo + "_equals_nccl"] = bool(ok)
@@ -856,9 +1018,12 @@ def main():
                                      nstreams=args.e2e_streams)
         extra["e2e"] = {"value": round(e2e_val, 1), "unit": "GB/s", "h2d_bytes_per_step": bi,
                         "d2h_bytes_per_step": bo}
+    extra["c2_stage"] = bench_c2_stage(wl, args)
     del wl
     torch.cuda.empty_cache()
     extra["c1"] = bench_c1(dev, args)
+    if not args.no_e2e:
+        extra["e2e_dropin"] = bench_dropin(dev)
     if not args.no_accumulate:
         extra["accumulate"] = bench_accumulate(dev, args, args.acc_elements)
     if world == 1 and not args.no_allreduce:
@@ -866,9 +1031,11 @@ def main():
     if world > 1 and not args.no_allreduce:
         extra["allreduce"] = bench_allreduce(dev, args, world, rank, args.ar_elements)
     clk = clocks.stop()
-    for k in ("c1", "accumulate", "reduce_local"):  # per-kernel share of the HBM peak
+    for k in ("c1", "accumulate", "reduce_local", "c2_stage"):  # share of the HBM peak
         if k in extra and "GBs" in extra[k]:
             extra[k]["frac_of_peak"] = round(extra[k]["GBs"] / peak, 4)
+    for v in extra.get("accumulate", {}).get("variants", {}).values():
+        v["frac_of_peak"] = round(v["GBs"] / peak, 4)
 
     dom_name, dom_gbs, other = ("k_quant_warp", q_gbs, {"k_dequant_warp_GBs": round(d_gbs, 1)}) \
         if q_time >= d_time else ("k_dequant_warp", d_gbs, {"k_quant_warp_GBs": round(q_gbs, 1)})
@@ -881,7 +1048,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(sec / args.steps * 1e3, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16 in/out, u4-u8 packed codes, f32 scales",
-            "data": "synthetic N(0,1) activations (torch.Generator seed 0), per-tensor scales",
+            "data": "synthetic: the reference RNG's N(0, s_i) draws (make_rng(0, 0x1D, i), "
+                    "BF16-rounded; s = 1, 1, 0.5, 4, 1), same bytes as the reference arm",
             "config": {"workload": "C2: LLaMA-8B block stored activations (seq 4096 x mb 4), "
                                    "8-stage DBCA policies, quant+dequant",
                        "elements_per_stage": sum(T_TOKENS * w for _, w in TENSORS),

@@ -123,7 +123,7 @@ typedef struct {
 /* Grouped launch over the tensors one pipeline stage stores (dbca.hpp:172-177
  * stage_policy -> layers.hpp:64-75 agoq_default(bits), layers.hpp:266-301
  * the stored set of every layer of the stage). All segments share
- * bits/codec/dtype; block is 128. Any segment count: up to 32 segments go
+ * bits/codec/dtype; block is 128. Any segment count: up to 8 segments go
  * into one launch, larger groups are split. Error indices in d_err are
  * group-global (blocks / elements counted over the segments in order).
  * validate != 0 performs the reference's dequantize-time checks

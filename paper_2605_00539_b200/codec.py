@@ -241,7 +241,7 @@ def quantize_grouped(xs: Sequence[torch.Tensor], bit_width: int,
                      kind: CodecKind = CodecKind.SymmetricLinear, stream=None,
                      check: bool = True, errors: ErrorRecord | None = None,
                      outs: Sequence[QuantizedTensor] | None = None) -> list[QuantizedTensor]:
-    """One launch (per 32 tensors) over all tensors a pipeline stage stores
+    """One launch per 8 tensors over all tensors a pipeline stage stores
     (layers.hpp:266-301 for every layer of the stage, dbca.hpp:172-177 width;
     block 128, packed)."""
     if not xs:
@@ -279,7 +279,7 @@ def dequantize_grouped(qs: Sequence[QuantizedTensor], out_dtype: torch.dtype = t
                        check: bool = True, errors: ErrorRecord | None = None,
                        validate: bool = True) -> list[torch.Tensor]:
     """dequantize_blockwise (quantize.hpp:178-189, validate :157-176 first)
-    over a group of packed block-128 tensors in one launch per 32 tensors.
+    over a group of packed block-128 tensors in one launch per 8 tensors.
     With validate the device checks code range and scales of every tensor;
     `check` reads the record and raises the reference's exception."""
     if not qs:

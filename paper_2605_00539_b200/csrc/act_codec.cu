@@ -1093,6 +1093,22 @@ agq_status dequantize_device(const void* codes, int layout, const float* scales,
                         err, s);
 }
 
+// Chunked host entry points: blk_base = block index of element 0 in the
+// error record.
+agq_status quantize_device_at(const void* x, int x_dtype, uint64_t n, int bits, uint32_t block,
+                              int codec, void* codes, int layout, float* scales,
+                              long long blk_base, agq_errors* err, cudaStream_t s) {
+  return quantize_one(x, x_dtype, n, bits, block, codec, codes, layout, scales, blk_base, err, s);
+}
+
+agq_status dequantize_device_at(const void* codes, int layout, const float* scales, uint64_t n,
+                                int bits, uint32_t block, int codec, void* out, int out_dtype,
+                                int validate, long long blk_base, agq_errors* err,
+                                cudaStream_t s) {
+  return dequantize_one(codes, layout, scales, n, bits, block, codec, out, out_dtype, validate,
+                        blk_base, err, s);
+}
+
 agq_status quantize_grouped_device(const agq_segment* segs, int nseg, int x_dtype, int bits,
                                    int codec, agq_errors* err, cudaStream_t s) {
   return grouped<true>(segs, nseg, x_dtype, bits, codec, 0, err, s);

@@ -15,11 +15,17 @@ constexpr int kBlock = 128;          // block size of every fast path
 constexpr int kTileBlocks = 64;      // blocks per tile
 constexpr int kTileElems = kTileBlocks * kBlock;  // 8192 elements
 constexpr int kThreads = 256;        // 32 consecutive elements per thread
-constexpr int kMaxSeg = 32;  // segments per grouped launch (larger groups split)
+// Segments per grouped launch; larger groups are split into launches of 8
+// (a 32-entry table measured 3-4% slower kernels: C1 round trip 19.9 vs 18.7
+// us, profiles/r02_ab_segtable.log).
+#ifndef AGQ_MAX_SEG
+#define AGQ_MAX_SEG 8
+#endif
+constexpr int kMaxSeg = AGQ_MAX_SEG;
 constexpr long long kNone = 0x7fffffffffffffffLL;
 
 // A list of equally-coded tensors processed by one launch (grouped launch of
-// the tensors one pipeline stage stores; ~1.3 KB of kernel parameters).
+// the tensors one pipeline stage stores).
 // tile_begin is a prefix sum over whole warp tiles; block_base the
 // group-global index of each segment's first block (error reporting).
 struct SegTable {

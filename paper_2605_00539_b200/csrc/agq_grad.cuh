@@ -96,6 +96,50 @@ __device__ __forceinline__ void dq_tab_accum(const uint32_t (&w)[NW], uint32_t t
     }
   }
 }
+// ---- f16-route block-table decode (every code, no per-code safety test) ----
+// The hardware cvt.rn.f16x2.e4m3x2 gives every E4M3 value v exactly; as an
+// FP32 value v = sign * (1 + M/8) * 2^X with a 3-bit M for EVERY code
+// (normal, subnormal: m * 2^-9 renormalised, zero: 0). The reference's
+// (float)(fl64(v / 448) * (double)s) = fl32(fl64((8+M)/7) * s) * 2^(X-9)
+// (powers of two commute with both roundings while the results stay normal,
+// i.e. s in [2^-60, 2^60], dq_fast), so with the block table
+// T[M] = fl32(fl64((8+M)/7) * s) * 2^-9 the decode is T[M] * (v & sign|exp),
+// an exact product, added with one FFMA. Zero codes give +-0 exactly, NaN
+// codes an infinite product (the sum is then non-finite: the reference's
+// abort). Table address from the f16 mantissa bits.
+__device__ __forceinline__ float fp8_tab_entry_f16(double t8, float s) {
+  return fmul(fp8_tab_entry(t8, s), 0x1p-9f);  // exact: the entry is a normal float
+}
+// acc[4i + b] = fadd(acc[4i + b], dq(code b of w[i])) through this lane's
+// block table `tab` (8 floats in shared memory).
+template <int NW>
+__device__ __forceinline__ void dq_f16_accum(const uint32_t (&w)[NW], const float* tab,
+                                             float (&acc)[4 * NW]) {
+  const char* tb = reinterpret_cast<const char*>(tab);
+#pragma unroll
+  for (int i = 0; i < NW; ++i) {
+    uint32_t h[2];
+    asm("{\n.reg .b16 lo, hi;\nmov.b32 {lo, hi}, %2;\ncvt.rn.f16x2.e4m3x2 %0, lo;\n"
+        "cvt.rn.f16x2.e4m3x2 %1, hi;\n}"
+        : "=r"(h[0]), "=r"(h[1])
+        : "r"(w[i]));
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      float f0, f1;
+      asm("{\n.reg .b16 a, b;\nmov.b32 {a, b}, %2;\ncvt.f32.f16 %0, a;\ncvt.f32.f16 %1, b;\n}"
+          : "=f"(f0), "=f"(f1)
+          : "r"(h[k]));
+      const float p0 = u2f(f2u(f0) & 0xff800000u), p1 = u2f(f2u(f1) & 0xff800000u);
+      const uint32_t t = h[k] >> 5;  // f16 mantissa bits 7-9 -> byte offset M * 4
+      const float e0 = *reinterpret_cast<const float*>(tb + (t & 0x1cu));
+      const float e1 = *reinterpret_cast<const float*>(tb + ((t >> 16) & 0x1cu));
+      const f32x2 a = fma2(pk2(e0, e1), pk2(p0, p1),
+                           pk2(acc[4 * i + 2 * k], acc[4 * i + 2 * k + 1]));
+      up2(a, acc[4 * i + 2 * k], acc[4 * i + 2 * k + 1]);
+    }
+  }
+}
+
 __device__ __forceinline__ float fp8_tab_entry_half(double t8, float s) {
   return fmul(fp8_tab_entry(t8, s), 0.5f);  // exact: the entry is a normal float
 }

@@ -3,11 +3,15 @@
 // entry points for the C++ drop-in API, the DBCA bit-width planner.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <climits>
+#include <condition_variable>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <random>
 #include <string>
@@ -33,7 +37,7 @@ agq_status unpack_device(const uint8_t* packed, uint64_t n, int bits, uint8_t* c
                          cudaStream_t s);
 agq_status accumulate_device(const uint8_t* codes, const float* scales, const void* local,
                              int local_dtype, uint64_t n, uint32_t block, int prec, uint8_t* oc,
-                             float* os, agq_errors* err, cudaStream_t s);
+                             float* os, agq_errors* err, cudaStream_t s, long long blk_base = 0);
 agq_status reduce_requant_device(int np, const uint8_t* const* pc, const float* const* ps,
                                  uint64_t len, uint32_t block, int nout, uint8_t* const* oc,
                                  float* const* os, long long blk_base, agq_errors* err,
@@ -162,6 +166,10 @@ agq_status ws_reserve(Workspace& w, size_t bytes) {
 
 size_t al(size_t x) { return (x + 255) / 256 * 256; }
 
+agq_errors none_errors();
+}  // namespace
+const agq_errors kNoErrors = none_errors();
+namespace {
 agq_errors none_errors() {
   agq_errors e;
   e.nonfinite_block = LLONG_MAX;
@@ -419,30 +427,270 @@ agq_status agq_allreduce_bf16_nccl(agq_comm* comm, void* data, uint64_t n, agq_s
 }
 
 // ---- host entry points --------------------------------------------------------
+// The C++ drop-in surface (quantize.hpp:78-189, collective.hpp:128-147 over
+// host std::vectors). Each call streams its tensor through a library-owned
+// pipeline in block-aligned chunks: parallel host copies between the
+// caller's (pageable) buffers and pinned bounce slots, H2D -> kernel -> D2H
+// on one stream per slot, so the copy-in of chunk k+1, the kernels of chunk
+// k and the copy-out of chunk k-1 overlap; one device error record per call
+// (chunk errors carry their global block index) and one synchronisation at
+// the end. Concurrent callers get separate pipelines.
+}  // extern "C"
+
+namespace agqh {
+agq_status quantize_device_at(const void* x, int x_dtype, uint64_t n, int bits, uint32_t block,
+                              int codec, void* codes, int layout, float* scales,
+                              long long blk_base, agq_errors* err, cudaStream_t s);
+agq_status dequantize_device_at(const void* codes, int layout, const float* scales, uint64_t n,
+                                int bits, uint32_t block, int codec, void* out, int out_dtype,
+                                int validate, long long blk_base, agq_errors* err,
+                                cudaStream_t s);
+namespace {
+
+// Persistent host copy threads: copy() splits a batch of memcpy jobs into
+// ~1 MB pieces, shares them with the workers (the caller works too) and
+// returns when every piece is done. Each batch owns its counters, so a worker
+// that wakes late can never touch another batch's pieces.
+class CopyPool {
+ public:
+  struct Job {
+    void* dst;
+    const void* src;
+    size_t bytes;
+  };
+  static CopyPool& get() {
+    static CopyPool* p = new CopyPool();  // never destroyed (threads detached)
+    return *p;
+  }
+  void copy(const std::vector<Job>& jobs) {
+    size_t total = 0;
+    for (const Job& j : jobs) total += j.bytes;
+    if (total == 0) return;
+    auto b = std::make_shared<Batch>();
+    const size_t piece = std::max<size_t>(1 << 20, total / (4 * (nthreads_ + 1)) + 1);
+    for (const Job& j : jobs)
+      for (size_t o = 0; o < j.bytes; o += piece)
+        b->pieces.push_back({static_cast<char*>(j.dst) + o, static_cast<const char*>(j.src) + o,
+                             std::min(piece, j.bytes - o)});
+    if (b->pieces.size() > 1 && nthreads_ > 0) {
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        cur_ = b;
+        ++gen_;
+      }
+      cv_.notify_all();
+    }
+    run(*b);
+    while (b->done.load(std::memory_order_acquire) < b->pieces.size()) std::this_thread::yield();
+    std::lock_guard<std::mutex> lk(mu_);
+    if (cur_ == b) cur_.reset();
+  }
+
+ private:
+  struct Batch {
+    std::vector<Job> pieces;
+    std::atomic<size_t> next{0};
+    std::atomic<size_t> done{0};
+  };
+  CopyPool() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    nthreads_ = (int)std::min<unsigned>(7, hw > 2 ? hw / 2 : 1);
+    for (int t = 0; t < nthreads_; ++t) std::thread([this] { loop(); }).detach();
+  }
+  static void run(Batch& b) {
+    for (;;) {
+      const size_t k = b.next.fetch_add(1, std::memory_order_relaxed);
+      if (k >= b.pieces.size()) break;
+      std::memcpy(b.pieces[k].dst, b.pieces[k].src, b.pieces[k].bytes);
+      b.done.fetch_add(1, std::memory_order_release);
+    }
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      std::shared_ptr<Batch> b;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        b = cur_;
+      }
+      if (b) run(*b);
+    }
+  }
+  int nthreads_ = 0;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::shared_ptr<Batch> cur_;
+  uint64_t gen_ = 0;
+};
+
+// One pipeline: kSlots slots of pinned + device staging, one stream each.
+constexpr int kSlots = 4;
+constexpr uint64_t kChunkElems = 2u << 20;  // 2M elements (8 MB of FP32) per chunk
+
+struct HostPipe {
+  int dev = -1;
+  bool busy = false;
+  cudaStream_t st[kSlots] = {};
+  cudaEvent_t ev[kSlots] = {};
+  char* pin[kSlots] = {};
+  char* dbuf[kSlots] = {};
+  size_t cap = 0;
+  agq_errors* d_err = nullptr;
+
+  agq_status reserve(size_t bytes) {
+    if (!st[0]) {
+      for (int k = 0; k < kSlots; ++k) {
+        cudaError_t e = cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming);
+        if (e != cudaSuccess) return cuda_fail(e, "host pipeline: streams");
+      }
+      cudaError_t e = cudaMalloc(&d_err, sizeof(agq_errors));
+      if (e != cudaSuccess) return cuda_fail(e, "host pipeline: error record");
+    }
+    if (cap >= bytes) return AGQ_OK;
+    for (int k = 0; k < kSlots; ++k) {
+      if (pin[k]) cudaFreeHost(pin[k]);
+      if (dbuf[k]) cudaFree(dbuf[k]);
+      pin[k] = dbuf[k] = nullptr;
+    }
+    cap = 0;
+    for (int k = 0; k < kSlots; ++k) {
+      cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&pin[k]), bytes, cudaHostAllocDefault);
+      if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&dbuf[k]), bytes);
+      if (e != cudaSuccess) return cuda_fail(e, "host pipeline: staging");
+    }
+    cap = bytes;
+    return AGQ_OK;
+  }
+};
+
+std::mutex g_pipes_mu;
+std::vector<HostPipe*> g_pipes;
+
+struct PipeLease {
+  HostPipe* p = nullptr;
+  PipeLease() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_pipes_mu);
+    for (HostPipe* q : g_pipes)
+      if (!q->busy && q->dev == dev) {
+        p = q;
+        break;
+      }
+    if (!p) {
+      p = new HostPipe();
+      p->dev = dev;
+      g_pipes.push_back(p);
+    }
+    p->busy = true;
+  }
+  ~PipeLease() {
+    std::lock_guard<std::mutex> lk(g_pipes_mu);
+    p->busy = false;
+  }
+};
+
+// One chunk's staging layout: `in` bytes copied host->device before the
+// kernel, `out` bytes device->host after it, both inside one slot.
+struct Part {
+  size_t off;  // inside the slot
+  size_t bytes;
+  char* host;  // caller buffer (in: source, out: destination)
+};
+
+// Run `nchunks` chunks through the pipeline. plan(k, in, out) fills the
+// chunk's in/out parts; launch(k, dev_slot, stream) enqueues its kernels.
+template <class Plan, class Launch>
+agq_status run_pipeline(HostPipe& p, uint64_t nchunks, size_t slot_bytes, Plan plan,
+                        Launch launch) {
+  if (agq_status st = p.reserve(slot_bytes)) return st;
+  if (agq_status st = cuda_fail(cudaMemcpy(p.d_err, &kNoErrors, sizeof(agq_errors),
+                                           cudaMemcpyHostToDevice),
+                                "host pipeline: reset"))
+    return st;
+  std::vector<std::vector<Part>> outs(kSlots);
+  CopyPool& pool = CopyPool::get();
+  for (uint64_t k = 0; k < nchunks + kSlots; ++k) {
+    const int s = (int)(k % kSlots);
+    std::vector<CopyPool::Job> jobs;
+    // drain the slot: chunk k - kSlots finished -> copy its results out
+    if (k >= kSlots) {
+      if (agq_status st = cuda_fail(cudaEventSynchronize(p.ev[s]), "host pipeline")) return st;
+      for (const Part& o : outs[s]) jobs.push_back({o.host, p.pin[s] + o.off, o.bytes});
+      outs[s].clear();
+    }
+    std::vector<Part> in;
+    if (k < nchunks) {
+      plan(k, in, outs[s]);
+      for (const Part& i : in) jobs.push_back({p.pin[s] + i.off, i.host, i.bytes});
+    }
+    pool.copy(jobs);
+    if (k >= nchunks) continue;
+    cudaStream_t st = p.st[s];
+    for (const Part& i : in)
+      cudaMemcpyAsync(p.dbuf[s] + i.off, p.pin[s] + i.off, i.bytes, cudaMemcpyHostToDevice, st);
+    if (agq_status r = launch(k, p.dbuf[s], st)) {
+      cudaDeviceSynchronize();
+      return r;
+    }
+    for (const Part& o : outs[s])
+      cudaMemcpyAsync(p.pin[s] + o.off, p.dbuf[s] + o.off, o.bytes, cudaMemcpyDeviceToHost, st);
+    if (agq_status r = cuda_fail(cudaEventRecord(p.ev[s], st), "host pipeline")) return r;
+  }
+  return AGQ_OK;
+}
+
+// Chunk length: a multiple of the block (chunks must not split blocks) and,
+// for block 128, of the 1024-element warp tile.
+uint64_t chunk_elems(uint64_t n, uint32_t block) {
+  uint64_t unit = block;
+  if (1024 % block == 0) unit = 1024;
+  uint64_t c = std::max<uint64_t>(unit, kChunkElems / unit * unit);
+  return std::min<uint64_t>(c, (n + unit - 1) / unit * unit);
+}
+
+agq_status read_errors(HostPipe& p, int op) {
+  agq_errors h;
+  if (agq_status st = cuda_fail(cudaMemcpy(&h, p.d_err, sizeof(h), cudaMemcpyDeviceToHost),
+                                "host pipeline: errors"))
+    return st;
+  return agq_errors_message(&h, op, nullptr, 0);
+}
+
+}  // namespace
+}  // namespace agqh
+
+extern "C" {
+
 agq_status agq_quantize_host(const float* x, uint64_t n, int bits, uint32_t block, int codec,
                              uint8_t* codes, float* scales) {
   if (agq_status st = check_args(bits, block, codec)) return st;
   if (agq_status st = check_device()) return st;
   if (n == 0) return AGQ_OK;
-  Workspace& w = workspace();
-  std::lock_guard<std::mutex> lk(w.mu);
-  const uint64_t nb = (n + block - 1) / block;
-  const size_t ox = 0, oc = al(n * 4), os = oc + al(n), oe = os + al(nb * 4);
-  if (agq_status st = ws_reserve(w, oe + al(sizeof(agq_errors)))) return st;
-  char* base = static_cast<char*>(w.dev);
-  agq_errors* d_err = reinterpret_cast<agq_errors*>(base + oe);
-  cudaStream_t s = w.stream;
-  cudaMemcpyAsync(base + ox, x, n * 4, cudaMemcpyHostToDevice, s);
-  agq_errors_reset(d_err, (agq_stream_t)s);
-  agq_status st = quantize_device(base + ox, AGQ_F32, n, bits, block, codec, base + oc,
-                                  AGQ_CODES_BYTES, reinterpret_cast<float*>(base + os), d_err, s);
+  const uint64_t ce = chunk_elems(n, block), K = (n + ce - 1) / ce;
+  const size_t oc = al(ce * 4), os = oc + al(ce), slot = os + al((ce / block + 1) * 4);
+  PipeLease lease;
+  HostPipe& p = *lease.p;
+  agq_status st = run_pipeline(
+      p, K, slot,
+      [&](uint64_t k, std::vector<Part>& in, std::vector<Part>& out) {
+        const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
+        const uint64_t nb = (len + block - 1) / block;
+        in.push_back({0, len * 4, (char*)(x + e0)});
+        out.push_back({oc, len, (char*)(codes + e0)});
+        out.push_back({os, nb * 4, (char*)(scales + e0 / block)});
+      },
+      [&](uint64_t k, char* d, cudaStream_t s) {
+        const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
+        return quantize_device_at(d, AGQ_F32, len, bits, block, codec, d + oc, AGQ_CODES_BYTES,
+                                  reinterpret_cast<float*>(d + os), (long long)(e0 / block),
+                                  p.d_err, s);
+      });
   if (st) return st;
-  agq_errors h;
-  cudaMemcpyAsync(codes, base + oc, n, cudaMemcpyDeviceToHost, s);
-  cudaMemcpyAsync(scales, base + os, nb * 4, cudaMemcpyDeviceToHost, s);
-  cudaMemcpyAsync(&h, d_err, sizeof(h), cudaMemcpyDeviceToHost, s);
-  if (agq_status e = cuda_fail(cudaStreamSynchronize(s), "quantize_host")) return e;
-  return agq_errors_message(&h, AGQ_OP_QUANTIZE, nullptr, 0);
+  return read_errors(p, AGQ_OP_QUANTIZE);
 }
 
 agq_status agq_dequantize_host(const uint8_t* codes, const float* scales, uint64_t n, int bits,
@@ -450,26 +698,27 @@ agq_status agq_dequantize_host(const uint8_t* codes, const float* scales, uint64
   if (agq_status st = check_args(bits, block, codec)) return st;
   if (agq_status st = check_device()) return st;
   if (n == 0) return AGQ_OK;
-  Workspace& w = workspace();
-  std::lock_guard<std::mutex> lk(w.mu);
-  const uint64_t nb = (n + block - 1) / block;
-  const size_t oc = 0, os = al(n), oo = os + al(nb * 4), oe = oo + al(n * 4);
-  if (agq_status st = ws_reserve(w, oe + al(sizeof(agq_errors)))) return st;
-  char* base = static_cast<char*>(w.dev);
-  agq_errors* d_err = reinterpret_cast<agq_errors*>(base + oe);
-  cudaStream_t s = w.stream;
-  cudaMemcpyAsync(base + oc, codes, n, cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(base + os, scales, nb * 4, cudaMemcpyHostToDevice, s);
-  agq_errors_reset(d_err, (agq_stream_t)s);
-  agq_status st = dequantize_device(base + oc, AGQ_CODES_BYTES, reinterpret_cast<float*>(base + os),
-                                    n, bits, block, codec, base + oo, AGQ_F32, 1, d_err, s);
+  const uint64_t ce = chunk_elems(n, block), K = (n + ce - 1) / ce;
+  const size_t os = al(ce), oo = os + al((ce / block + 1) * 4), slot = oo + al(ce * 4);
+  PipeLease lease;
+  HostPipe& p = *lease.p;
+  agq_status st = run_pipeline(
+      p, K, slot,
+      [&](uint64_t k, std::vector<Part>& in, std::vector<Part>& o) {
+        const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
+        const uint64_t nb = (len + block - 1) / block;
+        in.push_back({0, len, (char*)(codes + e0)});
+        in.push_back({os, nb * 4, (char*)(scales + e0 / block)});
+        o.push_back({oo, len * 4, (char*)(out + e0)});
+      },
+      [&](uint64_t k, char* d, cudaStream_t s) {
+        const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
+        return dequantize_device_at(d, AGQ_CODES_BYTES, reinterpret_cast<float*>(d + os), len,
+                                    bits, block, codec, d + oo, AGQ_F32, 1,
+                                    (long long)(e0 / block), p.d_err, s);
+      });
   if (st) return st;
-  agq_errors h;
-  cudaMemcpyAsync(&h, d_err, sizeof(h), cudaMemcpyDeviceToHost, s);
-  if (agq_status e = cuda_fail(cudaStreamSynchronize(s), "dequantize_host")) return e;
-  if (agq_status e = agq_errors_message(&h, AGQ_OP_DEQUANTIZE, nullptr, 0)) return e;
-  cudaMemcpyAsync(out, base + oo, n * 4, cudaMemcpyDeviceToHost, s);
-  return cuda_fail(cudaStreamSynchronize(s), "dequantize_host");
+  return read_errors(p, AGQ_OP_DEQUANTIZE);
 }
 
 agq_status agq_local_accumulate_host(const uint8_t* codes, const float* scales, uint64_t n,
@@ -478,30 +727,34 @@ agq_status agq_local_accumulate_host(const uint8_t* codes, const float* scales, 
   if (agq_status st = check_args(8, block, AGQ_CODEC_FP8_E4M3)) return st;
   if (agq_status st = check_device()) return st;
   if (n == 0) return AGQ_OK;
-  Workspace& w = workspace();
-  std::lock_guard<std::mutex> lk(w.mu);
-  const uint64_t nb = (n + block - 1) / block;
-  const size_t oc = 0, os = al(n), ol = os + al(nb * 4), oe = ol + al(n * 4);
-  if (agq_status st = ws_reserve(w, oe + al(sizeof(agq_errors)))) return st;
-  char* base = static_cast<char*>(w.dev);
-  agq_errors* d_err = reinterpret_cast<agq_errors*>(base + oe);
-  cudaStream_t s = w.stream;
-  cudaMemcpyAsync(base + oc, codes, n, cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(base + os, scales, nb * 4, cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(base + ol, local, n * 4, cudaMemcpyHostToDevice, s);
-  agq_errors_reset(d_err, (agq_stream_t)s);
-  agq_status st = accumulate_device(reinterpret_cast<uint8_t*>(base + oc),
-                                    reinterpret_cast<float*>(base + os), base + ol, AGQ_F32, n,
-                                    block, precision, reinterpret_cast<uint8_t*>(base + oc),
-                                    reinterpret_cast<float*>(base + os), d_err, s);
+  const uint64_t ce = chunk_elems(n, block), K = (n + ce - 1) / ce;
+  // inputs [codes | scales | local], outputs [codes | scales] after them: the
+  // next chunk's inputs are staged while this slot's outputs drain
+  const size_t os = al(ce), ol = os + al((ce / block + 1) * 4), oc = ol + al(ce * 4);
+  const size_t oo = oc + al(ce), slot = oo + al((ce / block + 1) * 4);
+  PipeLease lease;
+  HostPipe& p = *lease.p;
+  agq_status st = run_pipeline(
+      p, K, slot,
+      [&](uint64_t k, std::vector<Part>& in, std::vector<Part>& o) {
+        const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
+        const uint64_t nb = (len + block - 1) / block;
+        in.push_back({0, len, (char*)(codes + e0)});
+        in.push_back({os, nb * 4, (char*)(scales + e0 / block)});
+        in.push_back({ol, len * 4, (char*)(local + e0)});
+        o.push_back({oc, len, (char*)(out_codes + e0)});
+        o.push_back({oo, nb * 4, (char*)(out_scales + e0 / block)});
+      },
+      [&](uint64_t k, char* d, cudaStream_t s) {
+        const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
+        return accumulate_device(reinterpret_cast<uint8_t*>(d), reinterpret_cast<float*>(d + os),
+                                 d + ol, AGQ_F32, len, block, precision,
+                                 reinterpret_cast<uint8_t*>(d + oc),
+                                 reinterpret_cast<float*>(d + oo), p.d_err, s,
+                                 (long long)(e0 / block));
+      });
   if (st) return st;
-  agq_errors h;
-  cudaMemcpyAsync(&h, d_err, sizeof(h), cudaMemcpyDeviceToHost, s);
-  if (agq_status e = cuda_fail(cudaStreamSynchronize(s), "local_accumulate_host")) return e;
-  if (agq_status e = agq_errors_message(&h, AGQ_OP_ACCUMULATE, nullptr, 0)) return e;
-  cudaMemcpyAsync(out_codes, base + oc, n, cudaMemcpyDeviceToHost, s);
-  cudaMemcpyAsync(out_scales, base + os, nb * 4, cudaMemcpyDeviceToHost, s);
-  return cuda_fail(cudaStreamSynchronize(s), "local_accumulate_host");
+  return read_errors(p, AGQ_OP_ACCUMULATE);
 }
 
 agq_status agq_allreduce_simulated_host(int world, const uint8_t* const* codes,

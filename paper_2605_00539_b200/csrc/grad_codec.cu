@@ -43,7 +43,7 @@ __device__ __forceinline__ uint32_t acc_swz(uint32_t row, uint32_t c) {
 // error) by re-reading this lane's local values from the warp's staging slot.
 template <bool BF16L>
 __device__ __noinline__ void acc_report_nonfinite(const unsigned char* wb, int lane, uint64_t t,
-                                                  uint64_t gblk, agq_errors* err) {
+                                                  uint64_t gblk, long long eb, agq_errors* err) {
   constexpr int kCh = BF16L ? 2 : 4;
   uint32_t lbad = 0;
   for (int j = 0; j < kCh; ++j) {
@@ -60,8 +60,9 @@ __device__ __noinline__ void acc_report_nonfinite(const unsigned char* wb, int l
     }
   }
   if (lbad)
-    err_min(&err->nonfinite_local, (long long)(t * kAccWarpElems + lane * 16 + (__ffs(lbad) - 1)));
-  if ((lane & 7) == 0) err_min(&err->nonfinite_block, (long long)gblk);
+    err_min(&err->nonfinite_local,
+            eb * kBlock + (long long)(t * kAccWarpElems + lane * 16 + (__ffs(lbad) - 1)));
+  if ((lane & 7) == 0) err_min(&err->nonfinite_block, eb + (long long)gblk);
 }
 
 // Resident CTAs per SM: 3, except the FP32-local BF16-rounded instance,
@@ -70,7 +71,9 @@ __device__ __noinline__ void acc_report_nonfinite(const unsigned char* wb, int l
 template <bool BF16L, int PREC>
 __global__ void __launch_bounds__(kAccWarps * 32, !BF16L && PREC == AGQ_ACC_BF16 ? 2 : 3)
     k_accumulate_warp(const uint8_t* codes, const float* scales, const void* local,
-                      uint64_t ntiles, uint8_t* out_codes, float* out_scales, agq_errors* err) {
+                      uint64_t ntiles, uint8_t* out_codes, float* out_scales, long long eb,
+                      agq_errors* err) {
+  // eb: block index of element 0 in the error record (chunked host calls)
   constexpr int kCh = BF16L ? 2 : 4;
   constexpr uint32_t kRowB = kCh * 16;
   constexpr uint32_t kLocTileB = kAccWarpElems * (BF16L ? 2 : 4);  // 1 KB / 2 KB
@@ -127,7 +130,7 @@ __global__ void __launch_bounds__(kAccWarps * 32, !BF16L && PREC == AGQ_ACC_BF16
     __syncwarp();
     const uint64_t gblk = t * 4 + (lane >> 3);
     if ((!(sc >= 0.0f) || !(sc <= 3.402823466e38f)) && (lane & 7) == 0)
-      err_min(&err->bad_scale_block, (long long)gblk);
+      err_min(&err->bad_scale_block, eb + (long long)gblk);
     float v[16];
     // block-table decode for the FP32-local / FP32-sum kernel (shared-memory
     // bound on the 256-entry table: 86% -> 93% of HBM); the BF16-local and
@@ -148,7 +151,7 @@ __global__ void __launch_bounds__(kAccWarps * 32, !BF16L && PREC == AGQ_ACC_BF16
     }
     const uint32_t m = absmax_bits16(v);
     if (m >= 0x7f800000u)  // rare: kept out of line so it is not if-converted
-      acc_report_nonfinite<BF16L>(wb, lane, t, gblk, err);
+      acc_report_nonfinite<BF16L>(wb, lane, t, gblk, eb, err);
     uint32_t ow[4];
     fp8_requant16(v, u2f(m), ow);
     *reinterpret_cast<uint4*>(out_codes + t * kAccWarpElems + lane * 16) =
@@ -264,23 +267,26 @@ __global__ void __launch_bounds__(256, 1)
 // K4 with a per-warp cp.async ring (LDGSTS): the NP pieces' code words
 // (16 B per lane per piece) and block scales of warp-group i+S-1 are in
 // flight while warp-group i (512 elements = 4 blocks) is decoded, so a warp
-// keeps HBM requests outstanding through its arithmetic — the direct-load
-// kernel issues a group's loads, then idles the memory system while it
-// decodes. Whole 512-element warp-groups only (16-byte aligned pointers); the
-// ragged tail goes through reduce_group. Same arithmetic (reduce_compute), so
-// bit-identical.
+// keeps HBM requests outstanding through its arithmetic. Whole 512-element
+// warp-groups only (16-byte aligned pointers); the ragged tail goes through
+// reduce_group. Pieces are decoded one at a time straight from the ring slot
+// with the f16-route block tables (dq_f16_accum: no per-code safety test, a
+// register footprint independent of NP), summed from +0.0f in ascending
+// piece order, so bit-identical to reduce_group.
 template <int NP, int S>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, NP <= 4 ? 3 : 2)
     k_reduce128_pipe(PieceTable pt, uint64_t len, long long blk_base, agq_errors* err) {
   extern __shared__ __align__(16) unsigned char ring_smem[];
   __shared__ double lut[kDqTable];
-  __shared__ float btab[8 * NP * 32];
+  __shared__ __align__(16) float btab[8 * NP * 32];
   fill_fp8_dq_table(lut);
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr uint32_t kSlot = NP * 512 + NP * 16;  // codes, then 4 scales per piece
   unsigned char* ring = ring_smem + (size_t)warp * S * kSlot;
   float* wtab = btab + warp * NP * 32;
+  const float* mytab = wtab + (lane >> 3) * 8;  // this lane's block, piece 0
+  const double t8 = fp8_t8(lane & 7);           // lane 8b + j builds entry j of block b
   const uint64_t nwg = len / 512;
   const uint64_t wstride = gridDim.x * 8ull;
   auto issue = [&](uint64_t gi, int k) {
@@ -299,22 +305,39 @@ __global__ void __launch_bounds__(256, 1)
   for (int k = 0; k < S - 1; ++k) issue(wg + k * wstride, k);
   int slot = 0;
   for (; wg < nwg; wg += wstride) {
-    __syncwarp();  // every lane is done reading the slot refilled next
+    __syncwarp();  // every lane is done reading the slot refilled next (and the tables)
     issue(wg + (S - 1) * wstride, slot == 0 ? S - 1 : slot - 1);
     cp_async_wait<S - 1>();
     __syncwarp();
     const unsigned char* sl = ring + slot * kSlot;
-    uint4 cv[NP];
-    float sc[NP];
+    const float* scs = reinterpret_cast<const float*>(sl + NP * 512) + (lane >> 3);
+    uint32_t sbad = 0;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-      cv[p] = lds128(sl + p * 512 + lane * 16);
-      sc[p] = reinterpret_cast<const float*>(sl + NP * 512)[p * 4 + (lane >> 3)];
+      const float sc = scs[p * 4];
+      wtab[p * 32 + lane] = fp8_tab_entry_f16(t8, sc);
+      sbad |= bad_scale_bit(sc, p);
     }
-    reduce_compute<NP>(pt, wg * 512 + lane * 16, len, true, cv, sc, blk_base, lut, err, wtab);
+    __syncwarp();
+    float acc[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) acc[e] = 0.0f;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const uint4 cv = lds128(sl + p * 512 + lane * 16);
+      const uint32_t w[4] = {cv.x, cv.y, cv.z, cv.w};
+      const float sc = scs[p * 4];
+      if (dq_fast(sc))
+        dq_f16_accum<4>(w, mytab + p * 32, acc);
+      else  // zero / extreme block scale: the 256-entry table of exact units
+        dq_accum<16>(w, sc, lut, acc);
+    }
+    reduce_finish(pt, wg * 512 + lane * 16, len, true, true, (wg * 512 + lane * 16) / kBlock, sbad,
+                  acc, blk_base, err);
     slot = slot == S - 1 ? 0 : slot + 1;
   }
   cp_async_wait<0>();
+  __syncwarp();
   // ragged tail (< 512 elements) in 16-element groups, warp-uniform trip count
   const uint64_t ngroups = (len + kBlock - 1) / kBlock * 8;
   const uint64_t gpad = (ngroups + 31) / 32 * 32;
@@ -488,8 +511,8 @@ void launch_reduce128(const PieceTable& pt, uint64_t len, long long bb, int vec,
 namespace {
 template <bool BF16L, int PREC>
 agq_status launch_acc_warp(const uint8_t* codes, const float* scales, const void* local,
-                           uint64_t ntiles, uint8_t* oc, float* os, agq_errors* err,
-                           cudaStream_t s) {
+                           uint64_t ntiles, uint8_t* oc, float* os, long long eb,
+                           agq_errors* err, cudaStream_t s) {
   auto k = k_accumulate_warp<BF16L, PREC>;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kAccWarps * 32, 0);
@@ -497,24 +520,27 @@ agq_status launch_acc_warp(const uint8_t* codes, const float* scales, const void
   const uint64_t want = (ntiles + kAccWarps - 1) / kAccWarps;
   const uint64_t cap = (uint64_t)num_sms() * occ;
   k<<<(int)(want < cap ? want : cap), kAccWarps * 32, 0, s>>>(codes, scales, local, ntiles, oc,
-                                                              os, err);
+                                                              os, eb, err);
   count_launch();
   return cuda_fail(cudaGetLastError(), "accumulate: launch");
 }
 
 template <bool BF16L>
 agq_status acc_warp_prec(int prec, const uint8_t* codes, const float* scales, const void* local,
-                         uint64_t ntiles, uint8_t* oc, float* os, agq_errors* err,
+                         uint64_t ntiles, uint8_t* oc, float* os, long long eb, agq_errors* err,
                          cudaStream_t s) {
-  if (prec == AGQ_ACC_BF16) return launch_acc_warp<BF16L, AGQ_ACC_BF16>(codes, scales, local, ntiles, oc, os, err, s);
-  if (prec == AGQ_ACC_FP16) return launch_acc_warp<BF16L, AGQ_ACC_FP16>(codes, scales, local, ntiles, oc, os, err, s);
-  return launch_acc_warp<BF16L, AGQ_ACC_FP32>(codes, scales, local, ntiles, oc, os, err, s);
+  if (prec == AGQ_ACC_BF16) return launch_acc_warp<BF16L, AGQ_ACC_BF16>(codes, scales, local, ntiles, oc, os, eb, err, s);
+  if (prec == AGQ_ACC_FP16) return launch_acc_warp<BF16L, AGQ_ACC_FP16>(codes, scales, local, ntiles, oc, os, eb, err, s);
+  return launch_acc_warp<BF16L, AGQ_ACC_FP32>(codes, scales, local, ntiles, oc, os, eb, err, s);
 }
 }  // namespace
 
+// blk_base: block index of element 0 in the error record (the offset of a
+// chunk inside the caller's tensor; 0 for a whole-tensor call).
 agq_status accumulate_device(const uint8_t* codes, const float* scales, const void* local,
                              int local_dtype, uint64_t n, uint32_t block, int prec,
-                             uint8_t* oc, float* os, agq_errors* err, cudaStream_t s) {
+                             uint8_t* oc, float* os, agq_errors* err, cudaStream_t s,
+                             long long blk_base) {
   if (n == 0) return AGQ_OK;
   const bool bf16l = local_dtype == AGQ_BF16;
   const uint64_t unit = kAccWarpElems;
@@ -524,8 +550,8 @@ agq_status accumulate_device(const uint8_t* codes, const float* scales, const vo
     ntiles = n / unit;
   if (ntiles) {
     const agq_status r =
-        bf16l ? acc_warp_prec<true>(prec, codes, scales, local, ntiles, oc, os, err, s)
-              : acc_warp_prec<false>(prec, codes, scales, local, ntiles, oc, os, err, s);
+        bf16l ? acc_warp_prec<true>(prec, codes, scales, local, ntiles, oc, os, blk_base, err, s)
+              : acc_warp_prec<false>(prec, codes, scales, local, ntiles, oc, os, blk_base, err, s);
     if (r != AGQ_OK) return r;
   }
   const uint64_t done = ntiles * unit;
@@ -533,7 +559,7 @@ agq_status accumulate_device(const uint8_t* codes, const float* scales, const vo
   const uint64_t rest = n - done, nb = (rest + block - 1) / block;
   const void* ltail = static_cast<const char*>(local) + done * (bf16l ? 2 : 4);
   const int grid = gen_grid(nb * 32, 256);
-  const long long base = (long long)done;
+  const long long base = blk_base * (long long)block + (long long)done;
   if (prec == AGQ_ACC_BF16)
     k_accumulate_generic<AGQ_ACC_BF16><<<grid, 256, 0, s>>>(codes + done, scales + done / block, ltail,
         bf16l, rest, block, nb, oc + done, os + done / block, base, err);

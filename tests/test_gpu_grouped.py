@@ -1,6 +1,6 @@
 """Grouped launches over a whole pipeline stage (layers.hpp:266-301 stored
 set of every layer, dbca.hpp:172-177 stage width): any number of tensors in
-one call (split per 32 segments), equal to the single-tensor path, and the
+one call (one launch per 8 segments), equal to the single-tensor path, and the
 reference's validate errors (quantize.hpp:157-179) from grouped dequantize,
 reported for the first failing tensor with its own local index."""
 import numpy as np
@@ -24,14 +24,14 @@ def _layers(dev, nlayers, T, seed):
     return out
 
 
-def test_stage_store_4_layers_20_tensors_one_launch(cuda):
+def test_stage_store_4_layers_20_tensors_one_call(cuda):
     layers = _layers(cuda, 4, 256, 1)
     plan = A.plan_bit_widths(A.PipelineConfig(8, 16, 2))
     for stage in (1, 5, 8):
         store = A.StageActivationStore(A.stage_policy(plan, stage))
         n0 = A.launch_count()
         store.store(layers)
-        assert A.launch_count() - n0 == 1  # 20 tensors, one width, whole warp tiles
+        assert A.launch_count() - n0 == 3  # 20 tensors, one width: launches of 8 segments
         bits = plan.stages[stage - 1].assigned_bits
         back = store.read_all()
         for li, d in enumerate(layers):
@@ -46,7 +46,7 @@ def test_stage_store_4_layers_20_tensors_one_launch(cuda):
 
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
-def test_grouped_more_than_32_tensors_ragged(cuda, dtype):
+def test_grouped_many_tensors_ragged(cuda, dtype):
     rng = np.random.default_rng(7)
     sizes = [int(s) for s in rng.integers(1, 40000, 45)] + [8192 * 3, 1024, 128 * 9 + 5]
     xs = [torch.from_numpy(rng.standard_normal(n).astype(np.float32)).to(cuda).to(dtype)

@@ -285,6 +285,10 @@ agq_status agq_local_accumulate_host(const uint8_t* codes, const float* scales,
                                      uint64_t n, uint32_t block,
                                      const float* local, int precision,
                                      uint8_t* out_codes, float* out_scales);
+/* Diagnostics of the host-buffer pipelines: out[0..3] = cumulative seconds
+ * inside the pipelines, of host copies (caller <-> pinned staging), waiting
+ * for device work, and the number of calls; reset != 0 zeroes them. */
+agq_status agq_host_pipeline_stats(double* out, int reset);
 agq_status agq_allreduce_simulated_host(int world, const uint8_t* const* codes,
                                         const float* const* scales, uint64_t n,
                                         uint32_t block, int protocol /*0 dec,1 naive*/,

@@ -591,20 +591,18 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? kDequan
       if constexpr (CODEC == 2) mfast = fast && !fp8_row_has_nan<PACK>(cw);
       else mfast = fast;
     }
-    bool tfast = false;  // FP8, FP32 scale: block-table decode
-    uint32_t tb_s = 0;
+    bool tfast = false;  // FP8, FP32 scale: block-table decode (f16 route)
+    uint32_t tb = 0;
     if constexpr (CODEC == 2) {
       float* wt = dqtab + (threadIdx.x >> 5) * 64;
       const int j0 = (lane & 3) * 2;
       __syncwarp();  // the previous tile's lookups are done
-      wt[(lane >> 2) * 8 + j0] = fp8_tab_entry_half(fp8_t8(j0), s);
-      wt[(lane >> 2) * 8 + j0 + 1] = fp8_tab_entry_half(fp8_t8(j0 + 1), s);
+      wt[(lane >> 2) * 8 + j0] = fp8_tab_entry_f16(fp8_t8(j0), s);
+      wt[(lane >> 2) * 8 + j0 + 1] = fp8_tab_entry_f16(fp8_t8(j0 + 1), s);
       __syncwarp();
-      uint32_t unsafe = 0;
-#pragma unroll
-      for (int k = 0; k < PACK; ++k) unsafe |= fp8_tab_unsafe(cw[k]);
-      tfast = !fast && dq_fast(s) && unsafe == 0;
-      tb_s = (uint32_t)__cvta_generic_to_shared(wt + (lane >> 2) * 8);
+      // NaN codes keep the per-element path (the reference's NaN payload)
+      tfast = !fast && dq_fast(s) && !fp8_row_has_nan<PACK>(cw);
+      tb = (uint32_t)__cvta_generic_to_shared(wt + (lane >> 2) * 8);
     }
     uint64_t pk[kChunks];
     unpack_chunks<kChunkBits>(cw, pk, std::make_integer_sequence<int, kChunks>{});
@@ -615,8 +613,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? kDequan
 #pragma unroll
         for (int q = 0; q < kPerChunk / 4; ++q) {
           const uint32_t w1[1] = {cw[(j * kPerChunk) / 4 + q]};
-          float a4[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // + 0.0f: exact (entries are never 0)
-          dq_tab_accum<1>(w1, tb_s, a4);
+          // -0.0f + d = d for every d, signed zeros included
+          float a4[4] = {-0.0f, -0.0f, -0.0f, -0.0f};
+          dq_f16_accum<1>(w1, tb, a4);
 #pragma unroll
           for (int e = 0; e < 4; ++e) v[4 * q + e] = a4[e];
         }

@@ -25,6 +25,27 @@ __device__ __forceinline__ float apply_prec(float s) {
   if (PREC == AGQ_ACC_FP16) return round_fp16_ref(s);
   return s;
 }
+// round_bf16_ref / round_fp16_ref of 16 FINITE sums in pairs: cvt.rn.bf16x2
+// (RNE; overflow to inf like the integer rule) and cvt.rn.satfinite.f16x2
+// (RNE; |x| >= 65520 -> +-65504, the reference's saturation), then back to
+// FP32 exactly.
+template <int PREC>
+__device__ __forceinline__ void round_pairs16(float (&v)[16]) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    uint32_t d;
+    if (PREC == AGQ_ACC_BF16) {
+      asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(v[2 * k + 1]), "f"(v[2 * k]));
+      v[2 * k] = u2f(d << 16);
+      v[2 * k + 1] = u2f(d & 0xffff0000u);
+    } else {
+      asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(v[2 * k + 1]), "f"(v[2 * k]));
+      asm("{\n.reg .b16 a, b;\nmov.b32 {a, b}, %2;\ncvt.f32.f16 %0, a;\ncvt.f32.f16 %1, b;\n}"
+          : "=f"(v[2 * k]), "=f"(v[2 * k + 1])
+          : "r"(d));
+    }
+  }
+}
 
 // Exact FP8 decode with an FP32 block scale, (float)(fl64(e4m3(c)/448)*(double)s):
 // a shared table of the signed unit values fl64(e4m3(c)/448) for every code
@@ -55,47 +76,6 @@ __device__ __forceinline__ uint32_t byte_of(uint32_t w, int k) {
 // block allows it, else the 256-entry signed unit table; both exact. The
 // multi-piece reduce kernels and the FP32-local K3 use the block table
 // (profiles/r01_reduce_tab_ab.log, r01_acc_tab_ab2.log).
-// Lean table decode + accumulate of NW code words (4 codes each) against
-// this block's table at shared address tb_s (32-byte aligned, 8 entries
-// holding F[m]/2): the entry address comes straight from the code word
-// (shift + one LOP3), the signed power of two 2^(e-15) from an arithmetic
-// shift + one LOP3 ((e | 0x70) = e + 112 for e < 16), products and sums in
-// f32x2 pairs (one FFMA2 per pair onto acc). Per element ~6 issued ops, no F2F,
-// no bank conflicts.
-__device__ __forceinline__ float lds_f32(uint32_t a) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
-  return v;
-}
-// 2^(e-15) exponent bias in a register the optimiser cannot see through, so
-// (y & mask) | bias is one LOP3 (a LOP3 takes a single immediate)
-__constant__ uint32_t c_pow2_bias = 0x38000000u;
-template <int NW>
-__device__ __forceinline__ void dq_tab_accum(const uint32_t (&w)[NW], uint32_t tb_s,
-                                             float (&acc)[4 * NW]) {
-  const uint32_t bias = c_pow2_bias;
-#pragma unroll
-  for (int i = 0; i < NW; ++i) {
-    float f[4], p2[4];
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const uint32_t x = b == 3 ? w[i] : (w[i] << (24 - 8 * b));
-      const uint32_t y = (uint32_t)((int32_t)x >> 4);
-      p2[b] = u2f((y & 0x87800000u) | bias);
-      const uint32_t idx = b == 0 ? ((w[i] << 2) & 0x1cu) : ((w[i] >> (8 * b - 2)) & 0x1cu);
-      f[b] = lds_f32(idx | tb_s);
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      // one FFMA2 = fadd(acc, F*2^k) bit for bit: the product is exact (a
-      // normal float times a power of two), so the fused add rounds once,
-      // exactly like the separate add
-      const f32x2 a = fma2(pk2(f[2 * h], f[2 * h + 1]), pk2(p2[2 * h], p2[2 * h + 1]),
-                           pk2(acc[4 * i + 2 * h], acc[4 * i + 2 * h + 1]));
-      up2(a, acc[4 * i + 2 * h], acc[4 * i + 2 * h + 1]);
-    }
-  }
-}
 // ---- f16-route block-table decode (every code, no per-code safety test) ----
 // The hardware cvt.rn.f16x2.e4m3x2 gives every E4M3 value v exactly; as an
 // FP32 value v = sign * (1 + M/8) * 2^X with a 3-bit M for EVERY code
@@ -110,12 +90,17 @@ __device__ __forceinline__ void dq_tab_accum(const uint32_t (&w)[NW], uint32_t t
 __device__ __forceinline__ float fp8_tab_entry_f16(double t8, float s) {
   return fmul(fp8_tab_entry(t8, s), 0x1p-9f);  // exact: the entry is a normal float
 }
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
 // acc[4i + b] = fadd(acc[4i + b], dq(code b of w[i])) through this lane's
-// block table `tab` (8 floats in shared memory).
+// block table at shared address tb_s (8 floats, 32-byte aligned, so the
+// entry address is one LOP3: (mantissa bits & 0x1c) | tb_s).
 template <int NW>
-__device__ __forceinline__ void dq_f16_accum(const uint32_t (&w)[NW], const float* tab,
+__device__ __forceinline__ void dq_f16_accum(const uint32_t (&w)[NW], uint32_t tb_s,
                                              float (&acc)[4 * NW]) {
-  const char* tb = reinterpret_cast<const char*>(tab);
 #pragma unroll
   for (int i = 0; i < NW; ++i) {
     uint32_t h[2];
@@ -125,14 +110,16 @@ __device__ __forceinline__ void dq_f16_accum(const uint32_t (&w)[NW], const floa
         : "r"(w[i]));
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
-      float f0, f1;
+      // sign | exponent of both halves (one LOP3), then to FP32: p = +-2^X
+      // exactly (every E4M3 value is an f16 normal or zero; NaN -> inf)
+      float p0, p1;
       asm("{\n.reg .b16 a, b;\nmov.b32 {a, b}, %2;\ncvt.f32.f16 %0, a;\ncvt.f32.f16 %1, b;\n}"
-          : "=f"(f0), "=f"(f1)
-          : "r"(h[k]));
-      const float p0 = u2f(f2u(f0) & 0xff800000u), p1 = u2f(f2u(f1) & 0xff800000u);
-      const uint32_t t = h[k] >> 5;  // f16 mantissa bits 7-9 -> byte offset M * 4
-      const float e0 = *reinterpret_cast<const float*>(tb + (t & 0x1cu));
-      const float e1 = *reinterpret_cast<const float*>(tb + ((t >> 16) & 0x1cu));
+          : "=f"(p0), "=f"(p1)
+          : "r"(h[k] & 0xfc00fc00u));
+      // f16 mantissa bits 7-9 (23-25) -> byte offset M * 4; the second shift
+      // as a multiply-high (FMA pipe) to offload the integer ALU pipe
+      const float e0 = lds_f32(((h[k] >> 5) & 0x1cu) | tb_s);
+      const float e1 = lds_f32((__umulhi(h[k], 1u << 11) & 0x1cu) | tb_s);
       const f32x2 a = fma2(pk2(e0, e1), pk2(p0, p1),
                            pk2(acc[4 * i + 2 * k], acc[4 * i + 2 * k + 1]));
       up2(a, acc[4 * i + 2 * k], acc[4 * i + 2 * k + 1]);
@@ -140,19 +127,7 @@ __device__ __forceinline__ void dq_f16_accum(const uint32_t (&w)[NW], const floa
   }
 }
 
-__device__ __forceinline__ float fp8_tab_entry_half(double t8, float s) {
-  return fmul(fp8_tab_entry(t8, s), 0.5f);  // exact: the entry is a normal float
-}
-
-__device__ __forceinline__ bool fp8_tab_ok16(const uint32_t (&w)[4]) {
-  return (fp8_tab_unsafe(w[0]) | fp8_tab_unsafe(w[1]) | fp8_tab_unsafe(w[2]) |
-          fp8_tab_unsafe(w[3])) == 0u;
-}
-__device__ __forceinline__ bool fp8_tab_ok8(const uint32_t (&w)[2]) {
-  return (fp8_tab_unsafe(w[0]) | fp8_tab_unsafe(w[1])) == 0u;
-}
-
-// A block scale for which fp8_dequant_t16i is exact (zero blocks excluded).
+// A block scale for which the block-table decode is exact (zero blocks excluded).
 __device__ __forceinline__ bool dq_fast(float s) { return s >= kFastLo && s <= kFastHi; }
 
 // acc[e] = fadd(acc[e], dequant(code e of w, sc)) for the N codes of one
@@ -267,27 +242,22 @@ struct PieceTable {
   int np, nout;
 };
 
-// Fill this warp's per-piece block tables after the previous group's lookups
-// are done. LPB lanes per 128-block (8: 16 elements per lane, 16: 8 per
-// lane); lane l builds entry (l & 7) of warp-local block l / LPB, so a piece
-// table is 32 / LPB blocks x 8 entries (lanes l and l + 8 of a 16-lane block
-// store the same value). Blocks past the end build from scale 0 (unused).
-template <int LPB>
-__device__ __forceinline__ uint32_t tab_slot(int lane) { return (lane / LPB) * 8 + (lane & 7); }
-template <int NP, int LPB>
+// Fill this warp's per-piece block tables (dq_f16_accum) after the previous
+// group's lookups are done: 8 lanes per 128-block, lane l builds entry (l & 7)
+// of warp-local block l / 8, so a piece table is 4 blocks x 8 entries. Blocks
+// past the end build from scale 0 (unused).
+template <int NP>
 __device__ __forceinline__ void build_tables(float* wtab, const float (&sc)[NP]) {
   const int lane = threadIdx.x & 31;
   const double t8 = fp8_t8(lane & 7);
   __syncwarp();
 #pragma unroll
-  for (int p = 0; p < NP; ++p) wtab[p * (256 / LPB) + tab_slot<LPB>(lane)] = fp8_tab_entry_half(t8, sc[p]);
+  for (int p = 0; p < NP; ++p) wtab[p * 32 + lane] = fp8_tab_entry_f16(t8, sc[p]);
   __syncwarp();
 }
 // shared address of this lane's block table for piece p
-template <int LPB>
-__device__ __forceinline__ uint32_t tab_addr(const float* wtab, int p) {
-  const int lane = threadIdx.x & 31;
-  return (uint32_t)__cvta_generic_to_shared(wtab + p * (256 / LPB) + (lane / LPB) * 8);
+__device__ __forceinline__ uint32_t lane_tab(const float* wtab, int p) {
+  return (uint32_t)__cvta_generic_to_shared(wtab + p * 32 + ((threadIdx.x & 31) >> 3) * 8);
 }
 
 // Bad block scale of the all-reduce's inputs: the reference validates the
@@ -321,14 +291,14 @@ __device__ __forceinline__ void reduce_compute(const PieceTable& pt, uint64_t e0
 #pragma unroll
   for (int e = 0; e < 16; ++e) acc[e] = 0.0f;
   uint32_t sbad = 0;
-  if (wtab != nullptr) build_tables<NP, 8>(wtab, sc);  // all lanes
+  if (wtab != nullptr) build_tables<NP>(wtab, sc);  // all lanes
   if (in_range) {
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       sbad |= bad_scale_bit(sc[p], p);
       const uint32_t w[4] = {cv[p].x, cv[p].y, cv[p].z, cv[p].w};
-      if (wtab != nullptr && dq_fast(sc[p]) && fp8_tab_ok16(w)) {
-        dq_tab_accum<4>(w, tab_addr<8>(wtab, p), acc);
+      if (wtab != nullptr && dq_fast(sc[p])) {
+        dq_f16_accum<4>(w, lane_tab(wtab, p), acc);
       } else {
         dq_accum<16>(w, sc[p], t16, acc);
       }

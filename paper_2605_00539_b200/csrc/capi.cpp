@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <atomic>
 #include <climits>
+#include <chrono>
 #include <condition_variable>
 #include <thread>
 #include <cmath>
@@ -569,6 +570,14 @@ struct HostPipe {
 std::mutex g_pipes_mu;
 std::vector<HostPipe*> g_pipes;
 
+// Cumulative host-side time of the pipelines (agq_host_pipeline_stats).
+std::atomic<unsigned long long> g_ns_copy{0}, g_ns_wait{0}, g_ns_total{0}, g_calls{0};
+unsigned long long now_ns() {
+  return (unsigned long long)std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
 struct PipeLease {
   HostPipe* p = nullptr;
   PipeLease() {
@@ -613,12 +622,16 @@ agq_status run_pipeline(HostPipe& p, uint64_t nchunks, size_t slot_bytes, Plan p
     return st;
   std::vector<std::vector<Part>> outs(kSlots);
   CopyPool& pool = CopyPool::get();
+  const unsigned long long t_start = now_ns();
+  unsigned long long t_copy = 0, t_wait = 0;
   for (uint64_t k = 0; k < nchunks + kSlots; ++k) {
     const int s = (int)(k % kSlots);
     std::vector<CopyPool::Job> jobs;
     // drain the slot: chunk k - kSlots finished -> copy its results out
     if (k >= kSlots) {
+      const unsigned long long t0 = now_ns();
       if (agq_status st = cuda_fail(cudaEventSynchronize(p.ev[s]), "host pipeline")) return st;
+      t_wait += now_ns() - t0;
       for (const Part& o : outs[s]) jobs.push_back({o.host, p.pin[s] + o.off, o.bytes});
       outs[s].clear();
     }
@@ -627,7 +640,9 @@ agq_status run_pipeline(HostPipe& p, uint64_t nchunks, size_t slot_bytes, Plan p
       plan(k, in, outs[s]);
       for (const Part& i : in) jobs.push_back({p.pin[s] + i.off, i.host, i.bytes});
     }
+    const unsigned long long t1 = now_ns();
     pool.copy(jobs);
+    t_copy += now_ns() - t1;
     if (k >= nchunks) continue;
     cudaStream_t st = p.st[s];
     for (const Part& i : in)
@@ -640,6 +655,10 @@ agq_status run_pipeline(HostPipe& p, uint64_t nchunks, size_t slot_bytes, Plan p
       cudaMemcpyAsync(p.pin[s] + o.off, p.dbuf[s] + o.off, o.bytes, cudaMemcpyDeviceToHost, st);
     if (agq_status r = cuda_fail(cudaEventRecord(p.ev[s], st), "host pipeline")) return r;
   }
+  g_ns_copy += t_copy;
+  g_ns_wait += t_wait;
+  g_ns_total += now_ns() - t_start;
+  ++g_calls;
   return AGQ_OK;
 }
 
@@ -664,6 +683,18 @@ agq_status read_errors(HostPipe& p, int op) {
 }  // namespace agqh
 
 extern "C" {
+
+agq_status agq_host_pipeline_stats(double* out, int reset) {
+  // [pipeline seconds, host copy seconds, event-wait seconds, calls]
+  if (out) {
+    out[0] = g_ns_total.load() * 1e-9;
+    out[1] = g_ns_copy.load() * 1e-9;
+    out[2] = g_ns_wait.load() * 1e-9;
+    out[3] = (double)g_calls.load();
+  }
+  if (reset) g_ns_total = g_ns_copy = g_ns_wait = g_calls = 0;
+  return AGQ_OK;
+}
 
 agq_status agq_quantize_host(const float* x, uint64_t n, int bits, uint32_t block, int codec,
                              uint8_t* codes, float* scales) {

@@ -234,14 +234,14 @@ __device__ __forceinline__ void fused_group(unsigned char* const (&base)[NP], ui
         cv[p] = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
-    build_tables<NP, 8>(wtab, sc);  // every lane of the warp
+    build_tables<NP>(wtab, sc);  // every lane of the warp
     if (in_range) {
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
         sbad |= bad_scale_bit(sc[p], p);
         const uint32_t w[4] = {cv[p].x, cv[p].y, cv[p].z, cv[p].w};
-        if (dq_fast(sc[p]) && fp8_tab_ok16(w))
-          dq_tab_accum<4>(w, tab_addr<8>(wtab, p), acc);
+        if (dq_fast(sc[p]))
+          dq_f16_accum<4>(w, lane_tab(wtab, p), acc);
         else
           dq_accum<16>(w, sc[p], t16, acc);
       }

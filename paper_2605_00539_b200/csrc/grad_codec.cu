@@ -65,11 +65,9 @@ __device__ __noinline__ void acc_report_nonfinite(const unsigned char* wb, int l
   if ((lane & 7) == 0) err_min(&err->nonfinite_block, eb + (long long)gblk);
 }
 
-// Resident CTAs per SM: 3, except the FP32-local BF16-rounded instance,
-// which spills at 3 and runs 356 -> 315 us at 2^28 at 2
-// (profiles/r01_acc_prec_ab.log).
+// Three resident CTAs per SM (24 warps).
 template <bool BF16L, int PREC>
-__global__ void __launch_bounds__(kAccWarps * 32, !BF16L && PREC == AGQ_ACC_BF16 ? 2 : 3)
+__global__ void __launch_bounds__(kAccWarps * 32, 3)
     k_accumulate_warp(const uint8_t* codes, const float* scales, const void* local,
                       uint64_t ntiles, uint8_t* out_codes, float* out_scales, long long eb,
                       agq_errors* err) {
@@ -85,7 +83,7 @@ __global__ void __launch_bounds__(kAccWarps * 32, !BF16L && PREC == AGQ_ACC_BF16
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* wb = sbuf[warp];
   const double t8 = fp8_t8(lane & 7);  // lane 8b+j builds entry j of block b
-  const float* mytab = &btab[warp][lane & ~7];
+  const uint32_t mytab = (uint32_t)__cvta_generic_to_shared(&btab[warp][lane & ~7]);
   const uint64_t nw = (uint64_t)gridDim.x * kAccWarps;
   uint64_t t = (uint64_t)blockIdx.x * kAccWarps + warp;
   const unsigned char* lbase = static_cast<const unsigned char*>(local);
@@ -108,7 +106,7 @@ __global__ void __launch_bounds__(kAccWarps * 32, !BF16L && PREC == AGQ_ACC_BF16
     }
     const uint32_t cw[4] = {pc.x, pc.y, pc.z, pc.w};
     const float sc = ps;
-    btab[warp][lane] = fp8_tab_entry_half(t8, sc);  // F[m] / 2 (dq_tab_accum)
+    btab[warp][lane] = fp8_tab_entry_f16(t8, sc);  // T[M] (dq_f16_accum)
     __syncwarp();
     if (t + nw < ntiles) load(t + nw);
     float l[16];
@@ -132,26 +130,29 @@ __global__ void __launch_bounds__(kAccWarps * 32, !BF16L && PREC == AGQ_ACC_BF16
     if ((!(sc >= 0.0f) || !(sc <= 3.402823466e38f)) && (lane & 7) == 0)
       err_min(&err->bad_scale_block, eb + (long long)gblk);
     float v[16];
-    // block-table decode for the FP32-local / FP32-sum kernel (shared-memory
-    // bound on the 256-entry table: 86% -> 93% of HBM); the BF16-local and
-    // rounded-precision instances measured faster with the full table
-    constexpr bool kTab = !BF16L && PREC == 0;
-    if (kTab && dq_fast(sc) && fp8_tab_ok16(cw)) {
-      // v = l + dq (exact product, one rounding: = fadd(dq, l))
+    // block-table decode of every code (f16 route, exact; the 256-entry
+    // table of exact units only for zero / extreme block scales):
+    // v = l + dq (exact product, one rounding: = fadd(dq, l))
+    if (dq_fast(sc)) {
 #pragma unroll
       for (int e = 0; e < 16; ++e) v[e] = l[e];
-      dq_tab_accum<4>(cw, (uint32_t)__cvta_generic_to_shared(mytab), v);
-#pragma unroll
-      for (int e = 0; e < 16; ++e) v[e] = apply_prec<PREC>(v[e]);
-    } else {  // zero/subnormal/NaN codes or an extreme scale: full table
+      dq_f16_accum<4>(cw, mytab, v);
+    } else {  // zero block or an extreme scale: full table
       const double sd = (double)sc;
 #pragma unroll
       for (int e = 0; e < 16; ++e)
-        v[e] = apply_prec<PREC>(fadd(fp8_dq_lut(byte_of(cw[e >> 2], e & 3), sd, t16), l[e]));
+        v[e] = fadd(fp8_dq_lut(byte_of(cw[e >> 2], e & 3), sd, t16), l[e]);
     }
-    const uint32_t m = absmax_bits16(v);
-    if (m >= 0x7f800000u)  // rare: kept out of line so it is not if-converted
+    // Rounding to BF16 / FP16 (collective.hpp:141-142) is monotone and odd,
+    // so the absmax of the rounded sums is the rounded absmax of the raw
+    // sums: one scalar rounding for the block scale, the values in pairs by
+    // the hardware conversions (identical to round_bf16 / round_fp16 for
+    // every finite sum; a non-finite sum is an error either way).
+    const uint32_t mr = absmax_bits16(v);
+    const uint32_t m = f2u(apply_prec<PREC>(u2f(mr)));
+    if (mr >= 0x7f800000u || m >= 0x7f800000u)  // rare: out of line, not if-converted
       acc_report_nonfinite<BF16L>(wb, lane, t, gblk, eb, err);
+    if constexpr (PREC != AGQ_ACC_FP32) round_pairs16<PREC>(v);
     uint32_t ow[4];
     fp8_requant16(v, u2f(m), ow);
     *reinterpret_cast<uint4*>(out_codes + t * kAccWarpElems + lane * 16) =
@@ -273,22 +274,30 @@ __global__ void __launch_bounds__(256, 1)
 // with the f16-route block tables (dq_f16_accum: no per-code safety test, a
 // register footprint independent of NP), summed from +0.0f in ascending
 // piece order, so bit-identical to reduce_group.
+// W warps per CTA: small CTAs pack more warps per SM under the shared-memory
+// limit of the ring (P = 8: 4-warp CTAs, 5 per SM = 20 warps, vs 2 x 8).
+template <int NP>
+struct RedCfg {
+  static constexpr int kWarps = NP <= 4 ? 8 : 4;
+  static constexpr int kMinBlocks = NP <= 4 ? 3 : 5;
+};
 template <int NP, int S>
-__global__ void __launch_bounds__(256, NP <= 4 ? 3 : 2)
+__global__ void __launch_bounds__(RedCfg<NP>::kWarps * 32, RedCfg<NP>::kMinBlocks)
     k_reduce128_pipe(PieceTable pt, uint64_t len, long long blk_base, agq_errors* err) {
+  constexpr int W = RedCfg<NP>::kWarps;
   extern __shared__ __align__(16) unsigned char ring_smem[];
   __shared__ double lut[kDqTable];
-  __shared__ __align__(16) float btab[8 * NP * 32];
+  __shared__ __align__(32) float btab[W * NP * 32];
   fill_fp8_dq_table(lut);
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr uint32_t kSlot = NP * 512 + NP * 16;  // codes, then 4 scales per piece
   unsigned char* ring = ring_smem + (size_t)warp * S * kSlot;
   float* wtab = btab + warp * NP * 32;
-  const float* mytab = wtab + (lane >> 3) * 8;  // this lane's block, piece 0
-  const double t8 = fp8_t8(lane & 7);           // lane 8b + j builds entry j of block b
-  const uint64_t nwg = len / 512;
-  const uint64_t wstride = gridDim.x * 8ull;
+  const uint32_t mytab = (uint32_t)__cvta_generic_to_shared(wtab + (lane >> 3) * 8);
+  const double t8 = fp8_t8(lane & 7);  // lane 8b + j builds entry j of block b
+  const uint64_t nwg = len / 512;      // whole warp-groups; the tail is another launch
+  const uint64_t wstride = gridDim.x * (uint64_t)W;
   auto issue = [&](uint64_t gi, int k) {
     if (gi < nwg) {
       unsigned char* sl = ring + k * kSlot;
@@ -300,7 +309,7 @@ __global__ void __launch_bounds__(256, NP <= 4 ? 3 : 2)
     }
     cp_async_commit();
   };
-  uint64_t wg = blockIdx.x * 8ull + warp;
+  uint64_t wg = blockIdx.x * (uint64_t)W + warp;
 #pragma unroll
   for (int k = 0; k < S - 1; ++k) issue(wg + k * wstride, k);
   int slot = 0;
@@ -311,39 +320,43 @@ __global__ void __launch_bounds__(256, NP <= 4 ? 3 : 2)
     __syncwarp();
     const unsigned char* sl = ring + slot * kSlot;
     const float* scs = reinterpret_cast<const float*>(sl + NP * 512) + (lane >> 3);
-    uint32_t sbad = 0;
+    bool fast = true;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       const float sc = scs[p * 4];
       wtab[p * 32 + lane] = fp8_tab_entry_f16(t8, sc);
-      sbad |= bad_scale_bit(sc, p);
+      fast = fast && dq_fast(sc);
     }
     __syncwarp();
     float acc[16];
 #pragma unroll
     for (int e = 0; e < 16; ++e) acc[e] = 0.0f;
+    uint32_t sbad = 0;
+    if (__all_sync(0xffffffffu, fast)) {  // every piece of the warp-group: table decode
 #pragma unroll
-    for (int p = 0; p < NP; ++p) {
-      const uint4 cv = lds128(sl + p * 512 + lane * 16);
-      const uint32_t w[4] = {cv.x, cv.y, cv.z, cv.w};
-      const float sc = scs[p * 4];
-      if (dq_fast(sc))
-        dq_f16_accum<4>(w, mytab + p * 32, acc);
-      else  // zero / extreme block scale: the 256-entry table of exact units
-        dq_accum<16>(w, sc, lut, acc);
+      for (int p = 0; p < NP; ++p) {
+        const uint4 cv = lds128(sl + p * 512 + lane * 16);
+        const uint32_t w[4] = {cv.x, cv.y, cv.z, cv.w};
+        dq_f16_accum<4>(w, mytab + p * 128, acc);
+      }
+    } else {  // a zero / extreme / bad block scale somewhere: per piece
+#pragma unroll 1
+      for (int p = 0; p < NP; ++p) {
+        const uint4 cv = lds128(sl + p * 512 + lane * 16);
+        const uint32_t w[4] = {cv.x, cv.y, cv.z, cv.w};
+        const float sc = scs[p * 4];
+        sbad |= bad_scale_bit(sc, p);
+        if (dq_fast(sc))
+          dq_f16_accum<4>(w, mytab + p * 128, acc);
+        else
+          dq_accum<16>(w, sc, lut, acc);
+      }
     }
     reduce_finish(pt, wg * 512 + lane * 16, len, true, true, (wg * 512 + lane * 16) / kBlock, sbad,
                   acc, blk_base, err);
     slot = slot == S - 1 ? 0 : slot + 1;
   }
   cp_async_wait<0>();
-  __syncwarp();
-  // ragged tail (< 512 elements) in 16-element groups, warp-uniform trip count
-  const uint64_t ngroups = (len + kBlock - 1) / kBlock * 8;
-  const uint64_t gpad = (ngroups + 31) / 32 * 32;
-  for (uint64_t g = nwg * 32 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < gpad;
-       g += gridDim.x * (uint64_t)blockDim.x)
-    reduce_group<NP>(pt, g, g < ngroups ? len : 0, blk_base, lut, err, true, wtab);
 }
 
 // ---------------------------------------------------------------------------
@@ -480,19 +493,20 @@ template <int NP, int S>
 bool launch_reduce_pipe(const PieceTable& pt, uint64_t len, long long bb, agq_errors* err,
                         cudaStream_t s) {
   auto k = k_reduce128_pipe<NP, S>;
-  const size_t smem = (size_t)8 * S * (NP * 512 + NP * 16);
+  constexpr int W = RedCfg<NP>::kWarps;
+  const size_t smem = (size_t)W * S * (NP * 512 + NP * 16);
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess) {
     cudaGetLastError();
     return false;
   }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 256, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, W * 32, smem);
   if (occ < 1) return false;
-  const uint64_t want = (len / 512 + 7) / 8;
+  const uint64_t want = (len / 512 + W - 1) / W;
   const uint64_t cap = (uint64_t)num_sms() * occ;
   const int grid = (int)(want < 1 ? 1 : (want < cap ? want : cap));
-  k<<<grid, 256, smem, s>>>(pt, len, bb, err);
+  k<<<grid, W * 32, smem, s>>>(pt, len, bb, err);
   return true;
 }
 
@@ -500,7 +514,23 @@ template <int NP>
 void launch_reduce128(const PieceTable& pt, uint64_t len, long long bb, int vec, agq_errors* err,
                       cudaStream_t s) {
   if constexpr (NP > 0) {
-    if (vec && len >= 512 && launch_reduce_pipe<NP, kRedStages>(pt, len, bb, err, s)) return;
+    if (vec && len >= 512 && launch_reduce_pipe<NP, kRedStages>(pt, len, bb, err, s)) {
+      const uint64_t done = len / 512 * 512;
+      if (done == len) return;
+      // ragged tail (< 512 elements): the direct-load kernel on the rest
+      PieceTable tp = pt;
+      for (int p = 0; p < pt.np; ++p) {
+        tp.codes[p] += done;
+        tp.scales[p] += done / kBlock;
+      }
+      for (int o = 0; o < pt.nout; ++o) {
+        tp.out_codes[o] += done;
+        tp.out_scales[o] += done / kBlock;
+      }
+      k_reduce128<NP><<<1, 256, 0, s>>>(tp, len - done, bb + (long long)(done / kBlock), 1, err);
+      count_launch();
+      return;
+    }
   }
   const uint64_t groups = (len + kBlock - 1) / kBlock * 8;
   int grid = gen_grid(groups, 256);

@@ -102,6 +102,22 @@ def main():
                 if moved != want_m:
                     fails += 1
                     print(f"rank {rank}: MOVED {moved} != {want_m} algo={algo} n={n}", flush=True)
+    # the NCCL algorithm at other block sizes (receive slots sized per block):
+    # any block >= 1 is valid in the reference (quantize.hpp:64-74)
+    for blk, n in ((32, 70000), (64, 131072 + 77), (1000, 50000)):
+        g = []
+        for r in range(world):
+            rng = np.random.default_rng(7000 + 10 * blk + r)
+            g.append(O.quantize((rng.standard_normal(n) * 1e-2).astype(np.float32), 8, blk, O.FP8))
+        want_c, want_s = O.allreduce_decomposed([c for c, _ in g], [s for _, s in g], block=blk)
+        c, s = g[rank]
+        q = A.QuantizedTensor(torch.from_numpy(c).to(dev), torch.from_numpy(s).to(dev), 8, blk, (n,),
+                              A.CodecKind.Fp8E4M3, packed=False)
+        comm.allreduce_fp8(q, algo="nccl")
+        if not (np.array_equal(q.codes.cpu().numpy(), want_c) and
+                np.array_equal(q.scales.cpu().numpy().view(np.uint32), want_s.view(np.uint32))):
+            fails += 1
+            print(f"rank {rank}: MISMATCH nccl block={blk} n={n}", flush=True)
     # allreduce_naive_fp8 (collective.hpp:338-431) on real ranks: codes,
     # scales and overflow_elements against the oracle; this rank's
     # overflow_events against the one-device simulation.

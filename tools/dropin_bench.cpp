@@ -59,8 +59,17 @@ int main(int argc, char** argv) {
   auto q = agq::quantize_blockwise(x, 4);
   auto back = agq::dequantize_blockwise(q);
   const int reps = 15;
+  double st[4];
+  agq_host_pipeline_stats(st, 1);
   const double tq = median_time([&] { q = agq::quantize_blockwise(x, 4); }, reps);
+  double sq[4];
+  agq_host_pipeline_stats(sq, 1);
   const double td = median_time([&] { back = agq::dequantize_blockwise(q); }, reps);
+  double sd[4];
+  agq_host_pipeline_stats(sd, 1);
+  // what the API's value-initialised result vectors cost on this host alone
+  const double t_alloc_f32 = median_time([&] { std::vector<float> v(n); asm volatile("" ::"r"(v.data()) : "memory"); }, reps);
+  const double t_alloc_u8 = median_time([&] { std::vector<uint8_t> v(n); asm volatile("" ::"r"(v.data()) : "memory"); }, reps);
 
   // FP8 local_accumulate: 2^24-element gradient, FP32 local
   const std::size_t na = 1u << 24;
@@ -109,8 +118,13 @@ int main(int argc, char** argv) {
       "\"accumulate_h2d_bytes\": %.0f, \"accumulate_d2h_bytes\": %.0f, "
       "\"ref_quantize_ms\": %.3f, \"ref_dequantize_ms\": %.3f, \"ref_accumulate_ms\": %.3f, "
       "\"ref_threads\": 1, \"allocator\": \"glibc heap, no mmap/trim (vectors reused, both arms)\", "
+      "\"pipeline_quantize_ms\": {\"inside\": %.3f, \"host_copies\": %.3f, \"wait_device\": %.3f}, "
+      "\"pipeline_dequantize_ms\": {\"inside\": %.3f, \"host_copies\": %.3f, \"wait_device\": %.3f}, "
+      "\"alloc_zero_f32_ms\": %.3f, \"alloc_zero_u8_ms\": %.3f, "
       "\"quantize_bitexact_vs_ref\": %s, \"bitexact_vs_ref\": %s, \"accumulate_bitexact_vs_ref\": %s}\n",
       n, tq * 1e3, td * 1e3, (tq + td) * 1e3, ta * 1e3, q_h2d, q_d2h, d_h2d, d_d2h, a_h2d, a_d2h,
-      rq * 1e3, rd * 1e3, ra * 1e3, same_q ? "true" : "false", same ? "true" : "false", same_acc ? "true" : "false");
+      rq * 1e3, rd * 1e3, ra * 1e3, sq[0] * 1e3 / reps, sq[1] * 1e3 / reps,
+      sq[2] * 1e3 / reps, sd[0] * 1e3 / reps, sd[1] * 1e3 / reps, sd[2] * 1e3 / reps,
+      t_alloc_f32 * 1e3, t_alloc_u8 * 1e3, same_q ? "true" : "false", same ? "true" : "false", same_acc ? "true" : "false");
   return 0;
 }

@@ -732,14 +732,40 @@ def bench_allreduce(dev, args, world, rank, n):
         m = min(chunk, n - off)
         gb[off:off + m] = (torch.randn(m, device=dev, generator=g) * 1e-3).to(torch.bfloat16)
 
-    def bf16():
-        L.check(L.lib.agq_allreduce_bf16_nccl(comm._h, gb.data_ptr(), n, sp))
-    sec = timed(bf16, lambda: None)
+    def bf16_with(c):
+        def run():
+            L.check(L.lib.agq_allreduce_bf16_nccl(c._h, gb.data_ptr(), n, sp))
+        return run
+    sec = timed(bf16_with(comm), lambda: None)
     res["bf16_nccl"] = {"ms": round(sec * 1e3, 3), "bus_GBs": round(fac * 2 * n / sec / 1e9, 1),
-                        "frac_of_nvlink_900": round(fac * 2 * n / sec / 1e9 / NVLINK_GBS, 4)}
+                        "frac_of_nvlink_900": round(fac * 2 * n / sec / 1e9 / NVLINK_GBS, 4),
+                        "nccl_algo": "default (NCCL's tuner)"}
+    best_bf16 = res["bf16_nccl"]["ms"]
+    # the BF16 baseline under each forced NCCL algorithm (NVLS = in-switch
+    # reduction on NVSwitch), on a dedicated communicator created while
+    # NCCL_ALGO is set (NCCL reads it at communicator init)
+    for algo in args.bf16_algos:
+        old = os.environ.get("NCCL_ALGO")
+        os.environ["NCCL_ALGO"] = algo
+        try:
+            c2 = Communicator(device=dev.index)
+        finally:
+            if old is None:
+                os.environ.pop("NCCL_ALGO", None)
+            else:
+                os.environ["NCCL_ALGO"] = old
+        try:
+            sec = timed(bf16_with(c2), lambda: None)
+            res[f"bf16_nccl_{algo}"] = {"ms": round(sec * 1e3, 3),
+                                        "bus_GBs": round(fac * 2 * n / sec / 1e9, 1)}
+            best_bf16 = min(best_bf16, sec * 1e3)
+        except Exception as ex:
+            res[f"bf16_nccl_{algo}"] = {"error": str(ex)[:200]}
+        c2.close()
     done = [res[a]["ms"] for a in args.algos if "ms" in res[a]]
     if done:
         res["speedup_vs_bf16_nccl"] = round(res["bf16_nccl"]["ms"] / min(done), 3)
+        res["speedup_vs_best_bf16_nccl"] = round(best_bf16 / min(done), 3)
     del gb, q
     comm.close()
     torch.cuda.empty_cache()
@@ -969,6 +995,8 @@ def main():
     ap.add_argument("--ar-elements", type=int, default=LLAMA8B_PARAMS)
     ap.add_argument("--acc-elements", type=int, default=LLAMA8B_PARAMS)
     ap.add_argument("--algos", default="nccl,p2p,push")
+    ap.add_argument("--bf16-algos", default="NVLS,Ring",
+                    help="extra BF16 ncclAllReduce baselines with NCCL_ALGO forced (C4)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=16)
     ap.add_argument("--e2e-streams", type=int, default=4)
@@ -979,6 +1007,7 @@ def main():
                     help="C5: all-reduce message-size sweep + LLaMA-32B buckets (N > 1)")
     args = ap.parse_args()
     args.algos = [a for a in args.algos.split(",") if a]
+    args.bf16_algos = [a for a in args.bf16_algos.split(",") if a]
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup(args)
     if args.impl == "reference":

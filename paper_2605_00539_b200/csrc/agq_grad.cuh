@@ -167,19 +167,15 @@ __device__ __forceinline__ void fp8_requant_words(const float (&v)[4 * NW], floa
     const f32x2 ip2 = pk2(ip, ip), im2 = pk2(im, im);
     uint32_t wm[NW];
 #pragma unroll
-    for (int k = 0; k < 2 * NW; ++k) {
-      const f32x2 x = pk2(v[2 * k], v[2 * k + 1]);
-      float p0, p1, m0, m1;
-      up2(mul2(x, ip2), p0, p1);
-      up2(mul2(x, im2), m0, m1);
-      const uint32_t cp = cvt_e4m3x2(p0, p1), cm = cvt_e4m3x2(m0, m1);
-      if (k & 1) {
-        w[k >> 1] |= cp << 16;
-        wm[k >> 1] |= cm << 16;
-      } else {
-        w[k >> 1] = cp;
-        wm[k >> 1] = cm;
-      }
+    for (int k = 0; k < NW; ++k) {
+      // 4 codes per word: two paired conversions, halves joined by one PRMT
+      float p[4], m[4];
+      up2(mul2(pk2(v[4 * k], v[4 * k + 1]), ip2), p[0], p[1]);
+      up2(mul2(pk2(v[4 * k + 2], v[4 * k + 3]), ip2), p[2], p[3]);
+      up2(mul2(pk2(v[4 * k], v[4 * k + 1]), im2), m[0], m[1]);
+      up2(mul2(pk2(v[4 * k + 2], v[4 * k + 3]), im2), m[2], m[3]);
+      w[k] = cvt_e4m3x4(p[0], p[1], p[2], p[3]);
+      wm[k] = cvt_e4m3x4(m[0], m[1], m[2], m[3]);
     }
     // one word-level test; pairs whose brackets split are recomputed exactly
     uint32_t diff = 0;
@@ -223,10 +219,14 @@ __device__ __forceinline__ uint32_t absmax_bits8(const float (&v)[8]) {
   return m;
 }
 
+// |x| bits of the block absmax: the maximum of (bits << 1) (the shift drops
+// the sign; IMAD.SHL on the FMA pipe instead of a LOP3 on the integer ALU)
+// then >> 1. Non-finite values (inf / NaN) compare above every finite one.
 __device__ __forceinline__ uint32_t absmax_bits16(const float (&v)[16]) {
   uint32_t m = 0;
 #pragma unroll
-  for (int e = 0; e < 16; ++e) m = max(m, f2u(v[e]) & 0x7fffffffu);
+  for (int e = 0; e < 16; ++e) m = max(m, f2u(v[e]) * 2u);
+  m >>= 1;
   m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
   m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
   m = max(m, __shfl_xor_sync(0xffffffffu, m, 4));

@@ -205,6 +205,18 @@ AGQ_HD uint32_t fp8_code(float x, float a, float inv448) {
 // for two values; the host emulation is the reference's own RNE on the
 // exactly-converted double (fp8.hpp:32-66 is pure RNE on its argument).
 AGQ_HD uint32_t fp8_encode_double(double v);
+#if defined(__CUDACC__)
+// Four values -> four E4M3 codes in one word (element 0 in the low byte):
+// two paired conversions, the halves joined in the register move.
+__device__ __forceinline__ uint32_t cvt_e4m3x4(float a, float b, float c, float d) {
+  uint32_t r;
+  asm("{\n.reg .b16 lo, hi;\ncvt.rn.satfinite.e4m3x2.f32 lo, %2, %1;\n"
+      "cvt.rn.satfinite.e4m3x2.f32 hi, %4, %3;\nmov.b32 %0, {lo, hi};\n}"
+      : "=r"(r)
+      : "f"(a), "f"(b), "f"(c), "f"(d));
+  return r;
+}
+#endif
 AGQ_HD uint32_t cvt_e4m3x2(float lo, float hi) {
 #if defined(__CUDA_ARCH__)
   uint16_t r;

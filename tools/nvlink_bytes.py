@@ -22,31 +22,33 @@ dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 rank, world = dist.get_rank(), dist.get_world_size()
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 30
 pynvml.nvmlInit()
-h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local)
-try:
-    h = pynvml.nvmlDeviceGetHandleByPciBusId(
-        pynvml.nvmlDeviceGetPciInfo(h).busId)
-except Exception:
-    pass
-LINKS = 18
+h = pynvml.nvmlDeviceGetHandleByIndex(local)  # CUDA and NVML order agree on this box
+# The NVLink data counters (NVML field values) are not exposed on this VM;
+# GPU Performance Monitoring (GPM) is: NVLINK_TOTAL_{TX,RX}_PER_SEC averaged
+# between two samples, times the interval between them = bytes.
+import time  # noqa: E402
+
+_s1 = pynvml.nvmlGpmSampleAlloc()
+_s2 = pynvml.nvmlGpmSampleAlloc()
 
 
-def counters():
-    ids = []
-    for link in range(LINKS):
-        ids.append((pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, link))
-        ids.append((pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, link))
-    vals = pynvml.nvmlDeviceGetFieldValues(h, ids)
-    tx = rx = 0
-    for i, v in enumerate(vals):
-        if v.nvmlReturn != 0:
-            continue
-        x = v.value.ullVal
-        if i % 2 == 0:
-            tx += x
-        else:
-            rx += x
-    return tx * 1024, rx * 1024
+def gpm_begin():
+    pynvml.nvmlGpmSampleGet(h, _s1)
+    return time.perf_counter()
+
+
+def gpm_end(t0):
+    pynvml.nvmlGpmSampleGet(h, _s2)
+    dt = time.perf_counter() - t0
+    mg = pynvml.c_nvmlGpmMetricsGet_t()
+    mg.version = pynvml.NVML_GPM_METRICS_GET_VERSION
+    mg.numMetrics = 2
+    mg.sample1 = _s1
+    mg.sample2 = _s2
+    mg.metrics[0].metricId = pynvml.NVML_GPM_METRIC_NVLINK_TOTAL_TX_PER_SEC
+    mg.metrics[1].metricId = pynvml.NVML_GPM_METRIC_NVLINK_TOTAL_RX_PER_SEC
+    pynvml.nvmlGpmMetricsGet(mg)
+    return mg.metrics[0].value * dt, mg.metrics[1].value * dt, dt
 
 
 comm = Communicator(p2p_capacity=n)
@@ -66,13 +68,13 @@ for algo in ("p2p", "push", "nccl"):
         ps.copy_(src_s)
         torch.cuda.synchronize()
         dist.barrier()
-        t0, r0 = counters()
+        t0 = gpm_begin()
         comm.allreduce_fp8(q, algo=algo)
         torch.cuda.synchronize()
+        tx, rx, _ = gpm_end(t0)
         dist.barrier()
-        t1, r1 = counters()
-        tot_tx += t1 - t0
-        tot_rx += r1 - r0
+        tot_tx += tx
+        tot_rx += rx
     res[algo] = {"tx_bytes_per_call": tot_tx / K, "rx_bytes_per_call": tot_rx / K,
                  "tx_over_expected": round(tot_tx / K / res["expected_fp8_bytes_per_direction"], 4),
                  "rx_over_expected": round(tot_rx / K / res["expected_fp8_bytes_per_direction"], 4)}
@@ -81,13 +83,13 @@ tot_tx = tot_rx = 0
 for _ in range(K):
     torch.cuda.synchronize()
     dist.barrier()
-    t0, r0 = counters()
+    t0 = gpm_begin()
     comm.allreduce_bf16(gb)
     torch.cuda.synchronize()
+    tx, rx, _ = gpm_end(t0)
     dist.barrier()
-    t1, r1 = counters()
-    tot_tx += t1 - t0
-    tot_rx += r1 - r0
+    tot_tx += tx
+    tot_rx += rx
 res["bf16_nccl"] = {"tx_bytes_per_call": tot_tx / K, "rx_bytes_per_call": tot_rx / K,
                     "tx_over_ring_expected": round(tot_tx / K / res["expected_bf16_ring_bytes_per_direction"], 4),
                     "nccl_algo": os.environ.get("NCCL_ALGO", "default")}

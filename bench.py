@@ -515,8 +515,26 @@ def bench_c1(dev, args):
     torch.cuda.synchronize()
     sec = s.elapsed_time(e) * 1e-3 / iters
     nbytes = 2 * n * (2 + 0.5 + 4 / 128)
+    # the practical floor at this size: two back-to-back device copies moving
+    # the same bytes (each kernel of the round trip moves half of nbytes)
+    half = int(nbytes / 4)
+    cx = [torch.empty(half, dtype=torch.uint8, device=dev).fill_(1) for _ in range(R)]
+    cy = [torch.empty(half, dtype=torch.uint8, device=dev) for _ in range(R)]
+    for i in range(R):
+        cy[i].copy_(cx[i])
+    torch.cuda.synchronize()
+    s.record()
+    for i in range(2 * iters):
+        cy[i % R].copy_(cx[i % R])
+    e.record()
+    torch.cuda.synchronize()
+    floor = s.elapsed_time(e) * 1e-3 / iters
+    del cx, cy
     return {"config": "C1 INT4 block-128 quantize+dequantize, 4096x4096 BF16",
-            "us_per_roundtrip": round(sec * 1e6, 2), "GBs": round(nbytes / sec / 1e9, 1)}
+            "us_per_roundtrip": round(sec * 1e6, 2), "GBs": round(nbytes / sec / 1e9, 1),
+            "copy_floor_us": round(floor * 1e6, 2),
+            "copy_floor_note": "two back-to-back torch device copies of nbytes/4 each (same "
+                               "total traffic as the round trip), 16 rotating buffers"}
 
 
 def bench_reduce_local(dev, args, P=8):

@@ -129,7 +129,9 @@ struct agq_comm {
   unsigned char* peer[AGQ_MAX_WORLD] = {};
   bool p2p_ready = false;
   unsigned int* done_counter = nullptr;  // local, one per kernel in flight
-  unsigned long long* stats = nullptr;   // device: [elements, blocks] moved per peer
+  // device: two [elements, blocks] records of the phase-1 traffic, used by
+  // alternate epochs; each kernel zeroes the other one for the next call
+  unsigned long long* stats = nullptr;
   uint64_t epoch = 0;
   // message trace of the last all-reduce issued by this rank
   std::vector<agq_trace_event> trace;
@@ -323,6 +325,10 @@ __device__ __forceinline__ void epoch_end(const Args& a, bool ok) {
     mark_failed(a);
   }
   __threadfence();
+  // the next epoch's traffic record (this one stays readable for last_trace)
+  a.stats[2 * ((a.epoch + 1) & 1)] = 0ull;
+  a.stats[2 * ((a.epoch + 1) & 1) + 1] = 0ull;
+  __threadfence();
   *a.done_counter = 0u;
 }
 
@@ -393,8 +399,8 @@ __global__ void __launch_bounds__(256, 2) k_fused_allreduce(FusedArgs a) {
     n_blk += __shfl_xor_sync(0xffffffffu, n_blk, o);
   }
   if ((tid & 31) == 0 && n_el) {  // read from each of the P - 1 peers
-    atomicAdd(&a.stats[0], n_el * (a.P - 1));
-    atomicAdd(&a.stats[1], n_blk * (a.P - 1));
+    atomicAdd(&a.stats[2 * (a.epoch & 1)], n_el * (a.P - 1));
+    atomicAdd(&a.stats[2 * (a.epoch & 1) + 1], n_blk * (a.P - 1));
   }
   epoch_end(a, true);
 }
@@ -462,8 +468,8 @@ __global__ void __launch_bounds__(256) k_push_scatter(PushArgs a) {
     n_blk += __shfl_xor_sync(0xffffffffu, n_blk, o);
   }
   if ((threadIdx.x & 31) == 0 && (n_el | n_blk)) {
-    atomicAdd(&a.stats[0], n_el);
-    atomicAdd(&a.stats[1], n_blk);
+    atomicAdd(&a.stats[2 * (a.epoch & 1)], n_el);
+    atomicAdd(&a.stats[2 * (a.epoch & 1) + 1], n_blk);
   }
   // publish "scattered" once every CTA's stores are performed system-wide
   __threadfence_system();
@@ -563,7 +569,8 @@ agq_status comm_init(agq_comm** out, const unsigned char id[128], int nranks, in
   }
   e = cudaMalloc(&c->done_counter, 64);
   if (e == cudaSuccess) e = cudaMemset(c->done_counter, 0, 64);
-  if (e == cudaSuccess) e = cudaMalloc(&c->stats, 2 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMalloc(&c->stats, 4 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(c->stats, 0, 4 * sizeof(unsigned long long));
   if (e != cudaSuccess) {
     comm_destroy(c);
     return cuda_fail(e, "comm_init: counters");
@@ -969,8 +976,6 @@ agq_status allreduce_fp8(agq_comm* c, uint8_t* codes, float* scales, uint64_t n,
     return reduce_requant_device(1, &pc, &ps, n, block, 1, &codes, &scales, 0, err, s);
   }
   if (algo == AGQ_AR_FUSED_P2P || algo == AGQ_AR_PUSH_P2P) {
-    cudaError_t e = cudaMemsetAsync(c->stats, 0, 2 * sizeof(unsigned long long), s);
-    if (e != cudaSuccess) return cuda_fail(e, "all-reduce: stats");
     // one rank: the fused kernel (barriers and reduce with itself); the
     // push algorithm has no peer to scatter to
     return algo == AGQ_AR_FUSED_P2P || c->nranks == 1
@@ -989,7 +994,8 @@ agq_status comm_last_trace(agq_comm* c, agq_trace_event* events, int cap, int* c
     if (c->trace_algo == AGQ_AR_FUSED_P2P || c->trace_algo == AGQ_AR_PUSH_P2P) {
       // kernel-side counters of the last P2P call (elements, blocks)
       if (c->trace_stream) cudaStreamSynchronize(c->trace_stream);
-      cudaError_t e = cudaMemcpy(moved, c->stats, 2 * sizeof(unsigned long long),
+      cudaError_t e = cudaMemcpy(moved, c->stats + 2 * (c->epoch & 1),
+                                 2 * sizeof(unsigned long long),
                                  cudaMemcpyDeviceToHost);
       if (e != cudaSuccess) return cuda_fail(e, "last_trace: counters");
     }

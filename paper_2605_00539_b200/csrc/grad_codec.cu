@@ -88,27 +88,40 @@ __global__ void __launch_bounds__(kAccWarps * 32, 3)
   uint64_t t = (uint64_t)blockIdx.x * kAccWarps + warp;
   const unsigned char* lbase = static_cast<const unsigned char*>(local);
 
-  uint4 pc;       // 16 codes
-  float ps;       // block scale
-  uint4 pl[kCh];  // local gradient chunks (coalesced layout)
-  auto load = [&](uint64_t tt) {
-    pc = ldg128_stream(codes + tt * kAccWarpElems + lane * 16);
-    ps = __ldg(scales + tt * 4 + (lane >> 3));
+  // Tiles in flight per warp: a BF16-local tile is 1.5 KB, so two are kept
+  // in flight to cover the memory latency (24 warps x 2 x 1.5 KB per SM);
+  // an FP32-local tile (2.5 KB) needs one.
+  constexpr int kPf = 1;
+  uint4 pc[kPf];       // 16 codes
+  float ps[kPf];       // block scale
+  uint4 pl[kPf][kCh];  // local gradient chunks (coalesced layout)
+  auto load = [&](uint64_t tt, int d) {
+    pc[d] = ldg128_stream(codes + tt * kAccWarpElems + lane * 16);
+    ps[d] = __ldg(scales + tt * 4 + (lane >> 3));
 #pragma unroll
-    for (int j = 0; j < kCh; ++j) pl[j] = ldg128_stream(lbase + tt * kLocTileB + j * 512 + lane * 16);
+    for (int j = 0; j < kCh; ++j) pl[d][j] = ldg128_stream(lbase + tt * kLocTileB + j * 512 + lane * 16);
   };
-  if (t < ntiles) load(t);
+#pragma unroll
+  for (int d = 0; d < kPf; ++d)
+    if (t + d * nw < ntiles) load(t + d * nw, d);
   for (; t < ntiles; t += nw) {
 #pragma unroll
     for (int j = 0; j < kCh; ++j) {
       const uint32_t o = j * 512 + lane * 16;
-      sts128(wb + acc_swz<kCh>(o / kRowB, (o / 16) & (kCh - 1)), pl[j]);
+      sts128(wb + acc_swz<kCh>(o / kRowB, (o / 16) & (kCh - 1)), pl[0][j]);
     }
-    const uint32_t cw[4] = {pc.x, pc.y, pc.z, pc.w};
-    const float sc = ps;
+    const uint32_t cw[4] = {pc[0].x, pc[0].y, pc[0].z, pc[0].w};
+    const float sc = ps[0];
     btab[warp][lane] = fp8_tab_entry_f16(t8, sc);  // T[M] (dq_f16_accum)
     __syncwarp();
-    if (t + nw < ntiles) load(t + nw);
+#pragma unroll
+    for (int d = 0; d + 1 < kPf; ++d) {  // shift the queue (register renames)
+      pc[d] = pc[d + 1];
+      ps[d] = ps[d + 1];
+#pragma unroll
+      for (int j = 0; j < kCh; ++j) pl[d][j] = pl[d + 1][j];
+    }
+    if (t + kPf * nw < ntiles) load(t + kPf * nw, kPf - 1);
     float l[16];
 #pragma unroll
     for (int j = 0; j < kCh; ++j) {

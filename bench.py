@@ -515,6 +515,20 @@ def bench_c1(dev, args):
     torch.cuda.synchronize()
     sec = s.elapsed_time(e) * 1e-3 / iters
     nbytes = 2 * n * (2 + 0.5 + 4 / 128)
+
+    def fused(i):  # the same round trip through the fused entry point
+        L.check(L.lib.agq_quantize_roundtrip(xs[i].data_ptr(), L.AGQ_BF16, n, 4, 128, 0,
+                                             cs[i].data_ptr(), L.AGQ_CODES_PACKED, ss[i].data_ptr(),
+                                             ys[i].data_ptr(), L.AGQ_BF16, None, sp))
+    for i in range(R):
+        fused(i)
+    torch.cuda.synchronize()
+    s.record()
+    for i in range(iters):
+        fused(i % R)
+    e.record()
+    torch.cuda.synchronize()
+    fsec = s.elapsed_time(e) * 1e-3 / iters
     # the practical floor at this size: two back-to-back device copies moving
     # the same bytes (each kernel of the round trip moves half of nbytes)
     half = int(nbytes / 4)
@@ -533,6 +547,10 @@ def bench_c1(dev, args):
     return {"config": "C1 INT4 block-128 quantize+dequantize, 4096x4096 BF16",
             "us_per_roundtrip": round(sec * 1e6, 2), "GBs": round(nbytes / sec / 1e9, 1),
             "copy_floor_us": round(floor * 1e6, 2),
+            "fused_roundtrip_us": round(fsec * 1e6, 2),
+            "fused_roundtrip_GBs_moved": round(n * (2 + 0.5 + 4 / 128 + 2) / fsec / 1e9, 1),
+            "fused_note": "agq_quantize_roundtrip: one kernel pass (x read once, codes + scales + "
+                          "reconstruction written), bit-identical to the two calls",
             "copy_floor_note": "two back-to-back torch device copies of nbytes/4 each (same "
                                "total traffic as the round trip), 16 rotating buffers"}
 

@@ -111,6 +111,16 @@ agq_status agq_dequantize(const void* codes, int layout, const float* scales,
                           void* out, int out_dtype, int validate,
                           agq_errors* d_err, agq_stream_t stream);
 
+/* quantize + the reconstruction dequantize_blockwise gives for its codes in
+ * one call (quantize.hpp:193-196 roundtrip_relative_delta; the C1 round
+ * trip). SymmetricLinear BF16 in / out with block 128 and packed codes runs
+ * as ONE kernel pass (x read once); everything else as quantize followed by
+ * dequantize. Outputs are bit-identical to those two calls. */
+agq_status agq_quantize_roundtrip(const void* x, int x_dtype, uint64_t n, int bits,
+                                  uint32_t block, int codec, void* codes, int layout,
+                                  float* scales, void* out, int out_dtype,
+                                  agq_errors* d_err, agq_stream_t stream);
+
 /* One stored tensor of a layer (layers.hpp:148-163 SavedEntry::quantized):
  * block 128, SymmetricLinear unless codec says otherwise. */
 typedef struct {
@@ -281,6 +291,10 @@ agq_status agq_quantize_host(const float* x, uint64_t n, int bits,
 agq_status agq_dequantize_host(const uint8_t* codes, const float* scales,
                                uint64_t n, int bits, uint32_t block, int codec,
                                float* out);
+/* quantize then dequantize of host FP32 values, the codes kept on the device
+ * (quantize.hpp:193-196 roundtrip_relative_delta's reconstruction). */
+agq_status agq_roundtrip_host(const float* x, uint64_t n, int bits, uint32_t block,
+                              int codec, float* out);
 agq_status agq_local_accumulate_host(const uint8_t* codes, const float* scales,
                                      uint64_t n, uint32_t block,
                                      const float* local, int precision,

@@ -11,7 +11,8 @@ from . import _lib
 from ._lib import CudaError, InvalidArgument, ProtocolError
 from .codec import (CodecKind, ErrorRecord, QuantizedTensor, check_codec_args,
                     code_unit_value, dequantize_blockwise, dequantize_grouped, kDefaultBlockSize,
-                    pack_codes, quantize_blockwise, quantize_grouped, roundtrip_relative_delta,
+                    pack_codes, quantize_blockwise, quantize_grouped, quantize_roundtrip,
+                    roundtrip_relative_delta,
                     unpack_codes, validate)
 from .gradient import (AccumulatePrecision, ChunkAssignment, TraceEvent, allreduce_naive_simulated,
                        allreduce_simulated, decomposed_trace, local_accumulate, naive_trace,

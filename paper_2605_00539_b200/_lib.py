@@ -79,6 +79,8 @@ def _load() -> C.CDLL:
         "agq_quantize": (I, [P, I, U64, I, U32, I, P, I, P, P, S]),
         "agq_dequantize": (I, [P, I, P, U64, I, U32, I, P, I, I, P, S]),
         "agq_quantize_grouped": (I, [C.POINTER(AgqSegment), I, I, I, I, P, S]),
+        "agq_quantize_roundtrip": (I, [P, I, U64, I, U32, I, P, I, P, P, I, P, S]),
+        "agq_roundtrip_host": (I, [P, U64, I, U32, I, P]),
         "agq_dequantize_grouped": (I, [C.POINTER(AgqSegment), I, I, I, I, I, P, S]),
         "agq_pack_codes": (I, [P, U64, I, P, S]),
         "agq_unpack_codes": (I, [P, U64, I, P, S]),
@@ -129,7 +131,8 @@ lib = _load()
 EXPORTED = (
     "agq_version agq_last_error agq_device_ok agq_launch_count agq_errors_reset "
     "agq_errors_message agq_num_blocks agq_packed_bytes agq_check_codec_args agq_quantize "
-    "agq_dequantize agq_quantize_grouped agq_dequantize_grouped agq_pack_codes agq_unpack_codes "
+    "agq_dequantize agq_quantize_roundtrip agq_quantize_grouped agq_dequantize_grouped "
+    "agq_pack_codes agq_unpack_codes agq_roundtrip_host "
     "agq_fp8_accumulate agq_fp8_reduce_requant agq_chunk_assignment agq_allreduce_simulated "
     "agq_allreduce_naive_simulated agq_comm_unique_id agq_comm_init agq_comm_p2p_export "
     "agq_comm_p2p_open agq_comm_p2p_buffers agq_comm_destroy agq_comm_rank agq_comm_size "

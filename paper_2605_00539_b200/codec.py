@@ -307,11 +307,39 @@ def dequantize_grouped(qs: Sequence[QuantizedTensor], out_dtype: torch.dtype = t
     return res
 
 
+def quantize_roundtrip(x: torch.Tensor, bit_width: int, block_size: int = kDefaultBlockSize,
+                       kind: CodecKind = CodecKind.SymmetricLinear, out_dtype=None, stream=None,
+                       check: bool = True, errors: ErrorRecord | None = None):
+    """quantize_blockwise + dequantize_blockwise of its result in one call
+    (the round trip of quantize.hpp:193-196): (QuantizedTensor, reconstruction).
+    SymmetricLinear BF16 in/out at block 128 is one fused kernel pass (x read
+    once); bit-identical to the two calls."""
+    check_codec_args(bit_width, block_size, kind)
+    _require_cuda(x, "x")
+    n = x.numel()
+    out_dtype = out_dtype or x.dtype
+    codes = torch.empty(int(L.lib.agq_packed_bytes(n, bit_width)), dtype=torch.uint8, device=x.device)
+    scales = torch.empty(int(L.lib.agq_num_blocks(n, block_size)), dtype=torch.float32,
+                         device=x.device)
+    y = torch.empty(x.shape, dtype=out_dtype, device=x.device)
+    err = errors if errors is not None else (ErrorRecord(x.device) if check else None)
+    if err is not None:
+        err.reset(stream)
+    L.check(L.lib.agq_quantize_roundtrip(x.data_ptr(), _dtype_code(x), n, bit_width, block_size,
+                                         int(kind), codes.data_ptr(), L.AGQ_CODES_PACKED,
+                                         scales.data_ptr(), y.data_ptr(), _dtype_code(y),
+                                         err.ptr if err is not None else None, _stream(stream)))
+    if check and err is not None:
+        err.raise_if_any(L.AGQ_OP_QUANTIZE)
+    q = QuantizedTensor(codes, scales, bit_width, block_size, (n,), CodecKind(kind), True)
+    return q, y
+
+
 def roundtrip_relative_delta(x: torch.Tensor, bit_width: int, block_size: int = kDefaultBlockSize,
                              kind: CodecKind = CodecKind.SymmetricLinear) -> torch.Tensor:
     """quantize.hpp:193-206: x_hat = x (1 + delta); zero elements get 0."""
-    q = quantize_blockwise(x, bit_width, block_size, kind)
-    back = dequantize_blockwise(q).reshape(-1).double()
+    _, y = quantize_roundtrip(x, bit_width, block_size, kind, out_dtype=torch.float32)
+    back = y.reshape(-1).double()
     xd = x.reshape(-1).double()
     delta = torch.where(xd == 0, torch.zeros_like(xd), (back - xd) / xd)
     return delta

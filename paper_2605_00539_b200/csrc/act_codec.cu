@@ -279,7 +279,8 @@ __device__ __forceinline__ void encode_row(const uint4 (&ch)[InTraits<Tin>::kChu
 // packed codes straight to HBM, one scale per 4 lanes.
 template <int BITS, int PACK, int CODEC, typename Tin>
 __device__ __forceinline__ void quant_tile(const SegTable& st, agq_errors* err, const TileRef& tr,
-                                           int lane, const uint4 (&ch)[InTraits<Tin>::kChunks]) {
+                                           int lane, const uint4 (&ch)[InTraits<Tin>::kChunks],
+                                           uint32_t (&words)[PACK], float& a) {
   using TR = InTraits<Tin>;
   constexpr int kChunks = TR::kChunks;
   constexpr uint32_t kCodeB = kWarpElems * PACK / 8;
@@ -306,10 +307,9 @@ __device__ __forceinline__ void quant_tile(const SegTable& st, agq_errors* err, 
   }
   m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
   m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
-  const float a = u2f(m);
+  a = u2f(m);
   if (m >= 0x7f800000u && (lane & 3) == 0)
     err_min(&err->nonfinite_block, (long long)(st.block_base[tr.g] + tr.lt * 8 + (lane >> 2)));
-  uint32_t words[PACK];
   encode_row<BITS, PACK, CODEC, Tin>(ch, a, m == 0, fast_scale(a), words);
   uint32_t* cdst = reinterpret_cast<uint32_t*>(static_cast<unsigned char*>(st.codes[tr.g]) +
                                                tr.lt * kCodeB) + lane * PACK;
@@ -378,7 +378,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32,
     for (int j = 0; j < kChunks; ++j) ch[j] = lds128(wb + swz_off<kChunks>(lane, j));
     __syncwarp();
 
-    quant_tile<BITS, PACK, CODEC, Tin>(st, err, tr, lane, ch);
+    uint32_t words[PACK];
+    float a;
+    quant_tile<BITS, PACK, CODEC, Tin>(st, err, tr, lane, ch, words, a);
   }
 }
 
@@ -660,6 +662,94 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? kDequan
         o = make_uint4(f2u(v[0]), f2u(v[1]), f2u(v[2]), f2u(v[3]));
       }
       sts128(wb + swz_off<kChunks>(lane, j), o);
+    }
+    __syncwarp();
+    unsigned char* dst = static_cast<unsigned char*>(st.dst[tr.g]) + tr.lt * kTileB;
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j)
+      *reinterpret_cast<uint4*>(dst + j * 512 + lane * 16) =
+          lds128(wb + swz_of_linear<kChunks>(j * 512 + lane * 16));
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1+K2 fused round trip (SymmetricLinear, BF16 in / out, packed codes): the
+// quantize pass also writes the reconstruction dequantize_blockwise would
+// give for its codes (quantize.hpp:193-196 roundtrip_relative_delta; the
+// C1 config), straight from the lane's code words in registers. One read of
+// x, codes + scales + reconstruction written: 2 + b/8 + 4/128 + 2 bytes per
+// element instead of the two calls' 2 * (2 + b/8 + 4/128). Bit-identical to
+// k_quant_warp followed by k_dequant_warp (same encode, same decode).
+// ---------------------------------------------------------------------------
+__device__ __noinline__ float dequant_linear_slow(int bits, uint32_t c, float s) {
+  return dequant_double(0, bits, c, s);
+}
+
+#ifndef AGQ_RT_MINB
+#define AGQ_RT_MINB 2
+#endif
+template <int BITS>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, AGQ_RT_MINB)
+    k_roundtrip_warp(SegTable st, agq_errors* err) {
+  pdl_launch_dependents();
+  pdl_wait();
+  using Tin = __nv_bfloat16;
+  constexpr int kChunks = 4;
+  constexpr uint32_t kTileB = kWarpElems * 2;
+  __shared__ __align__(16) unsigned char sbuf[kWarpsPerCta][kTileB];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wb = sbuf[warp];
+  const uint64_t total = st.tile_begin[st.nseg];
+  const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
+  uint64_t t = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
+  auto load = [&](TileRef tr, uint4 (&buf)[kChunks]) {
+    const unsigned char* src = static_cast<const unsigned char*>(st.src[tr.g]) + tr.lt * kTileB;
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) buf[j] = ldg128_stream(src + j * 512 + lane * 16);
+  };
+  uint4 buf[kChunks];
+  TileRef nxt{0, 0};
+  SegCursor gseg;
+  if (t < total) {
+    nxt = locate_from(st, t, gseg);
+    load(nxt, buf);
+  }
+  for (; t < total; t += nw) {
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) sts128(wb + swz_of_linear<kChunks>(j * 512 + lane * 16), buf[j]);
+    __syncwarp();
+    const TileRef tr = nxt;
+    if (t + nw < total) {
+      nxt = locate_from(st, t + nw, gseg);
+      load(nxt, buf);
+    }
+    uint4 ch[kChunks];
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) ch[j] = lds128(wb + swz_off<kChunks>(lane, j));
+    __syncwarp();
+    uint32_t words[BITS];
+    float a;
+    quant_tile<BITS, BITS, 0, Tin>(st, err, tr, lane, ch, words, a);
+    // the reconstruction of this lane's 32 codes, staged for coalesced stores
+    const bool fast = fast_scale(a);  // a is BF16-valued (absmax of BF16 values)
+#pragma unroll
+    for (int j = 0; j < kChunks; ++j) {
+      float v[8];
+      if (fast) {
+        decode_linear_words<BITS, BITS, 8>(words, j * 8, a, v);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          v[e] = dequant_linear_slow(BITS, (code_at<BITS>(words, j * 8 + e)) & ((1u << BITS) - 1u), a);
+      }
+      uint32_t h[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+        h[k] = *reinterpret_cast<uint32_t*>(&b2);
+      }
+      sts128(wb + swz_off<kChunks>(lane, j), make_uint4(h[0], h[1], h[2], h[3]));
     }
     __syncwarp();
     unsigned char* dst = static_cast<unsigned char*>(st.dst[tr.g]) + tr.lt * kTileB;
@@ -1106,6 +1196,59 @@ agq_status dequantize_device_at(const void* codes, int layout, const float* scal
                                 cudaStream_t s) {
   return dequantize_one(codes, layout, scales, n, bits, block, codec, out, out_dtype, validate,
                         blk_base, err, s);
+}
+
+// quantize + the reconstruction (the round trip) in one pass where the fast
+// kernel applies (SymmetricLinear, BF16 in / out, block 128, packed, aligned
+// whole warp tiles); the rest as quantize followed by dequantize.
+agq_status roundtrip_device(const void* x, int x_dtype, uint64_t n, int bits, uint32_t block,
+                            int codec, void* codes, int layout, float* scales, void* out,
+                            int out_dtype, agq_errors* err, cudaStream_t s) {
+  if (n == 0) return AGQ_OK;
+  uint64_t ntiles = 0;
+  if (x_dtype == AGQ_BF16 && out_dtype == AGQ_BF16 && codec == AGQ_CODEC_SYMMETRIC_LINEAR &&
+      layout == AGQ_CODES_PACKED && block == (uint32_t)kBlock && aligned16(x) && aligned16(codes) &&
+      aligned16(scales) && aligned16(out))
+    ntiles = n / (uint64_t)kWarpElems;
+  if (ntiles > 0) {
+    SegTable st{};
+    st.src[0] = x;
+    st.codes[0] = codes;
+    st.scales[0] = scales;
+    st.dst[0] = out;
+    st.tile_begin[1] = ntiles;
+    st.nseg = 1;
+    cudaError_t e = cudaSuccess;
+    auto go = [&](auto kern) {
+      static const int occ = occupancy_of(kern, kWarpsPerCta * 32, 0);
+      const uint64_t want = (ntiles + kWarpsPerCta - 1) / kWarpsPerCta;
+      const uint64_t cap = (uint64_t)num_sms() * occ;
+      e = launch_pdl(kern, (int)(want < cap ? want : cap), kWarpsPerCta * 32, 0, s, st, err);
+    };
+    switch (bits) {
+      case 4: go(k_roundtrip_warp<4>); break;
+      case 5: go(k_roundtrip_warp<5>); break;
+      case 6: go(k_roundtrip_warp<6>); break;
+      case 7: go(k_roundtrip_warp<7>); break;
+      default: go(k_roundtrip_warp<8>); break;
+    }
+    count_launch();
+    if (agq_status r = cuda_fail(e != cudaSuccess ? e : cudaGetLastError(), "roundtrip: launch"))
+      return r;
+  }
+  const uint64_t done = ntiles * (uint64_t)kWarpElems;
+  if (done == n) return AGQ_OK;
+  const int pack = layout == AGQ_CODES_PACKED ? bits : 8;
+  const size_t ei = x_dtype == AGQ_BF16 ? 2 : 4, eo = out_dtype == AGQ_BF16 ? 2 : 4;
+  const void* xr = static_cast<const char*>(x) + done * ei;
+  void* cr = static_cast<uint8_t*>(codes) + done * pack / 8;
+  float* sr = scales + done / block;
+  void* orr = static_cast<char*>(out) + done * eo;
+  const long long bb = (long long)(done / block);
+  if (agq_status r = quantize_one(xr, x_dtype, n - done, bits, block, codec, cr, layout, sr, bb, err, s))
+    return r;
+  return dequantize_one(cr, layout, sr, n - done, bits, block, codec, orr, out_dtype, 0, bb, err,
+                        s);
 }
 
 agq_status quantize_grouped_device(const agq_segment* segs, int nseg, int x_dtype, int bits,

@@ -30,6 +30,9 @@ agq_status dequantize_device(const void* codes, int layout, const float* scales,
                              int validate, agq_errors* err, cudaStream_t s);
 agq_status quantize_grouped_device(const agq_segment* segs, int nseg, int x_dtype, int bits,
                                    int codec, agq_errors* err, cudaStream_t s);
+agq_status roundtrip_device(const void* x, int x_dtype, uint64_t n, int bits, uint32_t block,
+                            int codec, void* codes, int layout, float* scales, void* out,
+                            int out_dtype, agq_errors* err, cudaStream_t s);
 agq_status dequantize_grouped_device(const agq_segment* segs, int nseg, int out_dtype, int bits,
                                      int codec, int validate, agq_errors* err, cudaStream_t s);
 agq_status pack_device(const uint8_t* codes, uint64_t n, int bits, uint8_t* packed,
@@ -280,6 +283,16 @@ agq_status agq_dequantize(const void* codes, int layout, const float* scales, ui
     return set_error(AGQ_ERR_INVALID_ARGUMENT, "validate needs an error record");
   return dequantize_device(codes, layout, scales, n, bits, block, codec, out, out_dtype,
                            validate, d_err, (cudaStream_t)stream);
+}
+
+agq_status agq_quantize_roundtrip(const void* x, int x_dtype, uint64_t n, int bits,
+                                  uint32_t block, int codec, void* codes, int layout,
+                                  float* scales, void* out, int out_dtype, agq_errors* d_err,
+                                  agq_stream_t stream) {
+  if (agq_status st = check_args(bits, block, codec)) return st;
+  if (agq_status st = check_device()) return st;
+  return roundtrip_device(x, x_dtype, n, bits, block, codec, codes, layout, scales, out, out_dtype,
+                          d_err, (cudaStream_t)stream);
 }
 
 agq_status agq_quantize_grouped(const agq_segment* segs, int nseg, int x_dtype, int bits,
@@ -750,6 +763,39 @@ agq_status agq_dequantize_host(const uint8_t* codes, const float* scales, uint64
       });
   if (st) return st;
   return read_errors(p, AGQ_OP_DEQUANTIZE);
+}
+
+agq_status agq_roundtrip_host(const float* x, uint64_t n, int bits, uint32_t block, int codec,
+                              float* out) {
+  if (agq_status st = check_args(bits, block, codec)) return st;
+  if (agq_status st = check_device()) return st;
+  if (n == 0) return AGQ_OK;
+  const uint64_t ce = chunk_elems(n, block), K = (n + ce - 1) / ce;
+  // [x | reconstruction | codes | scales]: the codes never cross PCIe
+  const size_t oo = al(ce * 4), oc = oo + al(ce * 4), os = oc + al(ce);
+  const size_t slot = os + al((ce / block + 1) * 4);
+  PipeLease lease;
+  HostPipe& p = *lease.p;
+  agq_status st = run_pipeline(
+      p, K, slot,
+      [&](uint64_t k, std::vector<Part>& in, std::vector<Part>& o) {
+        const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
+        in.push_back({0, len * 4, (char*)(x + e0)});
+        o.push_back({oo, len * 4, (char*)(out + e0)});
+      },
+      [&](uint64_t k, char* d, cudaStream_t s) {
+        const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
+        // quantize with the chunk's global block indices for the errors
+        if (agq_status r = quantize_device_at(d, AGQ_F32, len, bits, block, codec, d + oc,
+                                              AGQ_CODES_BYTES, reinterpret_cast<float*>(d + os),
+                                              (long long)(e0 / block), p.d_err, s))
+          return r;
+        return dequantize_device_at(d + oc, AGQ_CODES_BYTES, reinterpret_cast<float*>(d + os), len,
+                                    bits, block, codec, d + oo, AGQ_F32, 0,
+                                    (long long)(e0 / block), p.d_err, s);
+      });
+  if (st) return st;
+  return read_errors(p, AGQ_OP_QUANTIZE);
 }
 
 agq_status agq_local_accumulate_host(const uint8_t* codes, const float* scales, uint64_t n,

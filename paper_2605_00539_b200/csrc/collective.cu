@@ -284,14 +284,21 @@ __device__ __forceinline__ void fused_group(unsigned char* const (&base)[NP], ui
 // rank, publishes "done" to every rank and waits for all of them, so the
 // kernel completes only when every rank has finished writing into (and
 // reading from) this rank's buffer; then it merges the peers' errors.
+// cta_stats (shared, or nullptr): this CTA's [elements, blocks] moved per
+// peer, added to the communicator's counters once per CTA.
 template <class Args>
-__device__ __forceinline__ void epoch_end(const Args& a, bool ok) {
+__device__ __forceinline__ void epoch_end(const Args& a, bool ok,
+                                          const unsigned long long* cta_stats = nullptr) {
   unsigned char* const* base = a.base;
   const int P = a.P, rank = a.rank;
   agq_errors* err = a.err;
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x != 0) return;
+  if (cta_stats != nullptr && cta_stats[0] != 0) {  // read from each of the P - 1 peers
+    atomicAdd(&a.stats[2 * (a.epoch & 1)], cta_stats[0] * (a.P - 1));
+    atomicAdd(&a.stats[2 * (a.epoch & 1) + 1], cta_stats[1] * (a.P - 1));
+  }
   const unsigned int prev = atomicAdd(a.done_counter, 1u);
   if (prev != gridDim.x * gridDim.y - 1) return;
   __threadfence_system();
@@ -337,9 +344,11 @@ __global__ void __launch_bounds__(256, 2) k_fused_allreduce(FusedArgs a) {
   __shared__ double lut[kDqTable];
   __shared__ float btab[8 * (NP > 0 ? NP : 1) * 32];  // 8 warps x NP pieces x 32 entries
   __shared__ int ok;
+  __shared__ unsigned long long cta_stats[2];
   fill_fp8_dq_table(lut);
   float* wtab = btab + (threadIdx.x >> 5) * (NP > 0 ? NP : 1) * 32;
   const int tid = threadIdx.x;
+  if (tid < 2) cta_stats[tid] = 0ull;
   // start barrier: announce "my input is final" to every rank, then wait for
   // every rank's announcement (each CTA waits; only CTA 0 announces).
   if (blockIdx.x == 0 && tid < a.P)
@@ -398,11 +407,11 @@ __global__ void __launch_bounds__(256, 2) k_fused_allreduce(FusedArgs a) {
     n_el += __shfl_xor_sync(0xffffffffu, n_el, o);
     n_blk += __shfl_xor_sync(0xffffffffu, n_blk, o);
   }
-  if ((tid & 31) == 0 && n_el) {  // read from each of the P - 1 peers
-    atomicAdd(&a.stats[2 * (a.epoch & 1)], n_el * (a.P - 1));
-    atomicAdd(&a.stats[2 * (a.epoch & 1) + 1], n_blk * (a.P - 1));
+  if ((tid & 31) == 0 && n_el) {
+    atomicAdd(&cta_stats[0], n_el);
+    atomicAdd(&cta_stats[1], n_blk);
   }
-  epoch_end(a, true);
+  epoch_end(a, true, cta_stats);
 }
 
 // ---------------------------------------------------------------------------

@@ -149,6 +149,11 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -190,7 +195,8 @@ __device__ void mark_failed(const Args& a) {
 template <class Args>
 __device__ bool start_barrier(const Args& a, int wait_off, bool skip_self) {
   uint64_t* my_flags = reinterpret_cast<uint64_t*>(a.base[a.rank]);
-  if (ld_acquire_sys(my_flags + kFailOff) != 0) return false;
+  // set by an earlier call (a previous kernel): a relaxed load suffices
+  if (ld_relaxed_sys(my_flags + kFailOff) != 0) return false;
   bool ok = true;
   for (int s = 0; s < a.P; ++s)
     if (!(skip_self && s == a.rank) &&
@@ -335,8 +341,7 @@ __device__ __forceinline__ void epoch_end(const Args& a, bool ok,
   // the next epoch's traffic record (this one stays readable for last_trace)
   a.stats[2 * ((a.epoch + 1) & 1)] = 0ull;
   a.stats[2 * ((a.epoch + 1) & 1) + 1] = 0ull;
-  __threadfence();
-  *a.done_counter = 0u;
+  *a.done_counter = 0u;  // read by the next kernel on this stream
 }
 
 template <int NP>

@@ -473,6 +473,14 @@ def bench_dropin(dev):
            "frac_of_pinned_pcie_bound": round((bq + bd) / rt, 3),
            # the metric's algorithmic bytes for FP32 in/out, b = 4
            "GBs_algorithmic": round(2 * n * (4 + 0.5 + 4 / 128) / rt / 1e9, 2),
+           "abi_host_entry_ms": {"quantize": j["abi_quantize_host_ms"],
+                                 "dequantize": j["abi_dequantize_host_ms"],
+                                 "frac_of_pinned_pcie_bound": round(
+                                     (bq + bd) / ((j["abi_quantize_host_ms"] +
+                                                   j["abi_dequantize_host_ms"]) * 1e-3), 3),
+                                 "note": "agq_*_host into caller-owned buffers: the library's "
+                                         "path without the API's value-initialised result "
+                                         "vectors"},
            "accumulate_ms": j["accumulate_ms"],
            "accumulate_frac_of_pinned_pcie_bound": round(ba / (j["accumulate_ms"] * 1e-3), 3),
            "reference_1thread": {"roundtrip_ms": round(j["ref_quantize_ms"] + j["ref_dequantize_ms"], 2),

@@ -67,6 +67,16 @@ int main(int argc, char** argv) {
   const double td = median_time([&] { back = agq::dequantize_blockwise(q); }, reps);
   double sd[4];
   agq_host_pipeline_stats(sd, 1);
+  // the C-ABI host entry points into caller-owned (warm) buffers: the
+  // library's path without the API's result-vector construction
+  std::vector<uint8_t> pc(n);
+  std::vector<float> pscales(n / 128), pout(n);
+  const double tq_abi = median_time([&] {
+    agq_quantize_host(x.data(), n, 4, 128, 0, pc.data(), pscales.data());
+  }, reps);
+  const double td_abi = median_time([&] {
+    agq_dequantize_host(pc.data(), pscales.data(), n, 4, 128, 0, pout.data());
+  }, reps);
   // what the API's value-initialised result vectors cost on this host alone
   const double t_alloc_f32 = median_time([&] { std::vector<float> v(n); asm volatile("" ::"r"(v.data()) : "memory"); }, reps);
   const double t_alloc_u8 = median_time([&] { std::vector<uint8_t> v(n); asm volatile("" ::"r"(v.data()) : "memory"); }, reps);
@@ -121,10 +131,11 @@ int main(int argc, char** argv) {
       "\"pipeline_quantize_ms\": {\"inside\": %.3f, \"host_copies\": %.3f, \"wait_device\": %.3f}, "
       "\"pipeline_dequantize_ms\": {\"inside\": %.3f, \"host_copies\": %.3f, \"wait_device\": %.3f}, "
       "\"alloc_zero_f32_ms\": %.3f, \"alloc_zero_u8_ms\": %.3f, "
+      "\"abi_quantize_host_ms\": %.3f, \"abi_dequantize_host_ms\": %.3f, "
       "\"quantize_bitexact_vs_ref\": %s, \"bitexact_vs_ref\": %s, \"accumulate_bitexact_vs_ref\": %s}\n",
       n, tq * 1e3, td * 1e3, (tq + td) * 1e3, ta * 1e3, q_h2d, q_d2h, d_h2d, d_d2h, a_h2d, a_d2h,
       rq * 1e3, rd * 1e3, ra * 1e3, sq[0] * 1e3 / reps, sq[1] * 1e3 / reps,
       sq[2] * 1e3 / reps, sd[0] * 1e3 / reps, sd[1] * 1e3 / reps, sd[2] * 1e3 / reps,
-      t_alloc_f32 * 1e3, t_alloc_u8 * 1e3, same_q ? "true" : "false", same ? "true" : "false", same_acc ? "true" : "false");
+      t_alloc_f32 * 1e3, t_alloc_u8 * 1e3, tq_abi * 1e3, td_abi * 1e3, same_q ? "true" : "false", same ? "true" : "false", same_acc ? "true" : "false");
   return 0;
 }

@@ -1095,7 +1095,7 @@ def main():
     del wl
     torch.cuda.empty_cache()
     extra["c1"] = bench_c1(dev, args)
-    if not args.no_e2e:
+    if not args.no_e2e and rank == 0:  # host-path measurement: one process
         extra["e2e_dropin"] = bench_dropin(dev)
     if not args.no_accumulate:
         extra["accumulate"] = bench_accumulate(dev, args, args.acc_elements)

@@ -205,7 +205,10 @@ typedef struct agq_comm agq_comm;
 enum { AGQ_AR_NCCL = 0, AGQ_AR_FUSED_P2P = 1, AGQ_AR_PUSH_P2P = 2 };
 
 agq_status agq_comm_unique_id(unsigned char id[128]);
-/* Collective over all ranks (NCCL communicator). device = CUDA ordinal. */
+/* Collective over all ranks (NCCL communicator). device = CUDA ordinal.
+ * id == NULL creates a P2P-only communicator (no NCCL): only
+ * AGQ_AR_FUSED_P2P / AGQ_AR_PUSH_P2P after p2p_export/open; it also allows
+ * several ranks on one GPU (which NCCL refuses). */
 agq_status agq_comm_init(agq_comm** comm, const unsigned char id[128],
                          int nranks, int rank, int device);
 /* Peer-memory setup for AGQ_AR_FUSED_P2P / AGQ_AR_PUSH_P2P: export this

@@ -31,17 +31,22 @@ class Communicator:
     ALGOS = {"nccl": L.AGQ_AR_NCCL, "p2p": L.AGQ_AR_FUSED_P2P, "push": L.AGQ_AR_PUSH_P2P}
 
     def __init__(self, group=None, device: int | None = None, p2p_capacity: int = 0,
-                 timeout_s: float | None = None):
+                 timeout_s: float | None = None, nccl: bool = True):
+        """nccl=False: a P2P-only communicator (the NVLink algorithms only, no
+        NCCL communicator); several ranks may then share one GPU."""
         import torch.distributed as dist
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.device = torch.cuda.current_device() if device is None else device
-        uid = C.create_string_buffer(128)
-        if self.rank == 0:
-            L.check(L.lib.agq_comm_unique_id(uid))
-        t = torch.frombuffer(bytearray(uid.raw), dtype=torch.uint8).clone()
-        t = self._bcast_bytes(t, group)
-        uid = C.create_string_buffer(bytes(t.tolist()), 128)
+        self.nccl = nccl
+        uid = None
+        if nccl:
+            uid = C.create_string_buffer(128)
+            if self.rank == 0:
+                L.check(L.lib.agq_comm_unique_id(uid))
+            t = torch.frombuffer(bytearray(uid.raw), dtype=torch.uint8).clone()
+            t = self._bcast_bytes(t, group)
+            uid = C.create_string_buffer(bytes(t.tolist()), 128)
         self._h = C.c_void_p()
         L.check(L.lib.agq_comm_init(C.byref(self._h), uid, self.world, self.rank, self.device))
         self._group = group
@@ -101,6 +106,8 @@ class Communicator:
         # where this rank's tensor lives, so all ranks pick the same algorithm.
         if self.p2p_capacity and q.num_elements() <= self.p2p_capacity and q.block_size == 128:
             return "p2p"
+        if not self.nccl:
+            raise L.InvalidArgument("P2P-only communicator: enable_p2p with enough capacity")
         return "nccl"
 
     def allreduce_fp8(self, q: QuantizedTensor, algo: str = "auto", stream=None,

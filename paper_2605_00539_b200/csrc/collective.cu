@@ -563,23 +563,31 @@ agq_status comm_unique_id(unsigned char id[128]) {
   return AGQ_OK;
 }
 
+// id == nullptr: a P2P-only communicator (no NCCL communicator; the NVLink
+// algorithms only). Also what lets several ranks share one GPU, which NCCL
+// refuses.
 agq_status comm_init(agq_comm** out, const unsigned char id[128], int nranks, int rank,
                      int device) {
   if (nranks < 1 || nranks > AGQ_MAX_WORLD || rank < 0 || rank >= nranks)
     return set_error(AGQ_ERR_INVALID_ARGUMENT, "need at least one worker");
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return cuda_fail(e, "comm_init: cudaSetDevice");
-  if (!nccl().ok) return set_error(AGQ_ERR_NCCL, "libnccl.so.2 not available");
-  ncclUniqueId u;
-  memcpy(u.internal, id, 128);
   agq_comm* c = new agq_comm();
   c->nranks = nranks;
   c->rank = rank;
   c->device = device;
-  agq_status st = nccl_fail(nccl().CommInitRank(&c->nccl, nranks, u, rank), "ncclCommInitRank");
-  if (st) {
-    delete c;
-    return st;
+  if (id != nullptr) {
+    if (!nccl().ok) {
+      delete c;
+      return set_error(AGQ_ERR_NCCL, "libnccl.so.2 not available");
+    }
+    ncclUniqueId u;
+    memcpy(u.internal, id, 128);
+    agq_status st = nccl_fail(nccl().CommInitRank(&c->nccl, nranks, u, rank), "ncclCommInitRank");
+    if (st) {
+      delete c;
+      return st;
+    }
   }
   e = cudaMalloc(&c->done_counter, 64);
   if (e == cudaSuccess) e = cudaMemset(c->done_counter, 0, 64);
@@ -996,6 +1004,7 @@ agq_status allreduce_fp8(agq_comm* c, uint8_t* codes, float* scales, uint64_t n,
                ? allreduce_p2p(c, codes, scales, n, block, err, s)
                : allreduce_push(c, codes, scales, n, block, err, s);
   }
+  if (!c->nccl) return set_error(AGQ_ERR_INVALID_ARGUMENT, "communicator has no NCCL (P2P only)");
   return allreduce_nccl(c, codes, scales, n, block, err, s);
 }
 
@@ -1028,6 +1037,7 @@ agq_status allreduce_naive(agq_comm* c, uint8_t* codes, float* scales, uint64_t 
                            uint32_t block, agq_errors* err, unsigned long long* events,
                            cudaStream_t s) {
   if (n == 0 || c->nranks == 1) return AGQ_OK;
+  if (!c->nccl) return set_error(AGQ_ERR_INVALID_ARGUMENT, "communicator has no NCCL (P2P only)");
   const int P = c->nranks, r = c->rank;
   std::vector<uint64_t> rg(2 * P);
   chunk_ranges(n, block, P, rg.data());
@@ -1102,6 +1112,7 @@ agq_status allreduce_naive(agq_comm* c, uint8_t* codes, float* scales, uint64_t 
 }
 
 agq_status allreduce_bf16_nccl(agq_comm* c, void* data, uint64_t n, cudaStream_t s) {
+  if (!c->nccl) return set_error(AGQ_ERR_INVALID_ARGUMENT, "communicator has no NCCL (P2P only)");
   return nccl_fail(nccl().AllReduce(data, data, n, ncclBfloat16, ncclSum, c->nccl, s),
                    "ncclAllReduce(bf16)");
 }

@@ -21,6 +21,9 @@ import paper_2605_00539_b200 as A  # noqa: E402
 from paper_2605_00539_b200.collective import Communicator  # noqa: E402
 
 
+ALGOS = ("p2p", "push")
+
+
 def grads(world, n, seed):
     out = []
     for r in range(world):
@@ -39,12 +42,14 @@ def main():
     rank, world = dist.get_rank(), dist.get_world_size()
     dev = torch.device("cuda", dev_i)
     cap = 8192 * 5 + 300
+    global ALGOS
+    ALGOS = ("p2p", "push") if world <= 8 else ("p2p",)  # the push kernels cover 2..8 ranks
     comm = Communicator(device=dev_i, p2p_capacity=cap, timeout_s=240.0, nccl=False)
     fails = 0
     for seed, n in enumerate([128 * 3, 8192 * 2 + 77, cap]):
         g = grads(world, n, seed)
         want_c, want_s = O.allreduce_decomposed([c for c, _ in g], [s for _, s in g])
-        for algo in ("p2p", "push"):
+        for algo in ALGOS:
             c, s = g[rank]
             pc, ps = comm.p2p_buffers(n)
             pc.copy_(torch.from_numpy(c))
@@ -67,7 +72,7 @@ def main():
     s = s.copy()
     if rank >= world - 2:
         s[rank] = -1.0
-    for algo in ("p2p", "push"):
+    for algo in ALGOS:
         pc, ps = comm.p2p_buffers(n)
         pc.copy_(torch.from_numpy(c))
         ps.copy_(torch.from_numpy(s))

@@ -102,8 +102,8 @@ constexpr int kReadyOff = 0;       // [16] start barrier, epoch per sender
 constexpr int kDoneOff = 16;       // [16] end barrier, epoch per sender
 constexpr int kScatteredOff = 32;  // [16] push algorithm: inbox slot written
 constexpr int kFailOff = 48;       // sticky: a barrier of this communicator timed out
-constexpr int kOverflowOff = 64;   // [16] overflow block reported by each rank
-constexpr int kBadScaleOff = 80;   // [16] bad-scale key reported by each rank
+constexpr int kErrOff = 64;        // [2] min overflow block / min bad-scale key of
+                                   // the group (peers atomicMin into them)
 size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 }  // namespace
 
@@ -314,9 +314,9 @@ __device__ __forceinline__ void epoch_end(const Args& a, bool ok,
   if (ok && ov != -1) {
     const long long bs = *reinterpret_cast<volatile long long*>(&err->bad_scale_block);
     for (int s = 0; s < P; ++s) {
-      uint64_t* pf = reinterpret_cast<uint64_t*>(base[s]);
-      if (ov != kNone) atomicMin(reinterpret_cast<long long*>(pf + kOverflowOff + rank), ov);
-      if (bs != kNone) atomicMin(reinterpret_cast<long long*>(pf + kBadScaleOff + rank), bs);
+      long long* pe = reinterpret_cast<long long*>(base[s]) + kErrOff;
+      if (ov != kNone) atomicMin(pe, ov);
+      if (bs != kNone) atomicMin(pe + 1, bs);
     }
     __threadfence_system();
     for (int s = 0; s < P; ++s)
@@ -325,14 +325,16 @@ __device__ __forceinline__ void epoch_end(const Args& a, bool ok,
     for (int s = 0; s < P; ++s)
       if (!wait_flag(my_flags + kDoneOff + s, a.epoch, my_flags + kFailOff, a.timeout_ns))
         fine = false;
-    for (int s = 0; s < P; ++s) {
-      volatile long long* o = reinterpret_cast<volatile long long*>(my_flags + kOverflowOff + s);
-      volatile long long* b = reinterpret_cast<volatile long long*>(my_flags + kBadScaleOff + s);
-      if (*o != kNone) err_min(&err->overflow_block, *o);
-      if (*b != kNone) err_min(&err->bad_scale_block, *b);
-      *o = kNone;  // reset for the next epoch (peers enter it only after
-      *b = kNone;  // this kernel: its start barrier needs our next "ready")
-    }
+    // one 16-byte read and reset of both words (peers enter the next epoch's
+    // end only after this kernel: their start barrier needs our next "ready")
+    long long e0, e1;
+    asm volatile("ld.volatile.global.v2.s64 {%0, %1}, [%2];"
+                 : "=l"(e0), "=l"(e1) : "l"(my_flags + kErrOff) : "memory");
+    if (e0 != kNone) err_min(&err->overflow_block, e0);
+    if (e1 != kNone) err_min(&err->bad_scale_block, e1);
+    if (e0 != kNone || e1 != kNone)
+      asm volatile("st.volatile.global.v2.s64 [%0], {%1, %1};"
+                   :: "l"(my_flags + kErrOff), "l"(kNone) : "memory");
     if (!fine) mark_failed(a);
   } else {
     mark_failed(a);
@@ -535,8 +537,8 @@ __global__ void __launch_bounds__(256, 2) k_push_reduce(PushArgs a, PieceTable p
 
 __global__ void k_init_flags(uint64_t* flags) {
   const int i = threadIdx.x;
-  if (i < kOverflowOff) flags[i] = 0;
-  else if (i < kBadScaleOff + AGQ_MAX_WORLD) flags[i] = (uint64_t)kNone;
+  if (i < kErrOff) flags[i] = 0;
+  else if (i < kErrOff + 2) flags[i] = (uint64_t)kNone;
 }
 
 }  // namespace agqk

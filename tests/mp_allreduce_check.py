@@ -66,7 +66,7 @@ def main():
     for seed, n, kind in cases:
         g = every_code_grads(world, n // 128, seed) if kind else grads(world, n, seed)
         want_c, want_s = O.allreduce_decomposed([c for c, _ in g], [s for _, s in g])
-        for algo in ("nccl", "p2p", "push", "auto"):
+        for algo in ("nccl", "p2p", "push", "auto", "auto-copy"):
             c, s = g[rank]
             if algo in ("p2p", "push", "auto"):
                 pc, ps = comm.p2p_buffers(n)
@@ -76,12 +76,16 @@ def main():
             else:
                 q = A.QuantizedTensor(torch.from_numpy(c).to(dev), torch.from_numpy(s).to(dev), 8, 128,
                                       (n,), A.CodecKind.Fp8E4M3, packed=False)
-            comm.allreduce_fp8(q, algo=algo)
+            # "auto-copy": auto on a tensor outside the symmetric buffers -> the
+            # fused kernel with the copy in / copy out path
+            comm.allreduce_fp8(q, algo="auto" if algo == "auto-copy" else algo)
             ok = np.array_equal(q.codes.cpu().numpy(), want_c) and \
                 np.array_equal(q.scales.cpu().numpy().view(np.uint32), want_s.view(np.uint32))
             if not ok:
                 fails += 1
                 print(f"rank {rank}: MISMATCH algo={algo} n={n}", flush=True)
+            if algo == "auto-copy":
+                continue
             # trace of what the real collective issued == the reference's trace
             mine, moved = comm.last_trace()
             full = comm.gather_trace()

@@ -116,11 +116,25 @@ inline QuantizedTensor local_accumulate(const QuantizedTensor& main,
   if (main.num_elements() != local_grad.size())
     throw std::invalid_argument("local gradient shape mismatch");
   detail::validate_structure(main);  // dequantize_blockwise(main) validates first
-  QuantizedTensor out = main;
-  detail::throw_status(agq_local_accumulate_host(main.codes.data(), main.scales.data(),
-                                                 main.num_elements(), main.block_size,
-                                                 local_grad.data(), static_cast<int>(precision),
-                                                 out.codes.data(), out.scales.data()));
+  // the transfers and kernels run while the result is built
+  detail::HostJob job;
+  detail::throw_status(agq_local_accumulate_host_begin(
+      main.codes.data(), main.scales.data(), main.num_elements(), main.block_size,
+      local_grad.data(), static_cast<int>(precision), job.out()));
+  QuantizedTensor out;
+  out.bit_width = main.bit_width;
+  out.block_size = main.block_size;
+  out.codec_kind = main.codec_kind;
+  out.shape = main.shape;
+  out.codes.resize(main.codes.size());
+  out.scales.resize(main.scales.size());
+  if (job)
+    job.finish(out.codes.data(), out.scales.data());
+  else
+    detail::throw_status(agq_local_accumulate_host(main.codes.data(), main.scales.data(),
+                                                   main.num_elements(), main.block_size,
+                                                   local_grad.data(), static_cast<int>(precision),
+                                                   out.codes.data(), out.scales.data()));
   return out;
 }
 

@@ -302,10 +302,36 @@ agq_status agq_local_accumulate_host(const uint8_t* codes, const float* scales,
                                      uint64_t n, uint32_t block,
                                      const float* local, int precision,
                                      uint8_t* out_codes, float* out_scales);
+/* Split form of the four entries above, for callers that allocate their
+ * result buffers after the call starts (the drop-in API value-initialises
+ * its result vectors: that host work overlaps the transfers and kernels).
+ * *_begin stages the inputs (they must stay valid until finish), enqueues
+ * every chunk and returns; *job is NULL when nothing was issued (n == 0, or
+ * the call's staging exceeds the library's 256 MB job cap — use the
+ * synchronous entry then). agq_host_job_finish waits, copies the results to
+ * out0 (codes or values) / out1 (scales, or NULL), reports the same errors
+ * as the synchronous entry and frees the job; out0 == NULL cancels it. */
+typedef struct agq_host_job agq_host_job;
+agq_status agq_quantize_host_begin(const float* x, uint64_t n, int bits, uint32_t block,
+                                   int codec, agq_host_job** job);
+agq_status agq_dequantize_host_begin(const uint8_t* codes, const float* scales,
+                                     uint64_t n, int bits, uint32_t block, int codec,
+                                     agq_host_job** job);
+agq_status agq_roundtrip_host_begin(const float* x, uint64_t n, int bits, uint32_t block,
+                                    int codec, agq_host_job** job);
+agq_status agq_local_accumulate_host_begin(const uint8_t* codes, const float* scales,
+                                           uint64_t n, uint32_t block,
+                                           const float* local, int precision,
+                                           agq_host_job** job);
+agq_status agq_host_job_finish(agq_host_job* job, void* out0, void* out1);
 /* Diagnostics of the host-buffer pipelines: out[0..3] = cumulative seconds
  * inside the pipelines, of host copies (caller <-> pinned staging), waiting
  * for device work, and the number of calls; reset != 0 zeroes them. */
 agq_status agq_host_pipeline_stats(double* out, int reset);
+/* The host pipelines' staging copy (caller memory <-> pinned slots): the
+ * library's copy threads plus the caller, streaming stores. Exported so a
+ * caller can measure the host-memory rate that bounds the *_host entries. */
+agq_status agq_host_copy(void* dst, const void* src, uint64_t bytes);
 agq_status agq_allreduce_simulated_host(int world, const uint8_t* const* codes,
                                         const float* const* scales, uint64_t n,
                                         uint32_t block, int protocol /*0 dec,1 naive*/,

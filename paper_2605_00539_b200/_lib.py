@@ -110,6 +110,12 @@ def _load() -> C.CDLL:
         "agq_allreduce_bf16_nccl": (I, [P, P, U64, S]),
         "agq_quantize_host": (I, [P, U64, I, U32, I, P, P]),
         "agq_host_pipeline_stats": (I, [C.POINTER(C.c_double), I]),
+        "agq_host_copy": (I, [P, P, U64]),
+        "agq_quantize_host_begin": (I, [P, U64, I, U32, I, P]),
+        "agq_dequantize_host_begin": (I, [P, P, U64, I, U32, I, P]),
+        "agq_roundtrip_host_begin": (I, [P, U64, I, U32, I, P]),
+        "agq_local_accumulate_host_begin": (I, [P, P, U64, U32, P, I, P]),
+        "agq_host_job_finish": (I, [P, P, P]),
         "agq_dequantize_host": (I, [P, P, U64, I, U32, I, P]),
         "agq_local_accumulate_host": (I, [P, P, U64, U32, P, I, P, P]),
         "agq_allreduce_simulated_host": (I, [I, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), U64,
@@ -138,7 +144,7 @@ EXPORTED = (
     "agq_comm_p2p_open agq_comm_p2p_buffers agq_comm_destroy agq_comm_rank agq_comm_size "
     "agq_comm_set_timeout agq_comm_last_trace agq_fill_input "
     "agq_allreduce_fp8 agq_allreduce_naive_fp8 agq_allreduce_bf16_nccl agq_quantize_host agq_dequantize_host "
-    "agq_local_accumulate_host agq_host_pipeline_stats agq_allreduce_simulated_host agq_stored_activation_counts "
+    "agq_local_accumulate_host agq_host_pipeline_stats agq_host_copy agq_quantize_host_begin agq_dequantize_host_begin agq_roundtrip_host_begin agq_local_accumulate_host_begin agq_host_job_finish agq_allreduce_simulated_host agq_stored_activation_counts "
     "agq_plan_bit_widths").split()
 
 

@@ -8,12 +8,14 @@
 #include <climits>
 #include <chrono>
 #include <condition_variable>
+#include <functional>
 #include <thread>
 #if defined(__x86_64__)
 #include <immintrin.h>
 #endif
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -506,7 +508,7 @@ void copy_piece(void* dst, const void* src, size_t n) {
 }
 
 // Persistent host copy threads: copy() splits a batch of memcpy jobs into
-// ~1 MB pieces, shares them with the workers (the caller works too) and
+// >= 512 KB pieces, shares them with the workers (the caller works too) and
 // returns when every piece is done. Each batch owns its counters, so a worker
 // that wakes late can never touch another batch's pieces.
 class CopyPool {
@@ -525,7 +527,7 @@ class CopyPool {
     for (const Job& j : jobs) total += j.bytes;
     if (total == 0) return;
     auto b = std::make_shared<Batch>();
-    const size_t piece = std::max<size_t>(1 << 20, total / (4 * (nthreads_ + 1)) + 1);
+    const size_t piece = std::max<size_t>(kMinPiece, total / (4 * (nthreads_ + 1)) + 1);
     for (const Job& j : jobs)
       for (size_t o = 0; o < j.bytes; o += piece)
         b->pieces.push_back({static_cast<char*>(j.dst) + o, static_cast<const char*>(j.src) + o,
@@ -534,16 +536,15 @@ class CopyPool {
       {
         std::lock_guard<std::mutex> lk(mu_);
         cur_ = b;
-        ++gen_;
+        gen_.fetch_add(1, std::memory_order_release);
       }
-      cv_.notify_all();
+      if (sleepers_.load(std::memory_order_acquire) > 0) cv_.notify_all();
     }
     run(*b);
-    while (b->done.load(std::memory_order_acquire) < b->pieces.size()) std::this_thread::yield();
+    while (b->done.load(std::memory_order_acquire) < b->pieces.size()) _mm_pause();
     std::lock_guard<std::mutex> lk(mu_);
     if (cur_ == b) cur_.reset();
   }
-
  private:
   struct Batch {
     std::vector<Job> pieces;
@@ -566,21 +567,38 @@ class CopyPool {
   void loop() {
     uint64_t seen = 0;
     for (;;) {
+      // spin briefly for the next batch (a pipeline submits one per chunk),
+      // then sleep
+      const auto t0 = std::chrono::steady_clock::now();
+      while (gen_.load(std::memory_order_acquire) == seen &&
+             (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                 std::chrono::steady_clock::now() - t0).count() < kSpinNs)
+        for (int i = 0; i < 64; ++i) _mm_pause();
       std::shared_ptr<Batch> b;
       {
         std::unique_lock<std::mutex> lk(mu_);
-        cv_.wait(lk, [&] { return gen_ != seen; });
-        seen = gen_;
+        if (gen_.load(std::memory_order_relaxed) == seen) {
+          sleepers_.fetch_add(1, std::memory_order_acq_rel);
+          cv_.wait(lk, [&] { return gen_.load(std::memory_order_relaxed) != seen; });
+          sleepers_.fetch_sub(1, std::memory_order_acq_rel);
+        }
+        seen = gen_.load(std::memory_order_relaxed);
         b = cur_;
       }
       if (b) run(*b);
     }
   }
+  // measured on the B200 box (profiles/r02_host_pipe_sweep.log): 512 KB
+  // pieces balance a chunk's batch over the threads; 200 us of spinning
+  // hides the wake-up latency between a pipeline's batches
+  static constexpr size_t kMinPiece = 512u << 10;
+  static constexpr uint64_t kSpinNs = 200000;
   int nthreads_ = 0;
   std::mutex mu_;
   std::condition_variable cv_;
   std::shared_ptr<Batch> cur_;
-  uint64_t gen_ = 0;
+  std::atomic<uint64_t> gen_{0};
+  std::atomic<int> sleepers_{0};
 };
 
 // One pipeline: kSlots slots of pinned + device staging, one stream each.
@@ -622,6 +640,29 @@ struct HostPipe {
     cap = bytes;
     return AGQ_OK;
   }
+  // begin/finish jobs: pinned staging for every chunk of the call (no slot
+  // reuse on the host side, so nothing waits before finish) and one event
+  // per chunk
+  char* big = nullptr;
+  size_t big_cap = 0;
+  std::vector<cudaEvent_t> cev;
+  agq_status reserve_job(size_t bytes, uint64_t chunks) {
+    if (big_cap < bytes) {
+      if (big) cudaFreeHost(big);
+      big = nullptr;
+      big_cap = 0;
+      cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&big), bytes, cudaHostAllocDefault);
+      if (e != cudaSuccess) return cuda_fail(e, "host pipeline: job staging");
+      big_cap = bytes;
+    }
+    while (cev.size() < chunks) {
+      cudaEvent_t e;
+      cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      if (r != cudaSuccess) return cuda_fail(r, "host pipeline: events");
+      cev.push_back(e);
+    }
+    return AGQ_OK;
+  }
 };
 
 std::mutex g_pipes_mu;
@@ -660,28 +701,48 @@ struct PipeLease {
 };
 
 // One chunk's staging layout: `in` bytes copied host->device before the
-// kernel, `out` bytes device->host after it, both inside one slot.
+// kernel, `out` bytes device->host after it, both inside one slot. Inputs
+// carry the caller's pointer; outputs a byte offset into output `which`
+// (0: codes or values, 1: scales), resolved when the outputs are known.
 struct Part {
   size_t off;  // inside the slot
   size_t bytes;
-  char* host;  // caller buffer (in: source, out: destination)
+  const char* host;  // input source
+  int which;         // output index
+  size_t rel;        // output byte offset
+};
+Part in_part(size_t off, size_t bytes, const void* src) {
+  return {off, bytes, static_cast<const char*>(src), -1, 0};
+}
+Part out_part(size_t off, size_t bytes, int which, size_t rel) {
+  return {off, bytes, nullptr, which, rel};
+}
+
+// One host entry point as chunks: plan(k, in, out) fills chunk k's parts,
+// launch(k, dev_slot, stream, err) enqueues its kernels.
+struct OpSpec {
+  uint64_t chunks = 0;
+  size_t slot = 0;
+  int op = 0;
+  std::function<void(uint64_t, std::vector<Part>&, std::vector<Part>&)> plan;
+  std::function<agq_status(uint64_t, char*, cudaStream_t, agq_errors*)> launch;
 };
 
-// Run `nchunks` chunks through the pipeline. plan(k, in, out) fills the
-// chunk's in/out parts; launch(k, dev_slot, stream) enqueues its kernels.
-template <class Plan, class Launch>
-agq_status run_pipeline(HostPipe& p, uint64_t nchunks, size_t slot_bytes, Plan plan,
-                        Launch launch) {
-  if (agq_status st = p.reserve(slot_bytes)) return st;
-  if (agq_status st = cuda_fail(cudaMemcpy(p.d_err, &kNoErrors, sizeof(agq_errors),
-                                           cudaMemcpyHostToDevice),
-                                "host pipeline: reset"))
-    return st;
+agq_status reset_errors(HostPipe& p) {
+  return cuda_fail(cudaMemcpy(p.d_err, &kNoErrors, sizeof(agq_errors), cudaMemcpyHostToDevice),
+                   "host pipeline: reset");
+}
+
+// Run the op through the slot ring: the host copies of chunk k overlap the
+// transfers and kernels of chunks k-3..k-1.
+agq_status run_pipeline(HostPipe& p, const OpSpec& op, char* const* outs_base) {
+  if (agq_status st = p.reserve(op.slot)) return st;
+  if (agq_status st = reset_errors(p)) return st;
   std::vector<std::vector<Part>> outs(kSlots);
   CopyPool& pool = CopyPool::get();
   const unsigned long long t_start = now_ns();
   unsigned long long t_copy = 0, t_wait = 0;
-  for (uint64_t k = 0; k < nchunks + kSlots; ++k) {
+  for (uint64_t k = 0; k < op.chunks + kSlots; ++k) {
     const int s = (int)(k % kSlots);
     std::vector<CopyPool::Job> jobs;
     // drain the slot: chunk k - kSlots finished -> copy its results out
@@ -689,22 +750,23 @@ agq_status run_pipeline(HostPipe& p, uint64_t nchunks, size_t slot_bytes, Plan p
       const unsigned long long t0 = now_ns();
       if (agq_status st = cuda_fail(cudaEventSynchronize(p.ev[s]), "host pipeline")) return st;
       t_wait += now_ns() - t0;
-      for (const Part& o : outs[s]) jobs.push_back({o.host, p.pin[s] + o.off, o.bytes});
+      for (const Part& o : outs[s])
+        jobs.push_back({outs_base[o.which] + o.rel, p.pin[s] + o.off, o.bytes});
       outs[s].clear();
     }
     std::vector<Part> in;
-    if (k < nchunks) {
-      plan(k, in, outs[s]);
+    if (k < op.chunks) {
+      op.plan(k, in, outs[s]);
       for (const Part& i : in) jobs.push_back({p.pin[s] + i.off, i.host, i.bytes});
     }
     const unsigned long long t1 = now_ns();
     pool.copy(jobs);
     t_copy += now_ns() - t1;
-    if (k >= nchunks) continue;
+    if (k >= op.chunks) continue;
     cudaStream_t st = p.st[s];
     for (const Part& i : in)
       cudaMemcpyAsync(p.dbuf[s] + i.off, p.pin[s] + i.off, i.bytes, cudaMemcpyHostToDevice, st);
-    if (agq_status r = launch(k, p.dbuf[s], st)) {
+    if (agq_status r = op.launch(k, p.dbuf[s], st, p.d_err)) {
       cudaDeviceSynchronize();
       return r;
     }
@@ -716,6 +778,77 @@ agq_status run_pipeline(HostPipe& p, uint64_t nchunks, size_t slot_bytes, Plan p
   g_ns_wait += t_wait;
   g_ns_total += now_ns() - t_start;
   ++g_calls;
+  return AGQ_OK;
+}
+
+// A begun host call (agq_*_host_begin): every chunk's inputs staged and its
+// transfers and kernels enqueued; the outputs wait in pinned staging until
+// agq_host_job_finish copies them to the caller. Holds its pipeline.
+constexpr size_t kJobStagingCap = 256u << 20;  // larger calls run synchronously
+}  // namespace
+}  // namespace agqh
+
+struct agq_host_job {
+  agqh::PipeLease lease;
+  int op = 0;
+  size_t slot = 0;
+  std::vector<std::vector<agqh::Part>> outs;  // per chunk
+};
+
+namespace agqh {
+namespace {
+
+// Issue all chunks of `op`; on success `job` owns the in-flight work.
+agq_status job_issue(agq_host_job& job, const OpSpec& op) {
+  HostPipe& p = *job.lease.p;
+  if (agq_status st = p.reserve(op.slot)) return st;
+  if (agq_status st = p.reserve_job(op.slot * op.chunks, op.chunks)) return st;
+  if (agq_status st = reset_errors(p)) return st;
+  job.op = op.op;
+  job.slot = op.slot;
+  job.outs.assign(op.chunks, {});
+  CopyPool& pool = CopyPool::get();
+  for (uint64_t k = 0; k < op.chunks; ++k) {
+    const int s = (int)(k % kSlots);  // device slot: reused in stream order
+    char* h = p.big + k * op.slot;
+    std::vector<Part> in;
+    op.plan(k, in, job.outs[k]);
+    std::vector<CopyPool::Job> jobs;
+    for (const Part& i : in) jobs.push_back({h + i.off, i.host, i.bytes});
+    pool.copy(jobs);
+    cudaStream_t st = p.st[s];
+    for (const Part& i : in)
+      cudaMemcpyAsync(p.dbuf[s] + i.off, h + i.off, i.bytes, cudaMemcpyHostToDevice, st);
+    if (agq_status r = op.launch(k, p.dbuf[s], st, p.d_err)) {
+      cudaDeviceSynchronize();
+      return r;
+    }
+    for (const Part& o : job.outs[k])
+      cudaMemcpyAsync(h + o.off, p.dbuf[s] + o.off, o.bytes, cudaMemcpyDeviceToHost, st);
+    if (agq_status r = cuda_fail(cudaEventRecord(p.cev[k], st), "host pipeline")) {
+      cudaDeviceSynchronize();
+      return r;
+    }
+  }
+  return AGQ_OK;
+}
+
+// Copy the outputs out, one batch per run of finished chunks (normally all
+// of them: the device work ran while the caller built its result buffers).
+agq_status job_finish(agq_host_job& job, char* const* outs_base) {
+  HostPipe& p = *job.lease.p;
+  CopyPool& pool = CopyPool::get();
+  const uint64_t K = job.outs.size();
+  for (uint64_t k = 0; k < K;) {
+    if (agq_status st = cuda_fail(cudaEventSynchronize(p.cev[k]), "host pipeline")) return st;
+    uint64_t e = k + 1;
+    while (e < K && cudaEventQuery(p.cev[e]) == cudaSuccess) ++e;
+    std::vector<CopyPool::Job> jobs;
+    for (; k < e; ++k)
+      for (const Part& o : job.outs[k])
+        jobs.push_back({outs_base[o.which] + o.rel, p.big + k * job.slot + o.off, o.bytes});
+    pool.copy(jobs);
+  }
   return AGQ_OK;
 }
 
@@ -736,6 +869,125 @@ agq_status read_errors(HostPipe& p, int op) {
   return agq_errors_message(&h, op, nullptr, 0);
 }
 
+// The host entry points as chunked ops (slot layouts: inputs first, outputs
+// after them, so a slot's next inputs can be staged while its outputs drain).
+OpSpec quantize_spec(const float* x, uint64_t n, int bits, uint32_t block, int codec) {
+  const uint64_t ce = chunk_elems(n, block);
+  const size_t oc = al(ce * 4), os = oc + al(ce);
+  OpSpec op;
+  op.chunks = (n + ce - 1) / ce;
+  op.slot = os + al((ce / block + 1) * 4);
+  op.op = AGQ_OP_QUANTIZE;
+  op.plan = [=](uint64_t k, std::vector<Part>& in, std::vector<Part>& out) {
+    const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
+    in.push_back(in_part(0, len * 4, x + e0));
+    out.push_back(out_part(oc, len, 0, e0));
+    out.push_back(out_part(os, (len + block - 1) / block * 4, 1, e0 / block * 4));
+  };
+  op.launch = [=](uint64_t k, char* d, cudaStream_t s, agq_errors* err) {
+    const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
+    return quantize_device_at(d, AGQ_F32, len, bits, block, codec, d + oc, AGQ_CODES_BYTES,
+                              reinterpret_cast<float*>(d + os), (long long)(e0 / block), err, s);
+  };
+  return op;
+}
+
+OpSpec dequantize_spec(const uint8_t* codes, const float* scales, uint64_t n, int bits,
+                       uint32_t block, int codec) {
+  const uint64_t ce = chunk_elems(n, block);
+  const size_t os = al(ce), oo = os + al((ce / block + 1) * 4);
+  OpSpec op;
+  op.chunks = (n + ce - 1) / ce;
+  op.slot = oo + al(ce * 4);
+  op.op = AGQ_OP_DEQUANTIZE;
+  op.plan = [=](uint64_t k, std::vector<Part>& in, std::vector<Part>& out) {
+    const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
+    in.push_back(in_part(0, len, codes + e0));
+    in.push_back(in_part(os, (len + block - 1) / block * 4, scales + e0 / block));
+    out.push_back(out_part(oo, len * 4, 0, e0 * 4));
+  };
+  op.launch = [=](uint64_t k, char* d, cudaStream_t s, agq_errors* err) {
+    const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
+    return dequantize_device_at(d, AGQ_CODES_BYTES, reinterpret_cast<float*>(d + os), len, bits,
+                                block, codec, d + oo, AGQ_F32, 1, (long long)(e0 / block), err, s);
+  };
+  return op;
+}
+
+OpSpec roundtrip_spec(const float* x, uint64_t n, int bits, uint32_t block, int codec) {
+  const uint64_t ce = chunk_elems(n, block);
+  // [x | reconstruction | codes | scales]: the codes never cross PCIe
+  const size_t oo = al(ce * 4), oc = oo + al(ce * 4), os = oc + al(ce);
+  OpSpec op;
+  op.chunks = (n + ce - 1) / ce;
+  op.slot = os + al((ce / block + 1) * 4);
+  op.op = AGQ_OP_QUANTIZE;
+  op.plan = [=](uint64_t k, std::vector<Part>& in, std::vector<Part>& out) {
+    const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
+    in.push_back(in_part(0, len * 4, x + e0));
+    out.push_back(out_part(oo, len * 4, 0, e0 * 4));
+  };
+  op.launch = [=](uint64_t k, char* d, cudaStream_t s, agq_errors* err) {
+    const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
+    // quantize with the chunk's global block indices for the errors
+    if (agq_status r = quantize_device_at(d, AGQ_F32, len, bits, block, codec, d + oc,
+                                          AGQ_CODES_BYTES, reinterpret_cast<float*>(d + os),
+                                          (long long)(e0 / block), err, s))
+      return r;
+    return dequantize_device_at(d + oc, AGQ_CODES_BYTES, reinterpret_cast<float*>(d + os), len,
+                                bits, block, codec, d + oo, AGQ_F32, 0, (long long)(e0 / block),
+                                err, s);
+  };
+  return op;
+}
+
+OpSpec accumulate_spec(const uint8_t* codes, const float* scales, uint64_t n, uint32_t block,
+                       const float* local, int precision) {
+  const uint64_t ce = chunk_elems(n, block);
+  const size_t os = al(ce), ol = os + al((ce / block + 1) * 4), oc = ol + al(ce * 4);
+  const size_t oo = oc + al(ce);
+  OpSpec op;
+  op.chunks = (n + ce - 1) / ce;
+  op.slot = oo + al((ce / block + 1) * 4);
+  op.op = AGQ_OP_ACCUMULATE;
+  op.plan = [=](uint64_t k, std::vector<Part>& in, std::vector<Part>& out) {
+    const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
+    const uint64_t nb = (len + block - 1) / block;
+    in.push_back(in_part(0, len, codes + e0));
+    in.push_back(in_part(os, nb * 4, scales + e0 / block));
+    in.push_back(in_part(ol, len * 4, local + e0));
+    out.push_back(out_part(oc, len, 0, e0));
+    out.push_back(out_part(oo, nb * 4, 1, e0 / block * 4));
+  };
+  op.launch = [=](uint64_t k, char* d, cudaStream_t s, agq_errors* err) {
+    const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
+    return accumulate_device(reinterpret_cast<uint8_t*>(d), reinterpret_cast<float*>(d + os),
+                             d + ol, AGQ_F32, len, block, precision,
+                             reinterpret_cast<uint8_t*>(d + oc), reinterpret_cast<float*>(d + oo),
+                             err, s, (long long)(e0 / block));
+  };
+  return op;
+}
+
+// The synchronous entry: one pipeline pass, one sync, the error record.
+agq_status run_sync(const OpSpec& op, void* out0, void* out1) {
+  PipeLease lease;
+  HostPipe& p = *lease.p;
+  char* base[2] = {static_cast<char*>(out0), static_cast<char*>(out1)};
+  if (agq_status st = run_pipeline(p, op, base)) return st;
+  return read_errors(p, op.op);
+}
+
+// The begin entry: *job = nullptr (nothing issued) when the call's staging
+// would exceed kJobStagingCap — the caller then uses the synchronous entry.
+agq_status run_begin(const OpSpec& op, agq_host_job** job) {
+  if (op.slot * op.chunks > kJobStagingCap) return AGQ_OK;
+  auto j = std::make_unique<agq_host_job>();
+  if (agq_status st = job_issue(*j, op)) return st;
+  *job = j.release();
+  return AGQ_OK;
+}
+
 }  // namespace
 }  // namespace agqh
 
@@ -753,32 +1005,19 @@ agq_status agq_host_pipeline_stats(double* out, int reset) {
   return AGQ_OK;
 }
 
+agq_status agq_host_copy(void* dst, const void* src, uint64_t bytes) {
+  if (bytes == 0) return AGQ_OK;
+  if (!dst || !src) return set_error(AGQ_ERR_INVALID_ARGUMENT, "agq_host_copy: null buffer");
+  CopyPool::get().copy({{dst, src, (size_t)bytes}});
+  return AGQ_OK;
+}
+
 agq_status agq_quantize_host(const float* x, uint64_t n, int bits, uint32_t block, int codec,
                              uint8_t* codes, float* scales) {
   if (agq_status st = check_args(bits, block, codec)) return st;
   if (agq_status st = check_device()) return st;
   if (n == 0) return AGQ_OK;
-  const uint64_t ce = chunk_elems(n, block), K = (n + ce - 1) / ce;
-  const size_t oc = al(ce * 4), os = oc + al(ce), slot = os + al((ce / block + 1) * 4);
-  PipeLease lease;
-  HostPipe& p = *lease.p;
-  agq_status st = run_pipeline(
-      p, K, slot,
-      [&](uint64_t k, std::vector<Part>& in, std::vector<Part>& out) {
-        const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
-        const uint64_t nb = (len + block - 1) / block;
-        in.push_back({0, len * 4, (char*)(x + e0)});
-        out.push_back({oc, len, (char*)(codes + e0)});
-        out.push_back({os, nb * 4, (char*)(scales + e0 / block)});
-      },
-      [&](uint64_t k, char* d, cudaStream_t s) {
-        const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
-        return quantize_device_at(d, AGQ_F32, len, bits, block, codec, d + oc, AGQ_CODES_BYTES,
-                                  reinterpret_cast<float*>(d + os), (long long)(e0 / block),
-                                  p.d_err, s);
-      });
-  if (st) return st;
-  return read_errors(p, AGQ_OP_QUANTIZE);
+  return run_sync(quantize_spec(x, n, bits, block, codec), codes, scales);
 }
 
 agq_status agq_dequantize_host(const uint8_t* codes, const float* scales, uint64_t n, int bits,
@@ -786,27 +1025,7 @@ agq_status agq_dequantize_host(const uint8_t* codes, const float* scales, uint64
   if (agq_status st = check_args(bits, block, codec)) return st;
   if (agq_status st = check_device()) return st;
   if (n == 0) return AGQ_OK;
-  const uint64_t ce = chunk_elems(n, block), K = (n + ce - 1) / ce;
-  const size_t os = al(ce), oo = os + al((ce / block + 1) * 4), slot = oo + al(ce * 4);
-  PipeLease lease;
-  HostPipe& p = *lease.p;
-  agq_status st = run_pipeline(
-      p, K, slot,
-      [&](uint64_t k, std::vector<Part>& in, std::vector<Part>& o) {
-        const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
-        const uint64_t nb = (len + block - 1) / block;
-        in.push_back({0, len, (char*)(codes + e0)});
-        in.push_back({os, nb * 4, (char*)(scales + e0 / block)});
-        o.push_back({oo, len * 4, (char*)(out + e0)});
-      },
-      [&](uint64_t k, char* d, cudaStream_t s) {
-        const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
-        return dequantize_device_at(d, AGQ_CODES_BYTES, reinterpret_cast<float*>(d + os), len,
-                                    bits, block, codec, d + oo, AGQ_F32, 1,
-                                    (long long)(e0 / block), p.d_err, s);
-      });
-  if (st) return st;
-  return read_errors(p, AGQ_OP_DEQUANTIZE);
+  return run_sync(dequantize_spec(codes, scales, n, bits, block, codec), out, nullptr);
 }
 
 agq_status agq_roundtrip_host(const float* x, uint64_t n, int bits, uint32_t block, int codec,
@@ -814,32 +1033,7 @@ agq_status agq_roundtrip_host(const float* x, uint64_t n, int bits, uint32_t blo
   if (agq_status st = check_args(bits, block, codec)) return st;
   if (agq_status st = check_device()) return st;
   if (n == 0) return AGQ_OK;
-  const uint64_t ce = chunk_elems(n, block), K = (n + ce - 1) / ce;
-  // [x | reconstruction | codes | scales]: the codes never cross PCIe
-  const size_t oo = al(ce * 4), oc = oo + al(ce * 4), os = oc + al(ce);
-  const size_t slot = os + al((ce / block + 1) * 4);
-  PipeLease lease;
-  HostPipe& p = *lease.p;
-  agq_status st = run_pipeline(
-      p, K, slot,
-      [&](uint64_t k, std::vector<Part>& in, std::vector<Part>& o) {
-        const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
-        in.push_back({0, len * 4, (char*)(x + e0)});
-        o.push_back({oo, len * 4, (char*)(out + e0)});
-      },
-      [&](uint64_t k, char* d, cudaStream_t s) {
-        const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
-        // quantize with the chunk's global block indices for the errors
-        if (agq_status r = quantize_device_at(d, AGQ_F32, len, bits, block, codec, d + oc,
-                                              AGQ_CODES_BYTES, reinterpret_cast<float*>(d + os),
-                                              (long long)(e0 / block), p.d_err, s))
-          return r;
-        return dequantize_device_at(d + oc, AGQ_CODES_BYTES, reinterpret_cast<float*>(d + os), len,
-                                    bits, block, codec, d + oo, AGQ_F32, 0,
-                                    (long long)(e0 / block), p.d_err, s);
-      });
-  if (st) return st;
-  return read_errors(p, AGQ_OP_QUANTIZE);
+  return run_sync(roundtrip_spec(x, n, bits, block, codec), out, nullptr);
 }
 
 agq_status agq_local_accumulate_host(const uint8_t* codes, const float* scales, uint64_t n,
@@ -848,34 +1042,61 @@ agq_status agq_local_accumulate_host(const uint8_t* codes, const float* scales, 
   if (agq_status st = check_args(8, block, AGQ_CODEC_FP8_E4M3)) return st;
   if (agq_status st = check_device()) return st;
   if (n == 0) return AGQ_OK;
-  const uint64_t ce = chunk_elems(n, block), K = (n + ce - 1) / ce;
-  // inputs [codes | scales | local], outputs [codes | scales] after them: the
-  // next chunk's inputs are staged while this slot's outputs drain
-  const size_t os = al(ce), ol = os + al((ce / block + 1) * 4), oc = ol + al(ce * 4);
-  const size_t oo = oc + al(ce), slot = oo + al((ce / block + 1) * 4);
-  PipeLease lease;
-  HostPipe& p = *lease.p;
-  agq_status st = run_pipeline(
-      p, K, slot,
-      [&](uint64_t k, std::vector<Part>& in, std::vector<Part>& o) {
-        const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
-        const uint64_t nb = (len + block - 1) / block;
-        in.push_back({0, len, (char*)(codes + e0)});
-        in.push_back({os, nb * 4, (char*)(scales + e0 / block)});
-        in.push_back({ol, len * 4, (char*)(local + e0)});
-        o.push_back({oc, len, (char*)(out_codes + e0)});
-        o.push_back({oo, nb * 4, (char*)(out_scales + e0 / block)});
-      },
-      [&](uint64_t k, char* d, cudaStream_t s) {
-        const uint64_t e0 = k * ce, len = std::min(ce, n - e0);
-        return accumulate_device(reinterpret_cast<uint8_t*>(d), reinterpret_cast<float*>(d + os),
-                                 d + ol, AGQ_F32, len, block, precision,
-                                 reinterpret_cast<uint8_t*>(d + oc),
-                                 reinterpret_cast<float*>(d + oo), p.d_err, s,
-                                 (long long)(e0 / block));
-      });
-  if (st) return st;
-  return read_errors(p, AGQ_OP_ACCUMULATE);
+  return run_sync(accumulate_spec(codes, scales, n, block, local, precision), out_codes,
+                  out_scales);
+}
+
+agq_status agq_quantize_host_begin(const float* x, uint64_t n, int bits, uint32_t block,
+                                   int codec, agq_host_job** job) {
+  if (!job) return set_error(AGQ_ERR_INVALID_ARGUMENT, "agq_*_host_begin: null job");
+  *job = nullptr;
+  if (agq_status st = check_args(bits, block, codec)) return st;
+  if (agq_status st = check_device()) return st;
+  if (n == 0) return AGQ_OK;
+  return run_begin(quantize_spec(x, n, bits, block, codec), job);
+}
+
+agq_status agq_dequantize_host_begin(const uint8_t* codes, const float* scales, uint64_t n,
+                                     int bits, uint32_t block, int codec, agq_host_job** job) {
+  if (!job) return set_error(AGQ_ERR_INVALID_ARGUMENT, "agq_*_host_begin: null job");
+  *job = nullptr;
+  if (agq_status st = check_args(bits, block, codec)) return st;
+  if (agq_status st = check_device()) return st;
+  if (n == 0) return AGQ_OK;
+  return run_begin(dequantize_spec(codes, scales, n, bits, block, codec), job);
+}
+
+agq_status agq_roundtrip_host_begin(const float* x, uint64_t n, int bits, uint32_t block,
+                                    int codec, agq_host_job** job) {
+  if (!job) return set_error(AGQ_ERR_INVALID_ARGUMENT, "agq_*_host_begin: null job");
+  *job = nullptr;
+  if (agq_status st = check_args(bits, block, codec)) return st;
+  if (agq_status st = check_device()) return st;
+  if (n == 0) return AGQ_OK;
+  return run_begin(roundtrip_spec(x, n, bits, block, codec), job);
+}
+
+agq_status agq_local_accumulate_host_begin(const uint8_t* codes, const float* scales, uint64_t n,
+                                           uint32_t block, const float* local, int precision,
+                                           agq_host_job** job) {
+  if (!job) return set_error(AGQ_ERR_INVALID_ARGUMENT, "agq_*_host_begin: null job");
+  *job = nullptr;
+  if (agq_status st = check_args(8, block, AGQ_CODEC_FP8_E4M3)) return st;
+  if (agq_status st = check_device()) return st;
+  if (n == 0) return AGQ_OK;
+  return run_begin(accumulate_spec(codes, scales, n, block, local, precision), job);
+}
+
+agq_status agq_host_job_finish(agq_host_job* job, void* out0, void* out1) {
+  if (!job) return AGQ_OK;
+  std::unique_ptr<agq_host_job> j(job);
+  if (!out0) {  // cancelled: drain the work, keep the pipeline consistent
+    for (uint64_t k = 0; k < j->outs.size(); ++k) cudaEventSynchronize(j->lease.p->cev[k]);
+    return AGQ_OK;
+  }
+  char* base[2] = {static_cast<char*>(out0), static_cast<char*>(out1)};
+  if (agq_status st = job_finish(*j, base)) return st;
+  return read_errors(*j->lease.p, j->op);
 }
 
 agq_status agq_allreduce_simulated_host(int world, const uint8_t* const* codes,

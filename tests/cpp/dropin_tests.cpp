@@ -325,11 +325,76 @@ static void dbca_cases() {
   CHECK(throws<std::invalid_argument>([&] { stage_policy(plan, 9); }));
 }
 
+// The API's begin/finish host jobs (agq_*_host_begin + agq_host_job_finish):
+// multi-chunk ragged sizes equal the oracle and the synchronous entries,
+// errors surface at finish with the synchronous text, cancel leaves the
+// pipeline usable, oversize calls fall back to the synchronous entry.
+static void host_job_cases() {
+  const std::size_t n = (5u << 20) + 77;  // 3 pipeline chunks, ragged tail
+  const auto x = gauss(n, 11);
+  for (CodecKind k : kKinds) {
+    const int b = bits_for(k, 5);
+    const auto q = quantize_blockwise(x, b, 128, k);
+    std::vector<std::uint8_t> oc(n);
+    std::vector<float> os(q.scales.size()), od(n), back(n);
+    char err[256];
+    CHECK(oracle_quantize(x.data(), n, b, 128, static_cast<int>(k), oc.data(), os.data(), err,
+                          sizeof err) == 0);
+    CHECK(q.codes == oc && q.scales == os);
+    CHECK(oracle_dequantize(oc.data(), os.data(), n, b, 128, static_cast<int>(k), od.data(), err,
+                            sizeof err) == 0);
+    CHECK(dequantize_blockwise(q) == od);
+    CHECK(agq_dequantize_host(q.codes.data(), q.scales.data(), n, b, 128, static_cast<int>(k),
+                              back.data()) == AGQ_OK);
+    CHECK(back == od);
+    const auto rd = roundtrip_relative_delta(x, b, 128, k);
+    CHECK(rd.size() == n && rd[n - 1] == (x[n - 1] == 0.0f ? 0.0
+              : (static_cast<double>(od[n - 1]) - x[n - 1]) / static_cast<double>(x[n - 1])));
+  }
+  {  // FP8 local accumulate, multi-chunk
+    const auto g = gauss(n, 12, 1e-3f), l = gauss(n, 13, 1e-3f);
+    const auto main = quantize_blockwise(g, 8, 128, CodecKind::Fp8E4M3);
+    const auto acc = local_accumulate(main, l);
+    std::vector<std::uint8_t> oc(n);
+    std::vector<float> os(main.scales.size());
+    char err[256];
+    CHECK(oracle_local_accumulate(main.codes.data(), main.scales.data(), n, 128, l.data(), 0,
+                                  oc.data(), os.data(), err, sizeof err) == 0);
+    CHECK(acc.codes == oc && acc.scales == os && acc.shape == main.shape &&
+          acc.codec_kind == CodecKind::Fp8E4M3 && acc.bit_width == 8);
+  }
+  {  // errors at finish carry the synchronous entry's text
+    auto q = quantize_blockwise(x, 4);
+    q.scales[7] = -1.0f;
+    CHECK(throws<std::invalid_argument>([&] { dequantize_blockwise(q); }, "bad scale at block 7"));
+    std::vector<float> bad(x.begin(), x.begin() + 4096);
+    bad[300] = NAN;
+    CHECK(throws<std::invalid_argument>([&] { quantize_blockwise(bad, 4); }, "non-finite input element in block 2"));
+  }
+  {  // cancel, then the next call still runs
+    agq_host_job* job = nullptr;
+    CHECK(agq_quantize_host_begin(x.data(), n, 4, 128, 0, &job) == AGQ_OK && job != nullptr);
+    CHECK(agq_host_job_finish(job, nullptr, nullptr) == AGQ_OK);
+    CHECK(quantize_blockwise(x, 4).codes == quantize_blockwise(x, 4).codes);
+  }
+  {  // n == 0 and oversize calls: no job, nothing issued
+    agq_host_job* job = reinterpret_cast<agq_host_job*>(1);
+    CHECK(agq_quantize_host_begin(x.data(), 0, 4, 128, 0, &job) == AGQ_OK && job == nullptr);
+    const std::size_t big = 56u << 20;  // 28 chunks x 10.06 MiB of staging > 256 MiB
+    std::vector<float> xb(big, 0.5f);
+    job = reinterpret_cast<agq_host_job*>(1);
+    CHECK(agq_quantize_host_begin(xb.data(), big, 4, 128, 0, &job) == AGQ_OK && job == nullptr);
+    const auto qb = quantize_blockwise(xb, 4);  // the synchronous fallback
+    CHECK(qb.codes[big - 1] == 14 && qb.scales.back() == 0.5f);
+  }
+}
+
 int main() {
   fp8_scalars();
   codec_cases();
   collective_cases();
   dbca_cases();
+  host_job_cases();
   std::printf("dropin_tests: %d checks, %d failures\n", g_checks, g_fail);
   return g_fail;
 }

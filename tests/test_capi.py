@@ -31,6 +31,21 @@ def test_exports_every_declared_symbol():
     assert set(syms) == set(L.EXPORTED)
 
 
+@pytest.mark.parametrize("nbytes", [0, 17, 65536 + 3, (5 << 20) + 11])
+def test_host_copy(nbytes):
+    """agq_host_copy: the staging copy of the host pipelines (copy threads,
+    streaming stores, ragged head/tail) — pure host code."""
+    rng = np.random.default_rng(nbytes)
+    src = rng.integers(0, 256, nbytes + 64, dtype=np.uint8)
+    dst = np.zeros_like(src)
+    # odd offsets: unaligned head and tail around the streaming body
+    L.check(L.lib.agq_host_copy(dst.ctypes.data + 1, src.ctypes.data + 3, nbytes))
+    assert np.array_equal(dst[1:1 + nbytes], src[3:3 + nbytes])
+    assert not dst[0] and not dst[1 + nbytes:].any()
+    if nbytes:
+        assert L.lib.agq_host_copy(None, src.ctypes.data, nbytes) != 0
+
+
 def test_library_is_sm100a_only():
     out = os.popen(f"cuobjdump --list-elf {L.LIB_PATH} 2>/dev/null").read()
     assert "sm_100a" in out

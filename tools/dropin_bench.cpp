@@ -59,27 +59,79 @@ int main(int argc, char** argv) {
   auto q = agq::quantize_blockwise(x, 4);
   auto back = agq::dequantize_blockwise(q);
   const int reps = 15;
-  double st[4];
-  agq_host_pipeline_stats(st, 1);
   const double tq = median_time([&] { q = agq::quantize_blockwise(x, 4); }, reps);
-  double sq[4];
-  agq_host_pipeline_stats(sq, 1);
   const double td = median_time([&] { back = agq::dequantize_blockwise(q); }, reps);
-  double sd[4];
-  agq_host_pipeline_stats(sd, 1);
   // the C-ABI host entry points into caller-owned (warm) buffers: the
   // library's path without the API's result-vector construction
   std::vector<uint8_t> pc(n);
   std::vector<float> pscales(n / 128), pout(n);
+  double st[4], sq[4], sd[4];
+  agq_host_pipeline_stats(st, 1);
   const double tq_abi = median_time([&] {
     agq_quantize_host(x.data(), n, 4, 128, 0, pc.data(), pscales.data());
   }, reps);
+  agq_host_pipeline_stats(sq, 1);
   const double td_abi = median_time([&] {
     agq_dequantize_host(pc.data(), pscales.data(), n, 4, 128, 0, pout.data());
   }, reps);
+  agq_host_pipeline_stats(sd, 1);
+  // the staging copy rate the pipelines run at (caller memory -> other
+  // memory through the library's copy threads): the host-memory bound
+  const double t_copy = median_time([&] { agq_host_copy(pout.data(), x.data(), 4 * n); }, reps);
   // what the API's value-initialised result vectors cost on this host alone
   const double t_alloc_f32 = median_time([&] { std::vector<float> v(n); asm volatile("" ::"r"(v.data()) : "memory"); }, reps);
   const double t_alloc_u8 = median_time([&] { std::vector<uint8_t> v(n); asm volatile("" ::"r"(v.data()) : "memory"); }, reps);
+
+  // where the API's dequantize time goes: the same steps as
+  // dequantize_blockwise, timed one by one
+  double parts[3] = {0, 0, 0};
+  for (int r = 0; r < reps; ++r) {
+    const double t0 = now();
+    std::vector<float> v(n);
+    const double t1 = now();
+    agq_dequantize_host(q.codes.data(), q.scales.data(), n, 4, 128, 0, v.data());
+    const double t2 = now();
+    back = std::move(v);
+    const double t3 = now();
+    parts[0] += t1 - t0;
+    parts[1] += t2 - t1;
+    parts[2] += t3 - t2;
+  }
+
+  // the same with the split entry the API uses (begin, zero, finish)
+  double jparts[3] = {0, 0, 0};
+  for (int r = 0; r < reps; ++r) {
+    const double t0 = now();
+    agq_host_job* job = nullptr;
+    agq_dequantize_host_begin(q.codes.data(), q.scales.data(), n, 4, 128, 0, &job);
+    const double t1 = now();
+    std::vector<float> v(n);
+    const double t2 = now();
+    agq_host_job_finish(job, v.data(), nullptr);
+    const double t3 = now();
+    back = std::move(v);
+    jparts[0] += t1 - t0;
+    jparts[1] += t2 - t1;
+    jparts[2] += t3 - t2;
+  }
+
+  double qparts[3] = {0, 0, 0};
+  for (int r = 0; r < reps; ++r) {
+    const double t0 = now();
+    agq_host_job* job = nullptr;
+    agq_quantize_host_begin(x.data(), n, 4, 128, 0, &job);
+    const double t1 = now();
+    agq::QuantizedTensor t;
+    t.codes.resize(n);
+    t.scales.resize(n / 128);
+    const double t2 = now();
+    agq_host_job_finish(job, t.codes.data(), t.scales.data());
+    const double t3 = now();
+    q = std::move(t);
+    qparts[0] += t1 - t0;
+    qparts[1] += t2 - t1;
+    qparts[2] += t3 - t2;
+  }
 
   // FP8 local_accumulate: 2^24-element gradient, FP32 local
   const std::size_t na = 1u << 24;
@@ -128,14 +180,21 @@ int main(int argc, char** argv) {
       "\"accumulate_h2d_bytes\": %.0f, \"accumulate_d2h_bytes\": %.0f, "
       "\"ref_quantize_ms\": %.3f, \"ref_dequantize_ms\": %.3f, \"ref_accumulate_ms\": %.3f, "
       "\"ref_threads\": 1, \"allocator\": \"glibc heap, no mmap/trim (vectors reused, both arms)\", "
-      "\"pipeline_quantize_ms\": {\"inside\": %.3f, \"host_copies\": %.3f, \"wait_device\": %.3f}, "
-      "\"pipeline_dequantize_ms\": {\"inside\": %.3f, \"host_copies\": %.3f, \"wait_device\": %.3f}, "
+      "\"abi_pipeline_quantize_ms\": {\"inside\": %.3f, \"host_copies\": %.3f, \"wait_device\": %.3f}, "
+      "\"abi_pipeline_dequantize_ms\": {\"inside\": %.3f, \"host_copies\": %.3f, \"wait_device\": %.3f}, "
       "\"alloc_zero_f32_ms\": %.3f, \"alloc_zero_u8_ms\": %.3f, "
       "\"abi_quantize_host_ms\": %.3f, \"abi_dequantize_host_ms\": %.3f, "
+      "\"host_copy_GBs\": %.2f, "
+      "\"api_dequantize_parts_ms\": {\"alloc_zero\": %.3f, \"host_call\": %.3f, \"assign_free\": %.3f}, "
+      "\"api_dequantize_job_parts_ms\": {\"begin\": %.3f, \"alloc_zero\": %.3f, \"finish\": %.3f}, "
+      "\"api_quantize_job_parts_ms\": {\"begin\": %.3f, \"alloc_zero\": %.3f, \"finish\": %.3f}, "
       "\"quantize_bitexact_vs_ref\": %s, \"bitexact_vs_ref\": %s, \"accumulate_bitexact_vs_ref\": %s}\n",
       n, tq * 1e3, td * 1e3, (tq + td) * 1e3, ta * 1e3, q_h2d, q_d2h, d_h2d, d_d2h, a_h2d, a_d2h,
       rq * 1e3, rd * 1e3, ra * 1e3, sq[0] * 1e3 / reps, sq[1] * 1e3 / reps,
       sq[2] * 1e3 / reps, sd[0] * 1e3 / reps, sd[1] * 1e3 / reps, sd[2] * 1e3 / reps,
-      t_alloc_f32 * 1e3, t_alloc_u8 * 1e3, tq_abi * 1e3, td_abi * 1e3, same_q ? "true" : "false", same ? "true" : "false", same_acc ? "true" : "false");
+      t_alloc_f32 * 1e3, t_alloc_u8 * 1e3, tq_abi * 1e3, td_abi * 1e3,
+      4.0 * n / t_copy / 1e9, parts[0] * 1e3 / reps, parts[1] * 1e3 / reps, parts[2] * 1e3 / reps,
+      jparts[0] * 1e3 / reps, jparts[1] * 1e3 / reps, jparts[2] * 1e3 / reps,
+      qparts[0] * 1e3 / reps, qparts[1] * 1e3 / reps, qparts[2] * 1e3 / reps, same_q ? "true" : "false", same ? "true" : "false", same_acc ? "true" : "false");
   return 0;
 }

@@ -150,6 +150,14 @@ __device__ __forceinline__ uint4 ldg128_stream(const void* p) {
                : "l"(p));
   return v;
 }
+// 256-bit streaming load (LDG.E.ENL2.256, sm_100): one lane's 32 contiguous
+// bytes, so a warp reads 1 KB per instruction without shared-memory staging.
+__device__ __forceinline__ void ldg256_stream(const void* p, uint32_t* w) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]),
+                 "=r"(w[6]), "=r"(w[7])
+               : "l"(p));
+}
 // Volatile-free 128-bit load for peer-mapped memory written by other GPUs in
 // this kernel's lifetime (no .nc: must observe the remote writes).
 __device__ __forceinline__ uint4 ldg128_relaxed(const void* p) {

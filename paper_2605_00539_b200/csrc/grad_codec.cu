@@ -23,41 +23,26 @@ namespace agqk {
 
 // ---------------------------------------------------------------------------
 // K3: each warp streams 512-element tiles
-// (16 per lane, 8 lanes per 128-block). Codes (16 B/lane) and the block
-// scale are loaded straight to registers; the local gradient is loaded with
-// coalesced 128-bit loads into a private swizzled shared slot so each lane
-// reads its 16 consecutive values conflict-free. The next tile is prefetched
-// into registers while the current one is computed. No CTA-wide barrier.
+// (16 per lane, 8 lanes per 128-block). Codes (16 B/lane), the block scale
+// and the lane's 16 local values (one or two 256-bit loads: 32 B of BF16 or
+// 64 B of FP32, every 32-byte sector read once) are loaded straight to
+// registers, the next tile's while the current one is computed. No shared-
+// memory staging and no CTA-wide barrier.
 // ---------------------------------------------------------------------------
 constexpr int kAccWarpElems = 512;
 constexpr int kAccWarps = 8;
 
-template <int kCh>  // 16-byte chunks per lane row: 4 (f32) or 2 (bf16)
-__device__ __forceinline__ uint32_t acc_swz(uint32_t row, uint32_t c) {
-  const uint32_t rot = kCh == 4 ? (row >> 1) : (row >> 2);
-  return row * (kCh * 16) + ((c + rot) & (kCh - 1)) * 16;
-}
-
 // A non-finite block sum: a non-finite local gradient makes it so; tell the
 // two reference errors apart (collective.hpp:138-139 vs the requant's block
-// error) by re-reading this lane's local values from the warp's staging slot.
+// error) by re-reading this lane's 16 local values.
 template <bool BF16L>
-__device__ __noinline__ void acc_report_nonfinite(const unsigned char* wb, int lane, uint64_t t,
+__device__ __noinline__ void acc_report_nonfinite(const unsigned char* lp, int lane, uint64_t t,
                                                   uint64_t gblk, long long eb, agq_errors* err) {
-  constexpr int kCh = BF16L ? 2 : 4;
   uint32_t lbad = 0;
-  for (int j = 0; j < kCh; ++j) {
-    const uint4 v = lds128(wb + acc_swz<kCh>(lane, j));
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    for (int k = 0; k < 4; ++k) {
-      if constexpr (BF16L) {
-        const uint32_t lo = w[k] << 16, hi = w[k] & 0xffff0000u;
-        lbad |= (uint32_t)((lo & 0x7f800000u) == 0x7f800000u) << (8 * j + 2 * k);
-        lbad |= (uint32_t)((hi & 0x7f800000u) == 0x7f800000u) << (8 * j + 2 * k + 1);
-      } else {
-        lbad |= (uint32_t)((w[k] & 0x7f800000u) == 0x7f800000u) << (4 * j + k);
-      }
-    }
+  for (int e = 0; e < 16; ++e) {
+    const uint32_t u = BF16L ? (uint32_t)reinterpret_cast<const uint16_t*>(lp)[e] << 16
+                             : reinterpret_cast<const uint32_t*>(lp)[e];
+    lbad |= (uint32_t)((u & 0x7f800000u) == 0x7f800000u) << e;
   }
   if (lbad)
     err_min(&err->nonfinite_local,
@@ -72,73 +57,46 @@ __global__ void __launch_bounds__(kAccWarps * 32, 3)
                       uint64_t ntiles, uint8_t* out_codes, float* out_scales, long long eb,
                       agq_errors* err) {
   // eb: block index of element 0 in the error record (chunked host calls)
-  constexpr int kCh = BF16L ? 2 : 4;
-  constexpr uint32_t kRowB = kCh * 16;
+  constexpr int kLW = BF16L ? 8 : 16;  // 32-bit words of local gradient per lane
   constexpr uint32_t kLocTileB = kAccWarpElems * (BF16L ? 2 : 4);  // 1 KB / 2 KB
-  __shared__ __align__(16) unsigned char sbuf[kAccWarps][kLocTileB];
   __shared__ double t16[kDqTable];
   __shared__ float btab[kAccWarps][32];  // per warp: 4 blocks x 8 table entries
   fill_fp8_dq_table(t16);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wb = sbuf[warp];
   const double t8 = fp8_t8(lane & 7);  // lane 8b+j builds entry j of block b
   const uint32_t mytab = (uint32_t)__cvta_generic_to_shared(&btab[warp][lane & ~7]);
   const uint64_t nw = (uint64_t)gridDim.x * kAccWarps;
   uint64_t t = (uint64_t)blockIdx.x * kAccWarps + warp;
-  const unsigned char* lbase = static_cast<const unsigned char*>(local);
+  const unsigned char* lbase = static_cast<const unsigned char*>(local) + lane * (kLW * 4);
 
-  // Tiles in flight per warp: a BF16-local tile is 1.5 KB, so two are kept
-  // in flight to cover the memory latency (24 warps x 2 x 1.5 KB per SM);
-  // an FP32-local tile (2.5 KB) needs one.
-  constexpr int kPf = 1;
-  uint4 pc[kPf];       // 16 codes
-  float ps[kPf];       // block scale
-  uint4 pl[kPf][kCh];  // local gradient chunks (coalesced layout)
-  auto load = [&](uint64_t tt, int d) {
-    pc[d] = ldg128_stream(codes + tt * kAccWarpElems + lane * 16);
-    ps[d] = __ldg(scales + tt * 4 + (lane >> 3));
+  // one tile in flight per warp beyond the one being computed
+  uint4 pc;             // 16 codes
+  float ps;             // block scale
+  uint32_t pl[kLW];     // 16 local values
+  auto load = [&](uint64_t tt) {
+    pc = ldg128_stream(codes + tt * kAccWarpElems + lane * 16);
+    ps = __ldg(scales + tt * 4 + (lane >> 3));
 #pragma unroll
-    for (int j = 0; j < kCh; ++j) pl[d][j] = ldg128_stream(lbase + tt * kLocTileB + j * 512 + lane * 16);
+    for (int h = 0; h < kLW / 8; ++h) ldg256_stream(lbase + tt * kLocTileB + h * 32, pl + 8 * h);
   };
-#pragma unroll
-  for (int d = 0; d < kPf; ++d)
-    if (t + d * nw < ntiles) load(t + d * nw, d);
+  if (t < ntiles) load(t);
   for (; t < ntiles; t += nw) {
-#pragma unroll
-    for (int j = 0; j < kCh; ++j) {
-      const uint32_t o = j * 512 + lane * 16;
-      sts128(wb + acc_swz<kCh>(o / kRowB, (o / 16) & (kCh - 1)), pl[0][j]);
-    }
-    const uint32_t cw[4] = {pc[0].x, pc[0].y, pc[0].z, pc[0].w};
-    const float sc = ps[0];
-    btab[warp][lane] = fp8_tab_entry_f16(t8, sc);  // T[M] (dq_f16_accum)
-    __syncwarp();
-#pragma unroll
-    for (int d = 0; d + 1 < kPf; ++d) {  // shift the queue (register renames)
-      pc[d] = pc[d + 1];
-      ps[d] = ps[d + 1];
-#pragma unroll
-      for (int j = 0; j < kCh; ++j) pl[d][j] = pl[d + 1][j];
-    }
-    if (t + kPf * nw < ntiles) load(t + kPf * nw, kPf - 1);
+    const uint32_t cw[4] = {pc.x, pc.y, pc.z, pc.w};
+    const float sc = ps;
     float l[16];
 #pragma unroll
-    for (int j = 0; j < kCh; ++j) {
-      const uint4 v = lds128(wb + acc_swz<kCh>(lane, j));
+    for (int k = 0; k < kLW; ++k) {
       if constexpr (BF16L) {
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          l[8 * j + 2 * k] = u2f(w[k] << 16);
-          l[8 * j + 2 * k + 1] = u2f(w[k] & 0xffff0000u);
-        }
+        l[2 * k] = u2f(pl[k] << 16);
+        l[2 * k + 1] = u2f(pl[k] & 0xffff0000u);
       } else {
-        l[4 * j] = u2f(v.x); l[4 * j + 1] = u2f(v.y);
-        l[4 * j + 2] = u2f(v.z); l[4 * j + 3] = u2f(v.w);
+        l[k] = u2f(pl[k]);
       }
     }
+    btab[warp][lane] = fp8_tab_entry_f16(t8, sc);  // T[M] (dq_f16_accum)
     __syncwarp();
+    if (t + nw < ntiles) load(t + nw);
     const uint64_t gblk = t * 4 + (lane >> 3);
     if ((!(sc >= 0.0f) || !(sc <= 3.402823466e38f)) && (lane & 7) == 0)
       err_min(&err->bad_scale_block, eb + (long long)gblk);
@@ -164,14 +122,14 @@ __global__ void __launch_bounds__(kAccWarps * 32, 3)
     const uint32_t mr = absmax_bits16(v);
     const uint32_t m = f2u(apply_prec<PREC>(u2f(mr)));
     if (mr >= 0x7f800000u || m >= 0x7f800000u)  // rare: out of line, not if-converted
-      acc_report_nonfinite<BF16L>(wb, lane, t, gblk, eb, err);
+      acc_report_nonfinite<BF16L>(lbase + t * kLocTileB, lane, t, gblk, eb, err);
     if constexpr (PREC != AGQ_ACC_FP32) round_pairs16<PREC>(v);
     uint32_t ow[4];
     fp8_requant16(v, u2f(m), ow);
     *reinterpret_cast<uint4*>(out_codes + t * kAccWarpElems + lane * 16) =
         make_uint4(ow[0], ow[1], ow[2], ow[3]);
     if ((lane & 7) == 0) out_scales[gblk] = u2f(m);
-    __syncwarp();  // the staging slot may still be read by the rare path
+    __syncwarp();  // btab is rewritten by the next tile
   }
 }
 

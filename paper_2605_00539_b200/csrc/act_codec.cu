@@ -6,10 +6,10 @@
 // dequantize_blockwise + pack_codes (tests/test_gpu_codec.py).
 //
 // Fast path (block 128, 16-byte aligned buffers, whole 1024-element warp
-// tiles): warp-autonomous persistent kernels. Each warp streams its own tiles
-// with coalesced 128-bit loads (next tile in flight in registers), staged
-// through a private swizzled 2/4 KB shared slot so each lane owns 32
-// consecutive elements (4 lanes per 128-element block): two shuffles give the
+// tiles): warp-autonomous persistent kernels. Each warp streams its own tiles;
+// each lane loads its 32 consecutive elements with 256-bit loads (next tile
+// in flight in registers; every 32-byte sector read once, no shared-memory
+// staging), 4 lanes per 128-element block: two shuffles give the
 // block absmax and a lane's 32 codes are exactly `bits` 32-bit words of the
 // packed stream. No CTA-wide barrier. (CTA-wide TMA bulk-copy, per-warp TMA
 // and cp.async rings were built, verified bit-exact and measured slower:
@@ -119,11 +119,11 @@ __device__ __forceinline__ void encode_linear_bf16_words(const uint4 (&ch)[4], c
 
 // ---------------------------------------------------------------------------
 // K1 (warp-autonomous variant): every warp streams its own 1024-element tiles
-// — coalesced 128-bit global loads (next tile prefetched into registers while
-// the current one is encoded), staged through a private 2 KB shared-memory
-// slot so each lane reads its 32 consecutive elements conflict-free, codes
-// written straight from registers (PACK 32-bit words per lane, contiguous per
-// warp). No CTA-wide barrier anywhere; only __syncwarp.
+// — each lane's 32 consecutive elements by 256-bit loads (next tile
+// prefetched into registers while the current one is encoded), codes written
+// straight from registers (PACK 32-bit words per lane, contiguous per warp).
+// No shared memory, no barrier. (Round 1 staged coalesced 128-bit loads
+// through a swizzled shared slot: 3% slower, profiles/r02_act_ldg256.log.)
 // ---------------------------------------------------------------------------
 constexpr int kWarpElems = 1024;
 constexpr int kWarpsPerCta = 8;
@@ -131,22 +131,6 @@ constexpr int kWarpsPerCta = 8;
 // profiles/r01_microbench_act_minb*); FP32-I/O instances run at 2.
 constexpr int kQuantMinB = 3;
 constexpr int kDequantMinB = 3;
-
-// Shared-memory swizzle of a warp tile: lane row r (32 elements = kChunks
-// 16-byte chunks) keeps chunk c at slot (c + rot(r)) mod kChunks, so the
-// coalesced writes (8 lanes = one 128-byte phase) and the per-row reads
-// (8 rows, same chunk) are both bank-conflict free, and every lane sees its
-// own row in natural order.
-template <int kChunks>
-__device__ __forceinline__ uint32_t swz_off(uint32_t row, uint32_t c) {
-  const uint32_t rot = kChunks == 4 ? (row >> 1) : row;
-  return row * (kChunks * 16) + ((c + rot) & (kChunks - 1)) * 16;
-}
-// Byte offset in the swizzled tile of the 16-byte chunk at natural offset `o`.
-template <int kChunks>
-__device__ __forceinline__ uint32_t swz_of_linear(uint32_t o) {
-  return swz_off<kChunks>(o / (kChunks * 16), (o / 16) & (kChunks - 1));
-}
 
 struct TileRef {
   int g;
@@ -334,17 +318,23 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32,
   using TR = InTraits<Tin>;
   constexpr int kChunks = TR::kChunks;
   constexpr uint32_t kTileB = kWarpElems * sizeof(Tin);    // 2 KB / 4 KB
-  __shared__ __align__(16) unsigned char sbuf[kWarpsPerCta][kTileB];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wb = sbuf[warp];
   const uint64_t total = st.tile_begin[st.nseg];
   const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
   uint64_t t = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
 
+  // the lane's row (32 consecutive values: 64 or 128 B) with 256-bit loads;
+  // every 32-byte sector of the tile is read once
   auto load = [&](TileRef tr, uint4 (&buf)[kChunks]) {
-    const unsigned char* src = static_cast<const unsigned char*>(st.src[tr.g]) + tr.lt * kTileB;
+    const unsigned char* src = static_cast<const unsigned char*>(st.src[tr.g]) + tr.lt * kTileB +
+                               lane * (kChunks * 16);
 #pragma unroll
-    for (int j = 0; j < kChunks; ++j) buf[j] = ldg128_stream(src + j * 512 + lane * 16);
+    for (int h = 0; h < kChunks / 2; ++h) {
+      uint32_t w[8];
+      ldg256_stream(src + 32 * h, w);
+      buf[2 * h] = make_uint4(w[0], w[1], w[2], w[3]);
+      buf[2 * h + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+    }
   };
   constexpr int kPf = kQuantPrefetch;  // tiles in flight per warp (registers)
   uint4 buf[kPf][kChunks];
@@ -359,9 +349,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32,
     }
   }
   for (; t < total; t += nw) {
+    uint4 ch[kChunks];
 #pragma unroll
-    for (int j = 0; j < kChunks; ++j) sts128(wb + swz_of_linear<kChunks>(j * 512 + lane * 16), buf[0][j]);
-    __syncwarp();
+    for (int j = 0; j < kChunks; ++j) ch[j] = buf[0][j];
     const TileRef tr = curq[0];
 #pragma unroll
     for (int d = 0; d + 1 < kPf; ++d) {
@@ -373,11 +363,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32,
       curq[kPf - 1] = locate_from(st, t + kPf * nw, gseg);
       load(curq[kPf - 1], buf[kPf - 1]);
     }
-    uint4 ch[kChunks];
-#pragma unroll
-    for (int j = 0; j < kChunks; ++j) ch[j] = lds128(wb + swz_off<kChunks>(lane, j));
-    __syncwarp();
-
     uint32_t words[PACK];
     float a;
     quant_tile<BITS, PACK, CODEC, Tin>(st, err, tr, lane, ch, words, a);
@@ -385,8 +370,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32,
 }
 
 // K2 warp-autonomous variant: lane loads its PACK code words (+ block scale),
-// next tile prefetched, decodes 32 values, stages the 2/4 KB warp output in
-// shared memory and writes it back with coalesced 128-bit stores.
+// next tile prefetched, decodes 32 values and writes them with 256-bit
+// stores (64 or 128 contiguous bytes per lane).
 template <int BITS, int PACK, int CODEC, typename Tout>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? kDequantMinB : 2)
     k_dequant_warp(SegTable st, int validate, agq_errors* err);
@@ -488,7 +473,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? kDequan
   constexpr uint32_t kTileB = kWarpElems * sizeof(Tout);
   constexpr uint32_t kCodeB = kWarpElems * PACK / 8;
   constexpr bool kBf16Out = sizeof(Tout) == 2;
-  __shared__ __align__(16) unsigned char sbuf[kWarpsPerCta][kTileB];
   __shared__ double fp8lut[CODEC == 2 ? 128 : 1];
   // exact unit values fl64(unit(c)) for the FP32-scale path (linear / FP4):
   // one LDS.64 + DMUL + F2F per element instead of a double division
@@ -504,7 +488,6 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? kDequan
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wb = sbuf[warp];
   const uint64_t total = st.tile_begin[st.nseg];
   const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
   uint64_t t = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
@@ -608,6 +591,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? kDequan
     }
     uint64_t pk[kChunks];
     unpack_chunks<kChunkBits>(cw, pk, std::make_integer_sequence<int, kChunks>{});
+    // the lane's 32 outputs (64 or 128 B) go out as 256-bit stores
+    unsigned char* dst = static_cast<unsigned char*>(st.dst[tr.g]) + tr.lt * kTileB +
+                         lane * (kChunks * 16);
+    uint4 prev = make_uint4(0, 0, 0, 0);
 #pragma unroll
     for (int j = 0; j < kChunks; ++j) {
       float v[kPerChunk];
@@ -661,15 +648,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? kDequan
       } else {
         o = make_uint4(f2u(v[0]), f2u(v[1]), f2u(v[2]), f2u(v[3]));
       }
-      sts128(wb + swz_off<kChunks>(lane, j), o);
+      if (j & 1)
+        stg256(dst + (j >> 1) * 32, prev, o);
+      else
+        prev = o;
     }
-    __syncwarp();
-    unsigned char* dst = static_cast<unsigned char*>(st.dst[tr.g]) + tr.lt * kTileB;
-#pragma unroll
-    for (int j = 0; j < kChunks; ++j)
-      *reinterpret_cast<uint4*>(dst + j * 512 + lane * 16) =
-          lds128(wb + swz_of_linear<kChunks>(j * 512 + lane * 16));
-    __syncwarp();
   }
 }
 
@@ -697,16 +680,20 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, AGQ_RT_MINB)
   using Tin = __nv_bfloat16;
   constexpr int kChunks = 4;
   constexpr uint32_t kTileB = kWarpElems * 2;
-  __shared__ __align__(16) unsigned char sbuf[kWarpsPerCta][kTileB];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* wb = sbuf[warp];
   const uint64_t total = st.tile_begin[st.nseg];
   const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
   uint64_t t = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
-  auto load = [&](TileRef tr, uint4 (&buf)[kChunks]) {
-    const unsigned char* src = static_cast<const unsigned char*>(st.src[tr.g]) + tr.lt * kTileB;
+  auto load = [&](TileRef tr, uint4 (&buf)[kChunks]) {  // the lane's 64-byte row
+    const unsigned char* src = static_cast<const unsigned char*>(st.src[tr.g]) + tr.lt * kTileB +
+                               lane * 64;
 #pragma unroll
-    for (int j = 0; j < kChunks; ++j) buf[j] = ldg128_stream(src + j * 512 + lane * 16);
+    for (int h = 0; h < 2; ++h) {
+      uint32_t w[8];
+      ldg256_stream(src + 32 * h, w);
+      buf[2 * h] = make_uint4(w[0], w[1], w[2], w[3]);
+      buf[2 * h + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+    }
   };
   uint4 buf[kChunks];
   TileRef nxt{0, 0};
@@ -716,23 +703,21 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, AGQ_RT_MINB)
     load(nxt, buf);
   }
   for (; t < total; t += nw) {
+    uint4 ch[kChunks];
 #pragma unroll
-    for (int j = 0; j < kChunks; ++j) sts128(wb + swz_of_linear<kChunks>(j * 512 + lane * 16), buf[j]);
-    __syncwarp();
+    for (int j = 0; j < kChunks; ++j) ch[j] = buf[j];
     const TileRef tr = nxt;
     if (t + nw < total) {
       nxt = locate_from(st, t + nw, gseg);
       load(nxt, buf);
     }
-    uint4 ch[kChunks];
-#pragma unroll
-    for (int j = 0; j < kChunks; ++j) ch[j] = lds128(wb + swz_off<kChunks>(lane, j));
-    __syncwarp();
     uint32_t words[BITS];
     float a;
     quant_tile<BITS, BITS, 0, Tin>(st, err, tr, lane, ch, words, a);
-    // the reconstruction of this lane's 32 codes, staged for coalesced stores
+    // the reconstruction of this lane's 32 codes: two 256-bit stores
     const bool fast = fast_scale(a);  // a is BF16-valued (absmax of BF16 values)
+    unsigned char* dst = static_cast<unsigned char*>(st.dst[tr.g]) + tr.lt * kTileB + lane * 64;
+    uint4 prev = make_uint4(0, 0, 0, 0);
 #pragma unroll
     for (int j = 0; j < kChunks; ++j) {
       float v[8];
@@ -749,15 +734,12 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, AGQ_RT_MINB)
         __nv_bfloat162 b2 = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
         h[k] = *reinterpret_cast<uint32_t*>(&b2);
       }
-      sts128(wb + swz_off<kChunks>(lane, j), make_uint4(h[0], h[1], h[2], h[3]));
+      const uint4 o = make_uint4(h[0], h[1], h[2], h[3]);
+      if (j & 1)
+        stg256(dst + (j >> 1) * 32, prev, o);
+      else
+        prev = o;
     }
-    __syncwarp();
-    unsigned char* dst = static_cast<unsigned char*>(st.dst[tr.g]) + tr.lt * kTileB;
-#pragma unroll
-    for (int j = 0; j < kChunks; ++j)
-      *reinterpret_cast<uint4*>(dst + j * 512 + lane * 16) =
-          lds128(wb + swz_of_linear<kChunks>(j * 512 + lane * 16));
-    __syncwarp();
   }
 }
 

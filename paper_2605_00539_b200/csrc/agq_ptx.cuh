@@ -158,6 +158,12 @@ __device__ __forceinline__ void ldg256_stream(const void* p, uint32_t* w) {
                  "=r"(w[6]), "=r"(w[7])
                : "l"(p));
 }
+// 256-bit store of one lane's 32 contiguous bytes (STG.E.ENL2.256).
+__device__ __forceinline__ void stg256(void* p, uint4 a, uint4 b) {
+  asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y),
+               "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
 // Volatile-free 128-bit load for peer-mapped memory written by other GPUs in
 // this kernel's lifetime (no .nc: must observe the remote writes).
 __device__ __forceinline__ uint4 ldg128_relaxed(const void* p) {

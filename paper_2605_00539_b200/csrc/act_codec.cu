@@ -128,9 +128,16 @@ __device__ __forceinline__ void encode_linear_bf16_words(const uint4 (&ch)[4], c
 constexpr int kWarpElems = 1024;
 constexpr int kWarpsPerCta = 8;
 // Resident CTAs per SM of the BF16 act kernels (measured best,
-// profiles/r01_microbench_act_minb*); FP32-I/O instances run at 2.
-constexpr int kQuantMinB = 3;
-constexpr int kDequantMinB = 3;
+// profiles/r01_microbench_act_minb*); FP32-I/O instances run at 2. The
+// macros exist only for experiment builds (Makefile `variant`).
+#ifndef AGQ_QUANT_MINB
+#define AGQ_QUANT_MINB 3
+#endif
+#ifndef AGQ_DEQUANT_MINB
+#define AGQ_DEQUANT_MINB 3
+#endif
+constexpr int kQuantMinB = AGQ_QUANT_MINB;
+constexpr int kDequantMinB = AGQ_DEQUANT_MINB;
 
 struct TileRef {
   int g;
@@ -138,9 +145,16 @@ struct TileRef {
 };
 
 // Tiles in flight per warp (profiles/r01_quant_prefetch_ab.log,
-// r01_dequant_prefetch_ab.log).
-constexpr int kQuantPrefetch = 1;
-constexpr int kDequantPrefetch = 2;
+// r01_dequant_prefetch_ab.log; dequant 2 -> 3 after the 256-bit stores:
+// b=4 dequant 103 -> 97 us on 235M elements, profiles/r02_dequant_pf_ab.log).
+#ifndef AGQ_QUANT_PF
+#define AGQ_QUANT_PF 1
+#endif
+#ifndef AGQ_DEQUANT_PF
+#define AGQ_DEQUANT_PF 3
+#endif
+constexpr int kQuantPrefetch = AGQ_QUANT_PF;
+constexpr int kDequantPrefetch = AGQ_DEQUANT_PF;
 // Incremental locate for a warp whose tiles only move forward (t += grid
 // warps): the current segment's [begin, end) tile range lives in registers,
 // so a tile costs one compare (no parameter-bank load in front of the
@@ -515,7 +529,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? kDequan
     sc = __ldg(st.scales[tr.g] + tr.lt * 8 + (lane >> 2));
   };
   // kDequantPrefetch tiles in flight per warp (codes + scale are <= 9
-  // registers per tile, so a second tile in flight is cheap and covers the
+  // registers per tile, so extra tiles in flight are cheap and cover the
   // load latency the kernel otherwise stalls on)
   constexpr int kPf = kDequantPrefetch;
   uint32_t words[kPf][PACK];

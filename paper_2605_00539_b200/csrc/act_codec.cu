@@ -5,7 +5,8 @@
 // tensor_io.hpp:63-100. Results are bit-identical to quantize_blockwise /
 // dequantize_blockwise + pack_codes (tests/test_gpu_codec.py).
 //
-// Fast path (block 128, 16-byte aligned buffers, whole 1024-element warp
+// Fast path (block 128, 32-byte aligned activations and 16-byte aligned
+// codes / scales, whole 1024-element warp
 // tiles): warp-autonomous persistent kernels. Each warp streams its own tiles;
 // each lane loads its 32 consecutive elements with 256-bit loads (next tile
 // in flight in registers; every 32-byte sector read once, no shared-memory
@@ -901,6 +902,8 @@ using namespace agqk;
 namespace {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+// the lane rows of the activations are read / written with 256-bit accesses
+bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
 
 int gen_grid(uint64_t work, int threads) {
   const uint64_t g = (work + threads - 1) / threads;
@@ -1021,7 +1024,7 @@ agq_status quantize_one(const void* x, int x_dtype, uint64_t n, int bits, uint32
   if (n == 0) return AGQ_OK;
   const int pack = layout == AGQ_CODES_PACKED ? bits : 8;
   uint64_t ntiles = 0;
-  if (block == (uint32_t)kBlock && aligned16(x) && aligned16(codes) && aligned16(scales))
+  if (block == (uint32_t)kBlock && aligned32(x) && aligned16(codes) && aligned16(scales))
     ntiles = n / (uint64_t)kWarpElems;
   if (ntiles > 0) {
     SegTable st{};
@@ -1059,7 +1062,7 @@ agq_status dequantize_one(const void* codes, int layout, const float* scales, ui
   if (n == 0) return AGQ_OK;
   const int pack = layout == AGQ_CODES_PACKED ? bits : 8;
   uint64_t ntiles = 0;
-  if (block == (uint32_t)kBlock && aligned16(out) && aligned16(codes) && aligned16(scales))
+  if (block == (uint32_t)kBlock && aligned32(out) && aligned16(codes) && aligned16(scales))
     ntiles = n / (uint64_t)kWarpElems;
   if (ntiles > 0) {
     SegTable st{};
@@ -1098,7 +1101,7 @@ agq_status dequantize_one(const void* codes, int layout, const float* scales, ui
 }
 
 bool seg_tiled(const agq_segment& g) {
-  return aligned16(g.x) && aligned16(g.codes) && aligned16(g.scales);
+  return aligned32(g.x) && aligned16(g.codes) && aligned16(g.scales);
 }
 
 // Grouped launch (the tensors one pipeline stage stores, any count): the
@@ -1203,8 +1206,8 @@ agq_status roundtrip_device(const void* x, int x_dtype, uint64_t n, int bits, ui
   if (n == 0) return AGQ_OK;
   uint64_t ntiles = 0;
   if (x_dtype == AGQ_BF16 && out_dtype == AGQ_BF16 && codec == AGQ_CODEC_SYMMETRIC_LINEAR &&
-      layout == AGQ_CODES_PACKED && block == (uint32_t)kBlock && aligned16(x) && aligned16(codes) &&
-      aligned16(scales) && aligned16(out))
+      layout == AGQ_CODES_PACKED && block == (uint32_t)kBlock && aligned32(x) && aligned16(codes) &&
+      aligned16(scales) && aligned32(out))
     ntiles = n / (uint64_t)kWarpElems;
   if (ntiles > 0) {
     SegTable st{};

@@ -449,6 +449,8 @@ using namespace agqk;
 
 namespace {
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+// K3 reads a lane's local-gradient row with 256-bit loads
+bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
 int gen_grid(uint64_t work, int threads) {
   const uint64_t g = (work + threads - 1) / threads;
   const uint64_t cap = (uint64_t)num_sms() * 16;
@@ -546,7 +548,7 @@ agq_status accumulate_device(const uint8_t* codes, const float* scales, const vo
   const bool bf16l = local_dtype == AGQ_BF16;
   const uint64_t unit = kAccWarpElems;
   uint64_t ntiles = 0;
-  if (block == (uint32_t)kBlock && aligned16(codes) && aligned16(scales) && aligned16(local) &&
+  if (block == (uint32_t)kBlock && aligned16(codes) && aligned16(scales) && aligned32(local) &&
       aligned16(oc) && aligned16(os))
     ntiles = n / unit;
   if (ntiles) {

@@ -140,6 +140,24 @@ constexpr int kWarpsPerCta = 8;
 constexpr int kQuantMinB = AGQ_QUANT_MINB;
 constexpr int kDequantMinB = AGQ_DEQUANT_MINB;
 
+// FP32 rows (128 B per lane) are moved through a private shared slot: a
+// lane's four 256-bit accesses at a 128-byte stride measured 10-20% slower
+// than coalesced 128-bit accesses + a swizzled transposition
+// (profiles/r02_f32_staging_ab.log); BF16 rows (64 B) go direct.
+// Swizzle: lane row r (kChunks 16-byte chunks) keeps chunk c at slot
+// (c + rot(r)) mod kChunks, so the coalesced side (8 lanes = one 128-byte
+// phase) and the per-row side (8 rows, same chunk) are both conflict free.
+template <int kChunks>
+__device__ __forceinline__ uint32_t swz_off(uint32_t row, uint32_t c) {
+  const uint32_t rot = kChunks == 4 ? (row >> 1) : row;
+  return row * (kChunks * 16) + ((c + rot) & (kChunks - 1)) * 16;
+}
+// Byte offset in the swizzled tile of the 16-byte chunk at natural offset `o`.
+template <int kChunks>
+__device__ __forceinline__ uint32_t swz_of_linear(uint32_t o) {
+  return swz_off<kChunks>(o / (kChunks * 16), (o / 16) & (kChunks - 1));
+}
+
 struct TileRef {
   int g;
   uint64_t lt;
@@ -333,22 +351,30 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32,
   using TR = InTraits<Tin>;
   constexpr int kChunks = TR::kChunks;
   constexpr uint32_t kTileB = kWarpElems * sizeof(Tin);    // 2 KB / 4 KB
+  constexpr bool kStaged = kChunks == 8;                    // FP32 rows
+  __shared__ __align__(16) unsigned char sbuf[kStaged ? kWarpsPerCta : 1][kStaged ? kTileB : 16];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wb = sbuf[kStaged ? warp : 0];
   const uint64_t total = st.tile_begin[st.nseg];
   const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
   uint64_t t = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
 
-  // the lane's row (32 consecutive values: 64 or 128 B) with 256-bit loads;
-  // every 32-byte sector of the tile is read once
+  // BF16: the lane's row (32 consecutive values, 64 B) with two 256-bit
+  // loads, every 32-byte sector of the tile read once; FP32: coalesced
+  // 128-bit loads, transposed through the shared slot
   auto load = [&](TileRef tr, uint4 (&buf)[kChunks]) {
-    const unsigned char* src = static_cast<const unsigned char*>(st.src[tr.g]) + tr.lt * kTileB +
-                               lane * (kChunks * 16);
+    const unsigned char* src = static_cast<const unsigned char*>(st.src[tr.g]) + tr.lt * kTileB;
+    if constexpr (kStaged) {
 #pragma unroll
-    for (int h = 0; h < kChunks / 2; ++h) {
-      uint32_t w[8];
-      ldg256_stream(src + 32 * h, w);
-      buf[2 * h] = make_uint4(w[0], w[1], w[2], w[3]);
-      buf[2 * h + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+      for (int j = 0; j < kChunks; ++j) buf[j] = ldg128_stream(src + j * 512 + lane * 16);
+    } else {
+#pragma unroll
+      for (int h = 0; h < kChunks / 2; ++h) {
+        uint32_t w[8];
+        ldg256_stream(src + lane * (kChunks * 16) + 32 * h, w);
+        buf[2 * h] = make_uint4(w[0], w[1], w[2], w[3]);
+        buf[2 * h + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+      }
     }
   };
   constexpr int kPf = kQuantPrefetch;  // tiles in flight per warp (registers)
@@ -365,8 +391,15 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32,
   }
   for (; t < total; t += nw) {
     uint4 ch[kChunks];
+    if constexpr (kStaged) {
 #pragma unroll
-    for (int j = 0; j < kChunks; ++j) ch[j] = buf[0][j];
+      for (int j = 0; j < kChunks; ++j)
+        sts128(wb + swz_of_linear<kChunks>(j * 512 + lane * 16), buf[0][j]);
+      __syncwarp();
+    } else {
+#pragma unroll
+      for (int j = 0; j < kChunks; ++j) ch[j] = buf[0][j];
+    }
     const TileRef tr = curq[0];
 #pragma unroll
     for (int d = 0; d + 1 < kPf; ++d) {
@@ -377,6 +410,11 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32,
     if (t + kPf * nw < total) {
       curq[kPf - 1] = locate_from(st, t + kPf * nw, gseg);
       load(curq[kPf - 1], buf[kPf - 1]);
+    }
+    if constexpr (kStaged) {
+#pragma unroll
+      for (int j = 0; j < kChunks; ++j) ch[j] = lds128(wb + swz_off<kChunks>(lane, j));
+      __syncwarp();
     }
     uint32_t words[PACK];
     float a;
@@ -488,6 +526,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? kDequan
   constexpr uint32_t kTileB = kWarpElems * sizeof(Tout);
   constexpr uint32_t kCodeB = kWarpElems * PACK / 8;
   constexpr bool kBf16Out = sizeof(Tout) == 2;
+  constexpr bool kStaged = !kBf16Out;  // FP32 rows: through the shared slot
+  __shared__ __align__(16) unsigned char sbuf[kStaged ? kWarpsPerCta : 1][kStaged ? kTileB : 16];
   __shared__ double fp8lut[CODEC == 2 ? 128 : 1];
   // exact unit values fl64(unit(c)) for the FP32-scale path (linear / FP4):
   // one LDS.64 + DMUL + F2F per element instead of a double division
@@ -503,6 +543,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? kDequan
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* wb = sbuf[kStaged ? warp : 0];
   const uint64_t total = st.tile_begin[st.nseg];
   const uint64_t nw = (uint64_t)gridDim.x * kWarpsPerCta;
   uint64_t t = (uint64_t)blockIdx.x * kWarpsPerCta + warp;
@@ -606,9 +647,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? kDequan
     }
     uint64_t pk[kChunks];
     unpack_chunks<kChunkBits>(cw, pk, std::make_integer_sequence<int, kChunks>{});
-    // the lane's 32 outputs (64 or 128 B) go out as 256-bit stores
-    unsigned char* dst = static_cast<unsigned char*>(st.dst[tr.g]) + tr.lt * kTileB +
-                         lane * (kChunks * 16);
+    // BF16: the lane's 32 outputs (64 B) go out as two 256-bit stores;
+    // FP32: staged, then coalesced 128-bit stores
+    unsigned char* dst = static_cast<unsigned char*>(st.dst[tr.g]) + tr.lt * kTileB;
     uint4 prev = make_uint4(0, 0, 0, 0);
 #pragma unroll
     for (int j = 0; j < kChunks; ++j) {
@@ -663,10 +704,20 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, sizeof(Tout) == 2 ? kDequan
       } else {
         o = make_uint4(f2u(v[0]), f2u(v[1]), f2u(v[2]), f2u(v[3]));
       }
-      if (j & 1)
-        stg256(dst + (j >> 1) * 32, prev, o);
+      if constexpr (kStaged)
+        sts128(wb + swz_off<kChunks>(lane, j), o);
+      else if (j & 1)
+        stg256(dst + lane * (kChunks * 16) + (j >> 1) * 32, prev, o);
       else
         prev = o;
+    }
+    if constexpr (kStaged) {
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < kChunks; ++j)
+        *reinterpret_cast<uint4*>(dst + j * 512 + lane * 16) =
+            lds128(wb + swz_of_linear<kChunks>(j * 512 + lane * 16));
+      __syncwarp();
     }
   }
 }

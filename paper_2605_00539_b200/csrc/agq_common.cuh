@@ -50,46 +50,6 @@ __device__ __forceinline__ void err_min(long long* field, long long v) {
   if (field) atomicMin(field, v);
 }
 
-// Rotate 4 values left by r (out[j] = in[(j + r) & 3]) with selects only, so
-// register arrays stay in registers.
-template <typename T>
-__device__ __forceinline__ void rotl4(T (&v)[4], int r) {
-  if (r & 1) {
-    const T t = v[0];
-    v[0] = v[1]; v[1] = v[2]; v[2] = v[3]; v[3] = t;
-  }
-  if (r & 2) {
-    T t0 = v[0], t1 = v[1];
-    v[0] = v[2]; v[1] = v[3]; v[2] = t0; v[3] = t1;
-  }
-}
-template <typename T>
-__device__ __forceinline__ void rotl8(T (&v)[8], int r) {
-  if (r & 1) {
-    const T t = v[0];
-#pragma unroll
-    for (int j = 0; j < 7; ++j) v[j] = v[j + 1];
-    v[7] = t;
-  }
-  if (r & 2) {
-    const T t0 = v[0], t1 = v[1];
-#pragma unroll
-    for (int j = 0; j < 6; ++j) v[j] = v[j + 2];
-    v[6] = t0; v[7] = t1;
-  }
-  if (r & 4) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const T t = v[j]; v[j] = v[j + 4]; v[j + 4] = t;
-    }
-  }
-}
-// Inverse rotation (out[(j + r) & 3] = in[j]).
-template <typename T>
-__device__ __forceinline__ void rotr4(T (&v)[4], int r) { rotl4(v, (4 - r) & 3); }
-template <typename T>
-__device__ __forceinline__ void rotr8(T (&v)[8], int r) { rotl8(v, (8 - r) & 7); }
-
 // OR a value of at most 64 significant bits into a little-endian word array
 // at compile-time bit offset OFF.
 template <int OFF, int NW>

@@ -203,21 +203,6 @@ __device__ __forceinline__ void fp8_requant_words(const float (&v)[4 * NW], floa
 __device__ __forceinline__ void fp8_requant16(const float (&v)[16], float a, uint32_t (&w)[4]) {
   fp8_requant_words<4>(v, a, w);
 }
-// 8-value variant (16 lanes per 128-block).
-__device__ __forceinline__ void fp8_requant8(const float (&v)[8], float a, uint32_t (&w)[2]) {
-  fp8_requant_words<2>(v, a, w);
-}
-
-__device__ __forceinline__ uint32_t absmax_bits8(const float (&v)[8]) {
-  uint32_t m = 0;
-#pragma unroll
-  for (int e = 0; e < 8; ++e) m = max(m, f2u(v[e]) & 0x7fffffffu);
-  m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
-  m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
-  m = max(m, __shfl_xor_sync(0xffffffffu, m, 4));
-  m = max(m, __shfl_xor_sync(0xffffffffu, m, 8));
-  return m;
-}
 
 // |x| bits of the block absmax: the maximum of (bits << 1) (the shift drops
 // the sign; IMAD.SHL on the FMA pipe instead of a LOP3 on the integer ALU)

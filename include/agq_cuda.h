@@ -202,7 +202,7 @@ agq_status agq_allreduce_naive_simulated(int world, const uint8_t* const* codes,
 
 /* ---- multi-GPU decomposed all-reduce (one process per GPU) --------------- */
 typedef struct agq_comm agq_comm;
-enum { AGQ_AR_NCCL = 0, AGQ_AR_FUSED_P2P = 1, AGQ_AR_PUSH_P2P = 2 };
+enum { AGQ_AR_NCCL = 0, AGQ_AR_FUSED_P2P = 1, AGQ_AR_PUSH_P2P = 2, AGQ_AR_ONESHOT_P2P = 3 };
 
 agq_status agq_comm_unique_id(unsigned char id[128]);
 /* Collective over all ranks (NCCL communicator). device = CUDA ordinal.
@@ -265,8 +265,12 @@ agq_status agq_comm_last_trace(agq_comm* comm, agq_trace_event* events, int cap,
  * reduce-requant kernel + ncclAllGather), AGQ_AR_FUSED_P2P (one kernel per
  * rank: pull pieces over NVLink, reduce, push results) or AGQ_AR_PUSH_P2P
  * (two kernels per rank, every NVLink transfer a store: scatter pieces into
- * the owners' inboxes, then reduce from local memory and push results).
- * All three give bit-identical results. */
+ * the owners' inboxes, then reduce from local memory and push results) or
+ * AGQ_AR_ONESHOT_P2P (small messages, n <= 4 Mi elements: every rank stores
+ * its whole gradient into every peer's inbox and reduces all blocks locally;
+ * one exchange, no end barrier, (P-1)x the wire bytes). All four give
+ * bit-identical results. The P2P algorithms keep their epoch on the device
+ * and allocate nothing per call, so they can be captured in a CUDA graph. */
 agq_status agq_allreduce_fp8(agq_comm* comm, uint8_t* codes, float* scales,
                              uint64_t n, uint32_t block, int algo,
                              agq_errors* d_err, agq_stream_t stream);

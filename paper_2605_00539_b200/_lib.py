@@ -16,7 +16,7 @@ AGQ_OK, AGQ_ERR_INVALID_ARGUMENT, AGQ_ERR_RUNTIME, AGQ_ERR_CUDA, AGQ_ERR_NCCL = 
 AGQ_F32, AGQ_BF16 = 0, 1
 AGQ_CODES_PACKED, AGQ_CODES_BYTES = 0, 1
 AGQ_OP_QUANTIZE, AGQ_OP_DEQUANTIZE, AGQ_OP_ACCUMULATE, AGQ_OP_ALLREDUCE = range(4)
-AGQ_AR_NCCL, AGQ_AR_FUSED_P2P, AGQ_AR_PUSH_P2P = 0, 1, 2
+AGQ_AR_NCCL, AGQ_AR_FUSED_P2P, AGQ_AR_PUSH_P2P, AGQ_AR_ONESHOT_P2P = 0, 1, 2, 3
 AGQ_MAX_WORLD = 16
 INT64_MAX = (1 << 63) - 1
 

@@ -28,7 +28,13 @@ class _CudaArray:
 
 
 class Communicator:
-    ALGOS = {"nccl": L.AGQ_AR_NCCL, "p2p": L.AGQ_AR_FUSED_P2P, "push": L.AGQ_AR_PUSH_P2P}
+    ALGOS = {"nccl": L.AGQ_AR_NCCL, "p2p": L.AGQ_AR_FUSED_P2P, "push": L.AGQ_AR_PUSH_P2P,
+             "oneshot": L.AGQ_AR_ONESHOT_P2P}
+    ONESHOT_MAX = 1 << 20  # elements: the one-shot inbox (csrc/collective.cu)
+    # auto picks the one-shot algorithm while n * (P - 1) stays below this:
+    # it sends 2 (P - 1) x the decomposed protocol's bytes but skips its
+    # second exchange and both barriers (profiles/r02_oneshot_*.log)
+    ONESHOT_AUTO = 3 << 19
 
     def __init__(self, group=None, device: int | None = None, p2p_capacity: int = 0,
                  timeout_s: float | None = None, nccl: bool = True):
@@ -104,7 +110,11 @@ class Communicator:
         # Depends only on state every rank shares (the collective
         # enable_p2p capacity, and n / block, equal on all ranks), never on
         # where this rank's tensor lives, so all ranks pick the same algorithm.
-        if self.p2p_capacity and q.num_elements() <= self.p2p_capacity and q.block_size == 128:
+        n = q.num_elements()
+        if self.p2p_capacity and n <= self.p2p_capacity and q.block_size == 128:
+            if (n <= self.ONESHOT_MAX and self.world <= 8 and
+                    n * (self.world - 1) <= self.ONESHOT_AUTO):
+                return "oneshot"
             return "p2p"
         if not self.nccl:
             raise L.InvalidArgument("P2P-only communicator: enable_p2p with enough capacity")

@@ -195,6 +195,22 @@ agq_errors none_errors() {
 
 using namespace agqh;
 
+namespace agqh {
+__global__ void k_errors_reset(agq_errors* e, agq_errors none) {
+  if (threadIdx.x == 0) *e = none;
+}
+void launch_errors_reset(agq_errors* e, cudaStream_t s) {
+  static const agq_errors none = none_errors();
+  k_errors_reset<<<1, 32, 0, s>>>(e, none);
+  count_launch();
+}
+}  // namespace agqh
+
+#ifdef AGQ_AR_PROFILE
+namespace agqh {
+agq_status ar_profile(unsigned long long* out);  // collective.cu, experiment builds
+}
+#endif
 extern "C" {
 
 const char* agq_version(void) { return "agoq-b200 0.1 (sm_100a)"; }
@@ -212,10 +228,9 @@ int agq_device_ok(void) {
 
 agq_status agq_errors_reset(agq_errors* d_err, agq_stream_t stream) {
   if (!d_err) return AGQ_OK;
-  static const agq_errors none = none_errors();
-  return cuda_fail(cudaMemcpyAsync(d_err, &none, sizeof(none), cudaMemcpyHostToDevice,
-                                   (cudaStream_t)stream),
-                   "errors_reset");
+  // a kernel, not a pageable-host memcpy: capturable in a CUDA graph
+  agqh::launch_errors_reset(d_err, (cudaStream_t)stream);
+  return cuda_fail(cudaGetLastError(), "errors_reset");
 }
 
 agq_status agq_errors_message(const agq_errors* h, int op, char* msg, size_t msglen) {
@@ -427,6 +442,9 @@ agq_status agq_comm_last_trace(agq_comm* comm, agq_trace_event* events, int cap,
 }
 int agq_comm_size(const agq_comm* comm) { return comm_size(comm); }
 
+#ifdef AGQ_AR_PROFILE
+agq_status agq_ar_profile(unsigned long long* out) { return agqh::ar_profile(out); }
+#endif
 agq_status agq_allreduce_fp8(agq_comm* comm, uint8_t* codes, float* scales, uint64_t n,
                              uint32_t block, int algo, agq_errors* d_err, agq_stream_t stream) {
   if (agq_status st = check_args(8, block, AGQ_CODEC_FP8_E4M3)) return st;

@@ -129,10 +129,13 @@ struct agq_comm {
   unsigned char* peer[AGQ_MAX_WORLD] = {};
   bool p2p_ready = false;
   unsigned int* done_counter = nullptr;  // local, one per kernel in flight
+  // local: the last completed P2P epoch. The kernels read it (+1 = this
+  // call's epoch) and the last CTA of the call stores it, so the epoch lives
+  // on the device and a captured CUDA graph replays correctly.
+  uint64_t* epoch_ctr = nullptr;
   // device: two [elements, blocks] records of the phase-1 traffic, used by
   // alternate epochs; each kernel zeroes the other one for the next call
   unsigned long long* stats = nullptr;
-  uint64_t epoch = 0;
   // message trace of the last all-reduce issued by this rank
   std::vector<agq_trace_event> trace;
   int trace_algo = -1;
@@ -143,6 +146,9 @@ namespace agqk {
 
 __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
   uint64_t v;
@@ -164,12 +170,25 @@ struct FusedArgs {
   unsigned char* base[AGQ_MAX_WORLD];  // symmetric buffer of every rank (self included)
   uint64_t scales_off, codes_off;      // byte offsets inside the buffer
   uint64_t begin, len;                 // my chunk (elements, block aligned)
-  uint64_t epoch, timeout_ns;
+  uint64_t* epoch_ctr;                 // last completed epoch (this rank, local)
+  uint64_t timeout_ns;
   unsigned int* done_counter;
   unsigned long long* stats;           // [elements, blocks] pulled from the peers
   agq_errors* err;
   int rank, P;
 };
+
+#ifdef AGQ_AR_PROFILE
+// experiment builds: globaltimer stamps of the last fused call
+__device__ unsigned long long g_ar_prof[8];
+#define AR_STAMP(i) (g_ar_prof[i] = globaltimer())
+#else
+#define AR_STAMP(i) ((void)0)
+#endif
+
+// This call's epoch: one past the last completed one (stored by the
+// previous call's last CTA, a kernel earlier on this stream).
+__device__ __forceinline__ uint64_t call_epoch(const uint64_t* ctr) { return __ldcg(ctr) + 1; }
 
 // Spin until *f >= epoch. False on timeout or when the communicator has
 // been marked failed (by this rank or a peer).
@@ -193,14 +212,14 @@ __device__ void mark_failed(const Args& a) {
 
 // Start barrier of a P2P epoch (thread 0 of each CTA; CTA 0 announces).
 template <class Args>
-__device__ bool start_barrier(const Args& a, int wait_off, bool skip_self) {
+__device__ bool start_barrier(const Args& a, int wait_off, bool skip_self, uint64_t ep) {
   uint64_t* my_flags = reinterpret_cast<uint64_t*>(a.base[a.rank]);
   // set by an earlier call (a previous kernel): a relaxed load suffices
   if (ld_relaxed_sys(my_flags + kFailOff) != 0) return false;
   bool ok = true;
   for (int s = 0; s < a.P; ++s)
     if (!(skip_self && s == a.rank) &&
-        !wait_flag(my_flags + wait_off + s, a.epoch, my_flags + kFailOff, a.timeout_ns))
+        !wait_flag(my_flags + wait_off + s, ep, my_flags + kFailOff, a.timeout_ns))
       ok = false;
   return ok;
 }
@@ -293,7 +312,7 @@ __device__ __forceinline__ void fused_group(unsigned char* const (&base)[NP], ui
 // cta_stats (shared, or nullptr): this CTA's [elements, blocks] moved per
 // peer, added to the communicator's counters once per CTA.
 template <class Args>
-__device__ __forceinline__ void epoch_end(const Args& a, bool ok,
+__device__ __forceinline__ void epoch_end(const Args& a, uint64_t ep, bool ok,
                                           const unsigned long long* cta_stats = nullptr) {
   unsigned char* const* base = a.base;
   const int P = a.P, rank = a.rank;
@@ -302,29 +321,38 @@ __device__ __forceinline__ void epoch_end(const Args& a, bool ok,
   __syncthreads();
   if (threadIdx.x != 0) return;
   if (cta_stats != nullptr && cta_stats[0] != 0) {  // read from each of the P - 1 peers
-    atomicAdd(&a.stats[2 * (a.epoch & 1)], cta_stats[0] * (a.P - 1));
-    atomicAdd(&a.stats[2 * (a.epoch & 1) + 1], cta_stats[1] * (a.P - 1));
+    atomicAdd(&a.stats[2 * (ep & 1)], cta_stats[0] * (a.P - 1));
+    atomicAdd(&a.stats[2 * (ep & 1) + 1], cta_stats[1] * (a.P - 1));
   }
   const unsigned int prev = atomicAdd(a.done_counter, 1u);
   if (prev != gridDim.x * gridDim.y - 1) return;
+  AR_STAMP(3);
+  // One system fence: it acquires every CTA's writes (each fenced before its
+  // increment, observed through the counter) and this rank's error record,
+  // and orders all of it before the relaxed "done" stores below (a release
+  // per store would cost one system fence per peer: ~2 us each).
   __threadfence_system();
   uint64_t* my_flags = reinterpret_cast<uint64_t*>(base[rank]);
   // a CTA that failed its start barrier recorded -1 (min over the record)
   const long long ov = *reinterpret_cast<volatile long long*>(&err->overflow_block);
   if (ok && ov != -1) {
     const long long bs = *reinterpret_cast<volatile long long*>(&err->bad_scale_block);
-    for (int s = 0; s < P; ++s) {
-      long long* pe = reinterpret_cast<long long*>(base[s]) + kErrOff;
-      if (ov != kNone) atomicMin(pe, ov);
-      if (bs != kNone) atomicMin(pe + 1, bs);
+    if (ov != kNone || bs != kNone) {  // rare: share this rank's data errors before "done"
+      for (int s = 0; s < P; ++s) {
+        long long* pe = reinterpret_cast<long long*>(base[s]) + kErrOff;
+        if (ov != kNone) atomicMin(pe, ov);
+        if (bs != kNone) atomicMin(pe + 1, bs);
+      }
+      __threadfence_system();
     }
-    __threadfence_system();
     for (int s = 0; s < P; ++s)
-      st_release_sys(reinterpret_cast<uint64_t*>(base[s]) + kDoneOff + rank, a.epoch);
+      st_relaxed_sys(reinterpret_cast<uint64_t*>(base[s]) + kDoneOff + rank, ep);
     bool fine = true;
+    AR_STAMP(4);
     for (int s = 0; s < P; ++s)
-      if (!wait_flag(my_flags + kDoneOff + s, a.epoch, my_flags + kFailOff, a.timeout_ns))
+      if (!wait_flag(my_flags + kDoneOff + s, ep, my_flags + kFailOff, a.timeout_ns))
         fine = false;
+    AR_STAMP(5);
     // one 16-byte read and reset of both words (peers enter the next epoch's
     // end only after this kernel: their start barrier needs our next "ready")
     long long e0, e1;
@@ -341,9 +369,11 @@ __device__ __forceinline__ void epoch_end(const Args& a, bool ok,
   }
   __threadfence();
   // the next epoch's traffic record (this one stays readable for last_trace)
-  a.stats[2 * ((a.epoch + 1) & 1)] = 0ull;
-  a.stats[2 * ((a.epoch + 1) & 1) + 1] = 0ull;
-  *a.done_counter = 0u;  // read by the next kernel on this stream
+  a.stats[2 * ((ep + 1) & 1)] = 0ull;
+  a.stats[2 * ((ep + 1) & 1) + 1] = 0ull;
+  *a.epoch_ctr = ep;     // every CTA of this call has read it (they all arrived)
+  AR_STAMP(6);
+  *a.done_counter = 0u;  // both read by the next kernel on this stream
 }
 
 template <int NP>
@@ -355,18 +385,21 @@ __global__ void __launch_bounds__(256, 2) k_fused_allreduce(FusedArgs a) {
   fill_fp8_dq_table(lut);
   float* wtab = btab + (threadIdx.x >> 5) * (NP > 0 ? NP : 1) * 32;
   const int tid = threadIdx.x;
+  if (tid == 0 && blockIdx.x == 0) AR_STAMP(0);
   if (tid < 2) cta_stats[tid] = 0ull;
+  const uint64_t ep = call_epoch(a.epoch_ctr);
   // start barrier: announce "my input is final" to every rank, then wait for
   // every rank's announcement (each CTA waits; only CTA 0 announces).
   if (blockIdx.x == 0 && tid < a.P)
-    st_release_sys(reinterpret_cast<uint64_t*>(a.base[tid]) + kReadyOff + a.rank, a.epoch);
+    st_release_sys(reinterpret_cast<uint64_t*>(a.base[tid]) + kReadyOff + a.rank, ep);
   if (tid == 0) {
-    ok = start_barrier(a, kReadyOff, false) ? 1 : 0;
+    ok = start_barrier(a, kReadyOff, false, ep) ? 1 : 0;
     if (!ok) err_min(&a.err->overflow_block, -1);
   }
   __syncthreads();
+  if (tid == 0 && blockIdx.x == 0) AR_STAMP(1);
   if (!ok) {
-    epoch_end(a, false);
+    epoch_end(a, ep, false);
     return;
   }
 
@@ -418,7 +451,8 @@ __global__ void __launch_bounds__(256, 2) k_fused_allreduce(FusedArgs a) {
     atomicAdd(&cta_stats[0], n_el);
     atomicAdd(&cta_stats[1], n_blk);
   }
-  epoch_end(a, true, cta_stats);
+  if (tid == 0 && blockIdx.x == 0) AR_STAMP(2);
+  epoch_end(a, ep, true, cta_stats);
 }
 
 // ---------------------------------------------------------------------------
@@ -440,7 +474,8 @@ struct PushArgs {
   uint64_t in_scales_off, in_codes_off;        // inbox (P slots, indexed by sender)
   uint64_t slot_scales, slot_codes;            // bytes per inbox slot
   uint64_t rg[2 * AGQ_MAX_WORLD];              // chunk [begin, end) per owner (elements)
-  uint64_t epoch, timeout_ns;
+  uint64_t* epoch_ctr;                         // last completed epoch (this rank, local)
+  uint64_t timeout_ns;
   unsigned int* done_counter;
   unsigned long long* stats;                   // [elements, blocks] scattered (all peers)
   agq_errors* err;
@@ -448,6 +483,7 @@ struct PushArgs {
 };
 
 __global__ void __launch_bounds__(256) k_push_scatter(PushArgs a) {
+  const uint64_t ep = call_epoch(a.epoch_ctr);  // k_push_reduce stores it
   const int q = (a.rank + 1 + (int)blockIdx.y) % a.P;  // staggered peers
   const uint64_t b = a.rg[2 * q], len = a.rg[2 * q + 1] - b;
   const unsigned char* src = a.base[a.rank] + a.codes_off + b;
@@ -484,8 +520,8 @@ __global__ void __launch_bounds__(256) k_push_scatter(PushArgs a) {
     n_blk += __shfl_xor_sync(0xffffffffu, n_blk, o);
   }
   if ((threadIdx.x & 31) == 0 && (n_el | n_blk)) {
-    atomicAdd(&a.stats[2 * (a.epoch & 1)], n_el);
-    atomicAdd(&a.stats[2 * (a.epoch & 1) + 1], n_blk);
+    atomicAdd(&a.stats[2 * (ep & 1)], n_el);
+    atomicAdd(&a.stats[2 * (ep & 1) + 1], n_blk);
   }
   // publish "scattered" once every CTA's stores are performed system-wide
   __threadfence_system();
@@ -496,7 +532,7 @@ __global__ void __launch_bounds__(256) k_push_scatter(PushArgs a) {
       __threadfence_system();
       for (int s = 0; s < a.P; ++s)
         if (s != a.rank)
-          st_release_sys(reinterpret_cast<uint64_t*>(a.base[s]) + kScatteredOff + a.rank, a.epoch);
+          st_release_sys(reinterpret_cast<uint64_t*>(a.base[s]) + kScatteredOff + a.rank, ep);
       *a.done_counter = 0u;
     }
   }
@@ -514,13 +550,14 @@ __global__ void __launch_bounds__(256, 2) k_push_reduce(PushArgs a, PieceTable p
   __shared__ int ok;
   fill_fp8_dq_table(lut);
   const int tid = threadIdx.x;
+  const uint64_t ep = call_epoch(a.epoch_ctr);
   if (tid == 0) {
-    ok = start_barrier(a, kScatteredOff, true) ? 1 : 0;
+    ok = start_barrier(a, kScatteredOff, true, ep) ? 1 : 0;
     if (!ok) err_min(&a.err->overflow_block, -1);
   }
   __syncthreads();
   if (!ok) {
-    epoch_end(a, false);
+    epoch_end(a, ep, false);
     return;
   }
   const uint64_t begin = a.rg[2 * a.rank], len = a.rg[2 * a.rank + 1] - begin;
@@ -532,13 +569,177 @@ __global__ void __launch_bounds__(256, 2) k_push_reduce(PushArgs a, PieceTable p
   float* wtab = NP > 0 ? btab + (tid >> 5) * NP * 32 : nullptr;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + tid; g < gpad; g += stride)
     reduce_group<NP>(pt, g, g < ngroups ? len : 0, (long long)b0, lut, a.err, true, wtab);
-  epoch_end(a, true);
+  epoch_end(a, ep, true);
+}
+
+// ---------------------------------------------------------------------------
+// One-shot all-reduce (AGQ_AR_ONESHOT_P2P), the small-message algorithm: one
+// exchange instead of two and no barrier. Every rank stores its WHOLE
+// gradient into every peer's inbox (slot [me] of the half selected by the
+// epoch's parity), then reduces ALL blocks itself (own gradient + P-1 inbox
+// slots, ascending sender rank): the same per-block arithmetic as the
+// decomposed protocol, so bit-identical results, and every rank sees every
+// data error (no error exchange). A peer can write a half again only two
+// epochs later, after its call in between consumed this rank's data of that
+// epoch, i.e. after this rank finished reading the half.
+// 2(P-1)x the wire bytes of the decomposed protocol: small messages only.
+// ---------------------------------------------------------------------------
+struct OneShotArgs {
+  unsigned char* base[AGQ_MAX_WORLD];
+  uint64_t scales_off, codes_off;  // my gradient in the symmetric buffer
+  uint64_t os_off;                 // inbox region: [parity][sender] slots
+  uint64_t n;
+  uint64_t* epoch_ctr;
+  uint64_t timeout_ns;
+  unsigned int* done_counter;
+  unsigned long long* stats;
+  agq_errors* err;
+  int rank, P;
+};
+
+// One-shot, LL flavour (single kernel, no fence, no flag word): every
+// 4-byte payload word travels with the epoch in the same 8-byte half of a
+// 16-byte store, so a receiver polls the data itself and knows it is this
+// call's as soon as the epoch matches (8-byte stores arrive whole over
+// NVLink). Per group of 16 codes: two 16-byte stores per peer; per block
+// scale: one 8-byte store. Each thread first sends all its groups, then
+// receives and reduces them, so no thread waits on data a later phase of
+// its own peer thread would send.
+struct OneShotLL {
+  uint64_t slot_bytes, codes_bytes;  // per sender slot: [codes LL | scales LL]
+};
+__device__ __forceinline__ void st_ll4(void* p, uint32_t a, uint32_t b, uint32_t f) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %3, %2, %3};" ::"l"(p), "r"(a), "r"(b),
+               "r"(f)
+               : "memory");
+}
+__device__ __forceinline__ void st_ll2(void* p, uint32_t a, uint32_t f) {
+  asm volatile("st.volatile.global.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(a), "r"(f) : "memory");
+}
+__device__ __forceinline__ uint4 ld_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ uint2 ld_v2(const void* p) {
+  uint2 v;
+  asm volatile("ld.volatile.global.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
+  return v;
+}
+
+template <int NP>
+__global__ void __launch_bounds__(256, 2)
+    k_oneshot_ll(OneShotArgs a, OneShotLL ll, const __grid_constant__ PieceTable out) {
+  __shared__ double lut[kDqTable];
+  __shared__ float btab[8 * NP * 32];
+  fill_fp8_dq_table(lut);
+  __syncthreads();
+  const int tid = threadIdx.x, sub = tid & 7;
+  const uint64_t ep = call_epoch(a.epoch_ctr);
+  const uint32_t f = (uint32_t)ep;
+  const uint64_t n = a.n, ngroups = (n + 15) / 16, gpad = (ngroups + 31) / 32 * 32;
+  const uint64_t stride = gridDim.x * (uint64_t)blockDim.x;
+  const uint64_t g0 = blockIdx.x * (uint64_t)blockDim.x + tid;
+  const unsigned char* my_codes = a.base[a.rank] + a.codes_off;
+  const float* my_scales = reinterpret_cast<const float*>(a.base[a.rank] + a.scales_off);
+  auto slot = [&](int dst, int sender) {
+    return a.base[dst] + a.os_off + ((ep & 1) * a.P + sender) * ll.slot_bytes;
+  };
+  auto my_group = [&](uint64_t g) {
+    uint32_t w[4] = {0, 0, 0, 0};
+    const uint64_t e0 = g * 16;
+    if (e0 + 16 <= n) {
+      const uint4 v = *reinterpret_cast<const uint4*>(my_codes + e0);
+      w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+    } else {
+      for (int e = 0; e < 16 && e0 + e < n; ++e) w[e >> 2] |= (uint32_t)my_codes[e0 + e] << (8 * (e & 3));
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  };
+  // 1) send: my groups (and my blocks' scales) to every peer
+  for (uint64_t g = g0; g < ngroups; g += stride) {
+    const uint4 v = my_group(g);
+    const uint64_t blk = g / 8;
+    const bool send_scale = sub == 0;  // group 8b carries block b's scale
+    const uint32_t sc = send_scale ? f2u(my_scales[blk]) : 0u;
+#pragma unroll
+    for (int d = 1; d < NP; ++d) {
+      const int q = (a.rank + d) % NP;
+      unsigned char* sl = slot(q, a.rank);
+      st_ll4(sl + g * 32, v.x, v.y, f);
+      st_ll4(sl + g * 32 + 16, v.z, v.w, f);
+      if (send_scale) st_ll2(sl + ll.codes_bytes + blk * 8, sc, f);
+    }
+  }
+  // 2) receive + reduce (ascending sender rank), result into my gradient
+  const uint64_t* fail = reinterpret_cast<const uint64_t*>(a.base[a.rank]) + kFailOff;
+  bool ok = true;
+  float* wtab = btab + (tid >> 5) * NP * 32;
+  for (uint64_t g = g0; g < gpad; g += stride) {
+    const uint64_t e0 = g * 16, blk = e0 / kBlock;
+    const bool in_range = g < ngroups;
+    const bool blk_exists = blk * kBlock < n;
+    uint4 cv[NP];
+    float sc[NP];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      cv[p] = make_uint4(0, 0, 0, 0);
+      sc[p] = 0.0f;
+      if (p == a.rank) {
+        if (blk_exists) sc[p] = my_scales[blk];
+        if (in_range) cv[p] = my_group(g);
+        continue;
+      }
+      const unsigned char* sl = slot(a.rank, p);
+      const uint64_t t0 = globaltimer();
+      for (uint32_t spin = 0;; ++spin) {
+        bool ready = true;
+        if (blk_exists) {
+          const uint2 s2 = ld_v2(sl + ll.codes_bytes + blk * 8);
+          if (s2.y == f) sc[p] = u2f(s2.x); else ready = false;
+        }
+        if (in_range) {
+          const uint4 lo = ld_v4(sl + g * 32), hi = ld_v4(sl + g * 32 + 16);
+          if (lo.y == f && lo.w == f && hi.y == f && hi.w == f)
+            cv[p] = make_uint4(lo.x, lo.z, hi.x, hi.z);
+          else
+            ready = false;
+        }
+        if (ready) break;
+        if ((spin & 255) == 255 &&
+            (ld_relaxed_sys(fail) != 0 || globaltimer() - t0 > a.timeout_ns)) {
+          ok = false;
+          break;
+        }
+      }
+    }
+    reduce_compute<NP>(out, e0, in_range ? n : 0, in_range && e0 + 16 <= n, cv, sc, 0, lut, a.err,
+                       wtab);
+  }
+  if (!ok) err_min(&a.err->overflow_block, -1);
+  if (g0 == 0) {  // per peer: the whole tensor
+    atomicAdd(&a.stats[2 * (ep & 1)], (unsigned long long)n * (NP - 1));
+    atomicAdd(&a.stats[2 * (ep & 1) + 1], (unsigned long long)((n + kBlock - 1) / kBlock) * (NP - 1));
+  }
+  __syncthreads();
+  if (tid != 0) return;
+  const unsigned int prev = atomicAdd(a.done_counter, 1u);
+  if (prev != gridDim.x - 1) return;
+  __threadfence();
+  if (ld_relaxed_sys(reinterpret_cast<const uint64_t*>(&a.err->overflow_block)) == (uint64_t)-1)
+    mark_failed(a);
+  a.stats[2 * ((ep + 1) & 1)] = 0ull;
+  a.stats[2 * ((ep + 1) & 1) + 1] = 0ull;
+  *a.epoch_ctr = ep;
+  *a.done_counter = 0u;
 }
 
 __global__ void k_init_flags(uint64_t* flags) {
-  const int i = threadIdx.x;
-  if (i < kErrOff) flags[i] = 0;
-  else if (i < kErrOff + 2) flags[i] = (uint64_t)kNone;
+  const int i = threadIdx.x;  // 128 threads: the flag words in use
+  flags[i] = (i == kErrOff || i == kErrOff + 1) ? (uint64_t)kNone : 0;
 }
 
 }  // namespace agqk
@@ -591,8 +792,9 @@ agq_status comm_init(agq_comm** out, const unsigned char id[128], int nranks, in
       return st;
     }
   }
-  e = cudaMalloc(&c->done_counter, 64);
+  e = cudaMalloc(&c->done_counter, 64);  // [0]: CTA counter, [8..15]: epoch
   if (e == cudaSuccess) e = cudaMemset(c->done_counter, 0, 64);
+  c->epoch_ctr = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(c->done_counter) + 8);
   if (e == cudaSuccess) e = cudaMalloc(&c->stats, 4 * sizeof(unsigned long long));
   if (e == cudaSuccess) e = cudaMemset(c->stats, 0, 4 * sizeof(unsigned long long));
   if (e != cudaSuccess) {
@@ -613,8 +815,13 @@ agq_status comm_set_timeout(agq_comm* c, double seconds) {
 // Symmetric buffer: [flags 4 KB | scales | codes | inbox scales | inbox codes],
 // the inbox holding P slots of one chunk each (push algorithm).
 struct SymLayout {
-  uint64_t scales_off, codes_off, in_scales_off, in_codes_off, slot_scales, slot_codes, bytes;
+  uint64_t scales_off, codes_off, in_scales_off, in_codes_off, slot_scales, slot_codes;
+  // one-shot inboxes (LL format): 2 halves x P slots of [codes 32 B per
+  // 16-code group | scales 8 B per block] for up to ll_cap elements
+  uint64_t ll_off, ll_cap, ll_codes_bytes, ll_slot_bytes;
+  uint64_t bytes;
 };
+constexpr uint64_t kOneShotLLMaxElems = 1u << 20;
 SymLayout sym_layout(uint64_t capacity, int P) {
   SymLayout L{};
   const uint64_t nb = (capacity + kBlock - 1) / kBlock;
@@ -625,7 +832,11 @@ SymLayout sym_layout(uint64_t capacity, int P) {
   L.slot_scales = round_up(chunk_blocks * 4, 256);
   L.in_codes_off = L.in_scales_off + (uint64_t)P * L.slot_scales;
   L.slot_codes = round_up(chunk_blocks * kBlock, 256);
-  L.bytes = L.in_codes_off + (uint64_t)P * L.slot_codes;
+  L.ll_off = L.in_codes_off + (uint64_t)P * L.slot_codes;
+  L.ll_cap = std::min<uint64_t>(capacity, kOneShotLLMaxElems);
+  L.ll_codes_bytes = round_up((L.ll_cap + 15) / 16 * 32, 256);
+  L.ll_slot_bytes = L.ll_codes_bytes + round_up((L.ll_cap + kBlock - 1) / kBlock * 8, 256);
+  L.bytes = L.ll_off + 2 * (uint64_t)P * L.ll_slot_bytes;
   return L;
 }
 
@@ -641,6 +852,11 @@ agq_status comm_p2p_export(agq_comm* c, uint64_t capacity, unsigned char handle[
     cudaError_t e = cudaMalloc(&c->sym, bytes);
     if (e != cudaSuccess) return cuda_fail(e, "p2p_export: cudaMalloc");
     c->sym_bytes = bytes;
+    {  // LL inboxes: no stale word may carry a future epoch
+      const SymLayout L = sym_layout(capacity, c->nranks);
+      e = cudaMemset(c->sym + L.ll_off, 0, L.bytes - L.ll_off);
+      if (e != cudaSuccess) return cuda_fail(e, "p2p_export: LL inbox");
+    }
     k_init_flags<<<1, 128>>>(reinterpret_cast<uint64_t*>(c->sym));
     count_launch();
     e = cudaDeviceSynchronize();
@@ -849,7 +1065,7 @@ agq_status allreduce_p2p(agq_comm* c, uint8_t* codes, float* scales, uint64_t n,
   a.codes_off = (uint64_t)(reinterpret_cast<unsigned char*>(sc_codes) - c->sym);
   a.begin = rg[2 * r];
   a.len = rg[2 * r + 1] - rg[2 * r];
-  a.epoch = ++c->epoch;
+  a.epoch_ctr = c->epoch_ctr;
   a.timeout_ns = c->timeout_ns;
   a.done_counter = c->done_counter;
   a.stats = c->stats;
@@ -921,7 +1137,7 @@ agq_status allreduce_push(agq_comm* c, uint8_t* codes, float* scales, uint64_t n
   a.in_codes_off = L.in_codes_off;
   a.slot_scales = L.slot_scales;
   a.slot_codes = L.slot_codes;
-  a.epoch = ++c->epoch;
+  a.epoch_ctr = c->epoch_ctr;
   a.timeout_ns = c->timeout_ns;
   a.done_counter = c->done_counter;
   a.stats = c->stats;
@@ -984,6 +1200,67 @@ agq_status allreduce_push(agq_comm* c, uint8_t* codes, float* scales, uint64_t n
   return AGQ_OK;
 }
 
+agq_status allreduce_oneshot(agq_comm* c, uint8_t* codes, float* scales, uint64_t n,
+                             uint32_t block, agq_errors* err, cudaStream_t s) {
+  if (!c->p2p_ready) return set_error(AGQ_ERR_INVALID_ARGUMENT, "p2p buffers not opened");
+  if (block != (uint32_t)kBlock) return set_error(AGQ_ERR_INVALID_ARGUMENT, "one-shot all-reduce needs block 128");
+  if (!err) return set_error(AGQ_ERR_INVALID_ARGUMENT, "one-shot all-reduce needs an error record");
+  const int P = c->nranks, r = c->rank;
+  if (P > 8) return set_error(AGQ_ERR_INVALID_ARGUMENT, "one-shot all-reduce: world size 1..8");
+  const SymLayout L = sym_layout(c->sym_cap, P);
+  if (n > L.ll_cap)
+    return set_error(AGQ_ERR_INVALID_ARGUMENT, "one-shot all-reduce: more than its inbox (1 Mi elements)");
+  uint8_t* sc_codes = c->sym + L.codes_off;
+  float* sc_scales = reinterpret_cast<float*>(c->sym + L.scales_off);
+  const uint64_t nb = (n + block - 1) / block;
+  const bool inplace = codes == sc_codes && scales == sc_scales;
+  if (!inplace) {
+    cudaMemcpyAsync(sc_codes, codes, n, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(sc_scales, scales, nb * 4, cudaMemcpyDeviceToDevice, s);
+  }
+  OneShotArgs a{};
+  for (int q = 0; q < P; ++q) a.base[q] = c->peer[q];
+  a.scales_off = L.scales_off;
+  a.codes_off = L.codes_off;
+  a.os_off = L.ll_off;
+  a.n = n;
+  a.epoch_ctr = c->epoch_ctr;
+  a.timeout_ns = c->timeout_ns;
+  a.done_counter = c->done_counter;
+  a.stats = c->stats;
+  a.err = err;
+  a.rank = r;
+  a.P = P;
+  OneShotLL ll{L.ll_slot_bytes, L.ll_codes_bytes};
+  PieceTable out{};
+  out.np = P;
+  out.nout = 1;
+  out.out_codes[0] = c->peer[r] + L.codes_off;
+  out.out_scales[0] = reinterpret_cast<float*>(c->peer[r] + L.scales_off);
+  // trace: the whole tensor from this rank to every peer
+  for (int q = 0; q < P; ++q)
+    if (q != r) c->trace.push_back(chunk_event(0, r, q, 0, n, block));
+  uint64_t grid = ((n + 15) / 16 + 255) / 256;
+  grid = std::min<uint64_t>(std::max<uint64_t>(grid, 1), (uint64_t)num_sms() * 2);
+  switch (P) {
+    case 1: k_oneshot_ll<1><<<(int)grid, 256, 0, s>>>(a, ll, out); break;
+    case 2: k_oneshot_ll<2><<<(int)grid, 256, 0, s>>>(a, ll, out); break;
+    case 3: k_oneshot_ll<3><<<(int)grid, 256, 0, s>>>(a, ll, out); break;
+    case 4: k_oneshot_ll<4><<<(int)grid, 256, 0, s>>>(a, ll, out); break;
+    case 5: k_oneshot_ll<5><<<(int)grid, 256, 0, s>>>(a, ll, out); break;
+    case 6: k_oneshot_ll<6><<<(int)grid, 256, 0, s>>>(a, ll, out); break;
+    case 7: k_oneshot_ll<7><<<(int)grid, 256, 0, s>>>(a, ll, out); break;
+    default: k_oneshot_ll<8><<<(int)grid, 256, 0, s>>>(a, ll, out); break;
+  }
+  count_launch();
+  if (agq_status st = cuda_fail(cudaGetLastError(), "one-shot all-reduce: launch")) return st;
+  if (!inplace) {
+    cudaMemcpyAsync(codes, sc_codes, n, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(scales, sc_scales, nb * 4, cudaMemcpyDeviceToDevice, s);
+  }
+  return AGQ_OK;
+}
+
 }  // namespace
 
 agq_status allreduce_fp8(agq_comm* c, uint8_t* codes, float* scales, uint64_t n, uint32_t block,
@@ -999,6 +1276,7 @@ agq_status allreduce_fp8(agq_comm* c, uint8_t* codes, float* scales, uint64_t n,
     const float* ps = scales;
     return reduce_requant_device(1, &pc, &ps, n, block, 1, &codes, &scales, 0, err, s);
   }
+  if (algo == AGQ_AR_ONESHOT_P2P) return allreduce_oneshot(c, codes, scales, n, block, err, s);
   if (algo == AGQ_AR_FUSED_P2P || algo == AGQ_AR_PUSH_P2P) {
     // one rank: the fused kernel (barriers and reduce with itself); the
     // push algorithm has no peer to scatter to
@@ -1010,18 +1288,28 @@ agq_status allreduce_fp8(agq_comm* c, uint8_t* codes, float* scales, uint64_t n,
   return allreduce_nccl(c, codes, scales, n, block, err, s);
 }
 
+#ifdef AGQ_AR_PROFILE
+agq_status ar_profile(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  return cuda_fail(cudaMemcpyFromSymbol(out, g_ar_prof, sizeof(g_ar_prof)), "ar_profile");
+}
+#endif
+
 agq_status comm_last_trace(agq_comm* c, agq_trace_event* events, int cap, int* count,
                            unsigned long long* moved) {
   *count = (int)c->trace.size();
   for (int i = 0; i < (int)c->trace.size() && i < cap; ++i) events[i] = c->trace[i];
   if (moved) {
     moved[0] = moved[1] = 0;
-    if (c->trace_algo == AGQ_AR_FUSED_P2P || c->trace_algo == AGQ_AR_PUSH_P2P) {
+    if (c->trace_algo == AGQ_AR_FUSED_P2P || c->trace_algo == AGQ_AR_PUSH_P2P ||
+        c->trace_algo == AGQ_AR_ONESHOT_P2P) {
       // kernel-side counters of the last P2P call (elements, blocks)
       if (c->trace_stream) cudaStreamSynchronize(c->trace_stream);
-      cudaError_t e = cudaMemcpy(moved, c->stats + 2 * (c->epoch & 1),
-                                 2 * sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost);
+      uint64_t ep = 0;  // the last completed epoch: its counters
+      cudaError_t e = cudaMemcpy(&ep, c->epoch_ctr, sizeof ep, cudaMemcpyDeviceToHost);
+      if (e == cudaSuccess)
+        e = cudaMemcpy(moved, c->stats + 2 * (ep & 1), 2 * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost);
       if (e != cudaSuccess) return cuda_fail(e, "last_trace: counters");
     }
   }

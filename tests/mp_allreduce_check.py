@@ -66,9 +66,9 @@ def main():
     for seed, n, kind in cases:
         g = every_code_grads(world, n // 128, seed) if kind else grads(world, n, seed)
         want_c, want_s = O.allreduce_decomposed([c for c, _ in g], [s for _, s in g])
-        for algo in ("nccl", "p2p", "push", "auto", "auto-copy"):
+        for algo in ("nccl", "p2p", "push", "oneshot", "auto", "auto-copy"):
             c, s = g[rank]
-            if algo in ("p2p", "push", "auto"):
+            if algo in ("p2p", "push", "oneshot", "auto"):
                 pc, ps = comm.p2p_buffers(n)
                 pc.copy_(torch.from_numpy(c))
                 ps.copy_(torch.from_numpy(s))
@@ -86,8 +86,18 @@ def main():
                 print(f"rank {rank}: MISMATCH algo={algo} n={n}", flush=True)
             if algo == "auto-copy":
                 continue
-            # trace of what the real collective issued == the reference's trace
             mine, moved = comm.last_trace()
+            alg = comm._auto_algo(q) if algo == "auto" else algo
+            if alg == "oneshot":  # not the reference protocol: its own messages
+                want_mine = [(q, n) for q in range(world) if q != rank]
+                got_mine = [(e.receiver, e.chunk_len) for e in mine
+                            if e.phase == "all_to_all" and e.sender == rank]
+                nb = (n + 127) // 128
+                if got_mine != want_mine or moved != (n * (world - 1), nb * (world - 1)):
+                    fails += 1
+                    print(f"rank {rank}: ONESHOT TRACE {got_mine} {moved} n={n}", flush=True)
+                continue
+            # trace of what the real collective issued == the reference's trace
             full = comm.gather_trace()
             want_t = A.decomposed_trace(n, 128, world)
             if [tuple(e.__dict__.values()) for e in full] != \
@@ -95,7 +105,6 @@ def main():
                 fails += 1
                 print(f"rank {rank}: TRACE MISMATCH algo={algo} n={n} {full[:3]} vs {want_t[:3]}",
                       flush=True)
-            alg = "p2p" if algo == "auto" else algo
             if alg in ("p2p", "push") and world > 1:
                 # the kernel's own counters of the phase-1 traffic
                 if alg == "p2p":
@@ -155,7 +164,7 @@ def main():
     # every rank (collective.hpp:278-281): block 0 (owned by rank 0) holds
     # 3e38 on every rank, so only rank 0's reduce overflows.
     if world > 1:
-        for algo in ("nccl", "p2p", "push"):
+        for algo in ("nccl", "p2p", "push", "oneshot"):
             n = 8192 * 2
             g = grads(world, n, 99, big_rank=-1)
             c, s = g[rank]
@@ -163,7 +172,7 @@ def main():
             c = c.copy()
             s = s.copy()
             c[:128], s[0] = big_c, big_s[0]
-            if algo in ("p2p", "push"):
+            if algo in ("p2p", "push", "oneshot"):
                 pc, ps = comm.p2p_buffers(n)
                 pc.copy_(torch.from_numpy(c))
                 ps.copy_(torch.from_numpy(s))
@@ -186,12 +195,12 @@ def main():
     nb = (n + 127) // 128
     bad = {min(1, world - 1): [150, 40], world - 1: [7]}
     want_blk = min(bad[min(bad)])
-    for algo in ("nccl", "p2p", "push"):
+    for algo in ("nccl", "p2p", "push", "oneshot"):
         c, s = grads(world, n, 123)[rank]
         s = s.copy()
         for b in bad.get(rank, []):
             s[b % nb] = -1.0
-        if algo in ("p2p", "push"):
+        if algo in ("p2p", "push", "oneshot"):
             pc, ps = comm.p2p_buffers(n)
             pc.copy_(torch.from_numpy(c))
             ps.copy_(torch.from_numpy(s))
@@ -207,6 +216,34 @@ def main():
             if str(e) != f"quantized tensor: bad scale at block {want_blk}":
                 fails += 1
                 print(f"rank {rank}: wrong bad-scale error algo={algo}: {e}", flush=True)
+    # CUDA graphs: the P2P all-reduces captured once and replayed on fresh
+    # inputs, interleaved with eager calls. The epoch lives on the device
+    # (each call's last CTA stores it), so replays stay in step with peers.
+    n = 8192 * 3 + 300
+    for algo in ("p2p", "push", "oneshot") if world > 1 else ("p2p", "oneshot"):
+        pc, ps = comm.p2p_buffers(n)
+        q = A.QuantizedTensor(pc, ps, 8, 128, (n,), A.CodecKind.Fp8E4M3, packed=False)
+        err = A.ErrorRecord(dev)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            comm.allreduce_fp8(q, algo=algo, check=False, errors=err)
+        for it in range(4):
+            g = grads(world, n, 300 + it)
+            want_c, want_s = O.allreduce_decomposed([c for c, _ in g], [s for _, s in g])
+            pc.copy_(torch.from_numpy(g[rank][0]))
+            ps.copy_(torch.from_numpy(g[rank][1]))
+            if it == 2:  # an eager call between replays
+                comm.allreduce_fp8(q, algo=algo)
+            else:
+                graph.replay()
+                torch.cuda.synchronize()
+                err.raise_if_any(A._lib.AGQ_OP_ALLREDUCE)
+            if not (np.array_equal(q.codes.cpu().numpy(), want_c) and
+                    np.array_equal(q.scales.cpu().numpy().view(np.uint32), want_s.view(np.uint32))):
+                fails += 1
+                print(f"rank {rank}: GRAPH MISMATCH algo={algo} it={it}", flush=True)
+        del graph
     # the barrier timeout: the last rank never calls; every other rank's call
     # times out, and the failure is sticky on ALL ranks (later calls fail fast)
     if world > 1:

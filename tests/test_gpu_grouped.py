@@ -31,7 +31,9 @@ def test_stage_store_4_layers_20_tensors_one_call(cuda):
         store = A.StageActivationStore(A.stage_policy(plan, stage))
         n0 = A.launch_count()
         store.store(layers)
-        assert A.launch_count() - n0 == 3  # 20 tensors, one width: launches of 8 segments
+        # 20 tensors, one width: three launches of up to 8 segments, plus the
+        # error-record reset (a kernel, so the call is graph-capturable)
+        assert A.launch_count() - n0 == 3 + 1
         bits = plan.stages[stage - 1].assigned_bits
         back = store.read_all()
         for li, d in enumerate(layers):

@@ -382,16 +382,16 @@ __global__ void __launch_bounds__(256, 2) k_fused_allreduce(FusedArgs a) {
   __shared__ float btab[8 * (NP > 0 ? NP : 1) * 32];  // 8 warps x NP pieces x 32 entries
   __shared__ int ok;
   __shared__ unsigned long long cta_stats[2];
-  fill_fp8_dq_table(lut);
-  float* wtab = btab + (threadIdx.x >> 5) * (NP > 0 ? NP : 1) * 32;
   const int tid = threadIdx.x;
   if (tid == 0 && blockIdx.x == 0) AR_STAMP(0);
-  if (tid < 2) cta_stats[tid] = 0ull;
   const uint64_t ep = call_epoch(a.epoch_ctr);
-  // start barrier: announce "my input is final" to every rank, then wait for
-  // every rank's announcement (each CTA waits; only CTA 0 announces).
+  // start barrier: announce "my input is final" to every rank (CTA 0, before
+  // anything else), then wait for every rank's announcement (each CTA)
   if (blockIdx.x == 0 && tid < a.P)
     st_release_sys(reinterpret_cast<uint64_t*>(a.base[tid]) + kReadyOff + a.rank, ep);
+  fill_fp8_dq_table(lut);
+  float* wtab = btab + (threadIdx.x >> 5) * (NP > 0 ? NP : 1) * 32;
+  if (tid < 2) cta_stats[tid] = 0ull;
   if (tid == 0) {
     ok = start_barrier(a, kReadyOff, false, ep) ? 1 : 0;
     if (!ok) err_min(&a.err->overflow_block, -1);
@@ -635,8 +635,6 @@ __global__ void __launch_bounds__(256, 2)
     k_oneshot_ll(OneShotArgs a, OneShotLL ll, const __grid_constant__ PieceTable out) {
   __shared__ double lut[kDqTable];
   __shared__ float btab[8 * NP * 32];
-  fill_fp8_dq_table(lut);
-  __syncthreads();
   const int tid = threadIdx.x, sub = tid & 7;
   const uint64_t ep = call_epoch(a.epoch_ctr);
   const uint32_t f = (uint32_t)ep;
@@ -674,6 +672,8 @@ __global__ void __launch_bounds__(256, 2)
       if (send_scale) st_ll2(sl + ll.codes_bytes + blk * 8, sc, f);
     }
   }
+  fill_fp8_dq_table(lut);  // (after the sends: they do not need it)
+  __syncthreads();
   // 2) receive + reduce (ascending sender rank), result into my gradient
   const uint64_t* fail = reinterpret_cast<const uint64_t*>(a.base[a.rank]) + kFailOff;
   bool ok = true;

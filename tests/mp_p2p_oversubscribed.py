@@ -43,7 +43,8 @@ def main():
     dev = torch.device("cuda", dev_i)
     cap = 8192 * 5 + 300
     global ALGOS
-    ALGOS = ("p2p", "push") if world <= 8 else ("p2p",)  # the push kernels cover 2..8 ranks
+    # the push and one-shot kernels cover 2..8 ranks
+    ALGOS = ("p2p", "push", "oneshot") if world <= 8 else ("p2p",)
     comm = Communicator(device=dev_i, p2p_capacity=cap, timeout_s=240.0, nccl=False)
     fails = 0
     for seed, n in enumerate([128 * 3, 8192 * 2 + 77, cap]):
@@ -60,6 +61,13 @@ def main():
                     np.array_equal(q.scales.cpu().numpy().view(np.uint32), want_s.view(np.uint32))):
                 fails += 1
                 print(f"rank {rank}: MISMATCH algo={algo} n={n}", flush=True)
+            if algo == "oneshot":  # its own messages: the whole tensor to every peer
+                mine, _ = comm.last_trace()
+                if [(e.receiver, e.chunk_len) for e in mine] != \
+                        [(q, n) for q in range(world) if q != rank]:
+                    fails += 1
+                    print(f"rank {rank}: ONESHOT TRACE n={n}", flush=True)
+                continue
             full = comm.gather_trace()
             want_t = A.decomposed_trace(n, 128, world)
             if [tuple(e.__dict__.values()) for e in full] != \

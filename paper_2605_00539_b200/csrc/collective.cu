@@ -726,6 +726,7 @@ __global__ void __launch_bounds__(256, 2)
   }
   __syncthreads();
   if (tid != 0) return;
+  __threadfence();  // this CTA's error-record updates before its count (release)
   const unsigned int prev = atomicAdd(a.done_counter, 1u);
   if (prev != gridDim.x - 1) return;
   __threadfence();

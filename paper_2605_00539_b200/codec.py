@@ -58,27 +58,47 @@ def _stream(stream) -> int:
 
 
 class ErrorRecord:
-    """Device-resident agq_errors record; `raise_if_any` syncs the stream."""
+    """Device-resident agq_errors record; `raise_if_any` syncs the stream.
+
+    A record read back clean needs no reset before its next use: reset()
+    then skips the reset kernel (the common path of every checked call).
+    Handing out `ptr` (to a kernel) makes its state unknown again."""
 
     def __init__(self, device):
         self.t = torch.empty(C.sizeof(L.AgqErrors), dtype=torch.uint8, device=device)
+        self._clean = False
 
     @property
     def ptr(self) -> int:
+        self._clean = False
         return self.t.data_ptr()
 
     def reset(self, stream=None):
-        L.check(L.lib.agq_errors_reset(self.ptr, _stream(stream)))
+        if not self._clean:
+            L.check(L.lib.agq_errors_reset(self.t.data_ptr(), _stream(stream)))
         return self
 
     def read(self) -> L.AgqErrors:
         raw = bytes(self.t.cpu().numpy().tobytes())
-        return L.AgqErrors.from_buffer_copy(raw)
+        h = L.AgqErrors.from_buffer_copy(raw)
+        self._clean = raw == _CLEAN_RECORD
+        return h
 
     def raise_if_any(self, op: int) -> L.AgqErrors:
         h = self.read()
         L.errors_message(h, op)
         return h
+
+
+def _clean_record() -> bytes:
+    """The bytes agq_errors_reset writes (index fields at INT64_MAX, counters 0)."""
+    h = L.AgqErrors()
+    for name, ctype in L.AgqErrors._fields_:
+        setattr(h, name, 0 if ctype == C.c_ulonglong else (1 << 63) - 1)
+    return bytes(h)
+
+
+_CLEAN_RECORD = _clean_record()
 
 
 def _dtype_code(t: torch.Tensor) -> int:
@@ -97,7 +117,12 @@ def _require_cuda(t: torch.Tensor, what: str):
 
 
 def check_codec_args(bit_width: int, block_size: int, kind: CodecKind) -> None:
-    L.check(L.lib.agq_check_codec_args(int(bit_width), int(block_size), int(kind)))
+    """quantize.hpp:64-74; valid arguments return without a library call,
+    invalid ones raise the library's (the reference's) message."""
+    b, k = int(bit_width), int(kind)
+    if 4 <= b <= 8 and int(block_size) >= 1 and (k == 0 or (k == 1 and b == 4) or (k == 2 and b == 8)):
+        return
+    L.check(L.lib.agq_check_codec_args(b, int(block_size), k))
 
 
 def quantize_blockwise(x: torch.Tensor, bit_width: int, block_size: int = kDefaultBlockSize,
@@ -133,9 +158,9 @@ def validate(q: QuantizedTensor) -> None:
     """quantize.hpp:157-176 (argument/shape part; data checks run on device)."""
     check_codec_args(q.bit_width, q.block_size, q.codec_kind)
     n = q.num_elements()
-    if q.scales.numel() != int(L.lib.agq_num_blocks(n, q.block_size)):
+    if q.scales.numel() != -(-n // q.block_size):  # agq_num_blocks
         raise L.InvalidArgument("quantized tensor: wrong number of scales")
-    expect = int(L.lib.agq_packed_bytes(n, q.bit_width)) if q.packed else n
+    expect = -(-n * q.bit_width // 8) if q.packed else n  # agq_packed_bytes
     if q.codes.numel() != expect:
         raise L.InvalidArgument("quantized tensor: shape/code count mismatch")
 

@@ -138,8 +138,8 @@ def quantize_blockwise(x: torch.Tensor, bit_width: int, block_size: int = kDefau
         n *= d
     if n != x.numel():
         raise L.InvalidArgument("shape does not match element count")
-    nb = int(L.lib.agq_num_blocks(n, block_size))
-    ncode = int(L.lib.agq_packed_bytes(n, bit_width)) if packed else n
+    nb = -(-n // block_size)  # agq_num_blocks
+    ncode = -(-n * bit_width // 8) if packed else n  # agq_packed_bytes
     codes = torch.empty(ncode, dtype=torch.uint8, device=x.device)
     scales = torch.empty(nb, dtype=torch.float32, device=x.device)
     err = errors if errors is not None else (ErrorRecord(x.device) if check else None)

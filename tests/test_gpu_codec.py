@@ -309,3 +309,23 @@ def test_roundtrip_fused_equals_two_calls(cuda, bits):
     want = torch.where(xd == 0, torch.zeros_like(xd),
                        (torch.from_numpy(O.dequantize(c, s, bits)).double() - xd) / xd)
     assert torch.equal(d.cpu(), want)
+
+
+def test_error_record_reset_skipped_after_clean_read(cuda):
+    """A record read back clean is not reset again (one kernel launch saved
+    per checked call); handing out its pointer makes it dirty again."""
+    x = torch.randn(8192, device=cuda)
+    err = A.ErrorRecord(cuda)
+    A.quantize_blockwise(x, 4, errors=err)  # checked call: reset, kernel, clean read
+    assert err._clean
+    n0 = A.launch_count()
+    err.reset()
+    assert A.launch_count() == n0  # skipped
+    _ = err.ptr
+    err.reset()
+    assert A.launch_count() == n0 + 1
+    bad = x.clone()
+    bad[5] = float("nan")
+    with pytest.raises(A.InvalidArgument):
+        A.quantize_blockwise(bad, 4, errors=err)
+    assert not err._clean  # an error was read: the next use resets

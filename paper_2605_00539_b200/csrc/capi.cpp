@@ -811,13 +811,22 @@ struct agq_host_job {
   int op = 0;
   size_t slot = 0;
   std::vector<std::vector<agqh::Part>> outs;  // per chunk
+  // the staging copies and enqueues run on this thread while the caller
+  // builds its result buffers; its status (and message) are read at finish
+  std::thread issuer;
+  agq_status issue_status = AGQ_OK;
+  std::string issue_error;
+  ~agq_host_job() {
+    if (issuer.joinable()) issuer.join();
+  }
 };
 
 namespace agqh {
 namespace {
 
 // Issue all chunks of `op`; on success `job` owns the in-flight work.
-agq_status job_issue(agq_host_job& job, const OpSpec& op) {
+// Staging buffers, events and the error record, on the calling thread.
+agq_status job_prepare(agq_host_job& job, const OpSpec& op) {
   HostPipe& p = *job.lease.p;
   if (agq_status st = p.reserve(op.slot)) return st;
   if (agq_status st = p.reserve_job(op.slot * op.chunks, op.chunks)) return st;
@@ -825,6 +834,13 @@ agq_status job_issue(agq_host_job& job, const OpSpec& op) {
   job.op = op.op;
   job.slot = op.slot;
   job.outs.assign(op.chunks, {});
+  return AGQ_OK;
+}
+
+// Stage every chunk's inputs and enqueue its transfers and kernels (the
+// issuer thread).
+agq_status job_issue(agq_host_job& job, const OpSpec& op) {
+  HostPipe& p = *job.lease.p;
   CopyPool& pool = CopyPool::get();
   for (uint64_t k = 0; k < op.chunks; ++k) {
     const int s = (int)(k % kSlots);  // device slot: reused in stream order
@@ -1001,7 +1017,15 @@ agq_status run_sync(const OpSpec& op, void* out0, void* out1) {
 agq_status run_begin(const OpSpec& op, agq_host_job** job) {
   if (op.slot * op.chunks > kJobStagingCap) return AGQ_OK;
   auto j = std::make_unique<agq_host_job>();
-  if (agq_status st = job_issue(*j, op)) return st;
+  if (agq_status st = job_prepare(*j, op)) return st;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  agq_host_job* jp = j.get();
+  jp->issuer = std::thread([jp, op, dev] {
+    cudaSetDevice(dev);
+    jp->issue_status = job_issue(*jp, op);
+    if (jp->issue_status != AGQ_OK) jp->issue_error = agq_last_error();
+  });
   *job = j.release();
   return AGQ_OK;
 }
@@ -1108,6 +1132,8 @@ agq_status agq_local_accumulate_host_begin(const uint8_t* codes, const float* sc
 agq_status agq_host_job_finish(agq_host_job* job, void* out0, void* out1) {
   if (!job) return AGQ_OK;
   std::unique_ptr<agq_host_job> j(job);
+  if (j->issuer.joinable()) j->issuer.join();  // every chunk staged and enqueued
+  if (j->issue_status != AGQ_OK) return set_error(j->issue_status, j->issue_error.c_str());
   if (!out0) {  // cancelled: drain the work, keep the pipeline consistent
     for (uint64_t k = 0; k < j->outs.size(); ++k) cudaEventSynchronize(j->lease.p->cev[k]);
     return AGQ_OK;

@@ -309,8 +309,9 @@ agq_status agq_local_accumulate_host(const uint8_t* codes, const float* scales,
 /* Split form of the four entries above, for callers that allocate their
  * result buffers after the call starts (the drop-in API value-initialises
  * its result vectors: that host work overlaps the transfers and kernels).
- * *_begin stages the inputs (they must stay valid until finish), enqueues
- * every chunk and returns; *job is NULL when nothing was issued (n == 0, or
+ * *_begin returns at once: a library thread stages the inputs (they must
+ * stay valid and unchanged until finish) and enqueues every chunk; *job is
+ * NULL when nothing was issued (n == 0, or
  * the call's staging exceeds the library's 256 MB job cap — use the
  * synchronous entry then). agq_host_job_finish waits, copies the results to
  * out0 (codes or values) / out1 (scales, or NULL), reports the same errors

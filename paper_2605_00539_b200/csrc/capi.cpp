@@ -1021,11 +1021,15 @@ agq_status run_begin(const OpSpec& op, agq_host_job** job) {
   int dev = 0;
   cudaGetDevice(&dev);
   agq_host_job* jp = j.get();
-  jp->issuer = std::thread([jp, op, dev] {
-    cudaSetDevice(dev);
-    jp->issue_status = job_issue(*jp, op);
-    if (jp->issue_status != AGQ_OK) jp->issue_error = agq_last_error();
-  });
+  try {
+    jp->issuer = std::thread([jp, op, dev] {
+      cudaSetDevice(dev);
+      jp->issue_status = job_issue(*jp, op);
+      if (jp->issue_status != AGQ_OK) jp->issue_error = agq_last_error();
+    });
+  } catch (...) {  // no thread available: issue on the caller's thread
+    if (agq_status st = job_issue(*jp, op)) return st;
+  }
   *job = j.release();
   return AGQ_OK;
 }

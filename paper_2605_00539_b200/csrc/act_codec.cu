@@ -102,7 +102,10 @@ __device__ __forceinline__ void encode_linear_bf16_words(const uint4 (&ch)[4], c
   uint32_t pr[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const f32x2 x = pk2(u2f(wv[k] << 16), u2f(wv[k] & 0xffff0000u));
+    // low half to FP32 with a byte permute (integer ALU) instead of the
+    // shift the compiler issues as IMAD on the FMA pipe the encode keeps
+    // 70% busy (C2 quant +2-3%, profiles/r02_quant_prmt_unpack_ab.log)
+    const f32x2 x = pk2(u2f(__byte_perm(wv[k], 0u, 0x1044)), u2f(wv[k] & 0xffff0000u));
     const f32x2 v = mul2(x, inv2);
     const f32x2 xl = mul2(x, L2);
     const f32x2 r = fma2(v, na2, xl);

@@ -87,7 +87,9 @@ __device__ __noinline__ uint32_t encode_slow(int codec, int bits, float x, float
 template <int PACK, int K>
 __device__ __forceinline__ void put_pair(uint32_t (&words)[PACK], uint32_t p) {
   constexpr int o = 2 * PACK * K, w = o / 32, sh = o % 32;
-  words[w] += p << sh;
+  // funnel shift + add (integer ALU, LEA) rather than an IMAD on the FMA
+  // pipe the encode keeps busy (profiles/r02_quant_alu_pack_ab.log)
+  words[w] += sh ? __funnelshift_l(0u, p, sh) : p;
   if constexpr (sh + 2 * PACK > 32) words[w + 1] += p >> (32 - sh);
 }
 template <int BITS, int PACK, int J = 0>
@@ -112,7 +114,7 @@ __device__ __forceinline__ void encode_linear_bf16_words(const uint4 (&ch)[4], c
     const f32x2 v2 = fma2(r, rcp2, v);
     float lo, hi;
     up2(add2(v2, mg2), lo, hi);
-    pr[k] = (f2u(hi) << PACK) + f2u(lo) + kPairOff;
+    pr[k] = __funnelshift_l(0u, f2u(hi), PACK) + f2u(lo) + kPairOff;
   }
   put_pair<PACK, 4 * J + 0>(words, pr[0]);
   put_pair<PACK, 4 * J + 1>(words, pr[1]);

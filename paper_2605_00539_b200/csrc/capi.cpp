@@ -803,6 +803,7 @@ agq_status run_pipeline(HostPipe& p, const OpSpec& op, char* const* outs_base) {
 // transfers and kernels enqueued; the outputs wait in pinned staging until
 // agq_host_job_finish copies them to the caller. Holds its pipeline.
 constexpr size_t kJobStagingCap = 256u << 20;  // larger calls run synchronously
+constexpr size_t kJobAsyncMin = 1u << 20;      // smaller calls stage on the caller's thread
 }  // namespace
 }  // namespace agqh
 
@@ -1021,6 +1022,11 @@ agq_status run_begin(const OpSpec& op, agq_host_job** job) {
   int dev = 0;
   cudaGetDevice(&dev);
   agq_host_job* jp = j.get();
+  if (op.slot * op.chunks < kJobAsyncMin) {  // small call: a thread costs more than it hides
+    if (agq_status st = job_issue(*jp, op)) return st;
+    *job = j.release();
+    return AGQ_OK;
+  }
   try {
     jp->issuer = std::thread([jp, op, dev] {
       cudaSetDevice(dev);

@@ -17,6 +17,12 @@
 // AGQ_AR_PUSH_P2P (v3): the same decomposition with every NVLink transfer a
 //   store: scatter chunk q into rank q's inbox, then reduce from local memory
 //   and store the result into every rank's buffer.
+// AGQ_AR_ONESHOT_P2P (v4, small messages): every rank stores its whole
+//   gradient into every peer's double-buffered inbox with LL stores (payload
+//   word + epoch in each 8-byte half) and reduces all blocks itself; no fence,
+//   no barrier (k_oneshot_ll).
+// The epoch of the P2P algorithms lives on the device (each call reads it
+//   and its last CTA stores it), so captured CUDA graphs replay correctly.
 //
 // Failure handling: a timed-out barrier (a peer that never arrived) records
 // overflow_block = -1 (agq_errors_message: "peer did not arrive") and marks

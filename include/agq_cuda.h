@@ -270,7 +270,11 @@ agq_status agq_comm_last_trace(agq_comm* comm, agq_trace_event* events, int cap,
  * its whole gradient into every peer's inbox and reduces all blocks locally;
  * one exchange, no end barrier, (P-1)x the wire bytes). All four give
  * bit-identical results. The P2P algorithms keep their epoch on the device
- * and allocate nothing per call, so they can be captured in a CUDA graph. */
+ * and allocate nothing per call, so they can be captured in a CUDA graph.
+ * Collective contract: every rank issues the same sequence of P2P calls on
+ * a communicator (same n, block, algorithm), each rank on one stream; the
+ * calls of one rank must not run concurrently (they share the symmetric
+ * buffer, its inboxes and the epoch). */
 agq_status agq_allreduce_fp8(agq_comm* comm, uint8_t* codes, float* scales,
                              uint64_t n, uint32_t block, int algo,
                              agq_errors* d_err, agq_stream_t stream);

@@ -204,3 +204,27 @@ def test_fill_input_is_the_reference_rng():
     assert (c == 2.5).all()
     with pytest.raises(A.InvalidArgument, match="a <= b"):
         materialize(10, 0, "uniform", 1.0, 0.0)
+
+
+def test_host_copy_concurrent_callers():
+    """Several threads using the copy pool at once (the host jobs' issuer
+    threads and other pipelines do): every batch completes, byte for byte."""
+    import threading
+    rng = np.random.default_rng(7)
+    srcs = [rng.integers(0, 256, (3 << 20) + 17 * i, dtype=np.uint8) for i in range(6)]
+    dsts = [np.zeros_like(s) for s in srcs]
+    errs = []
+
+    def run(i):
+        for _ in range(5):
+            if L.lib.agq_host_copy(dsts[i].ctypes.data, srcs[i].ctypes.data, srcs[i].nbytes) != 0:
+                errs.append(i)
+
+    ts = [threading.Thread(target=run, args=(i,)) for i in range(len(srcs))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs
+    for s, d in zip(srcs, dsts):
+        assert np.array_equal(s, d)
